@@ -1,0 +1,152 @@
+/*
+ * dses_b200.h -- C ABI of the B200-native DSES (Direct Semi-Exhaustive Search)
+ * registration hot path.  No torch or CUDA types appear in these signatures:
+ * pointers are plain host pointers unless a name ends in `_dev`, sizes are
+ * int64, the CUDA stream is passed as `void*` (a cudaStream_t; NULL = the
+ * legacy default stream).
+ *
+ * Reference interfaces replaced (reference = gridreg 0.1.0 under
+ * /root/reference/pkg/src/gridreg):
+ *
+ *   dses_mode_dense_batch  <- _kernels.mode_dense_batch   (_kernels.py:173-193)
+ *                             (and mode_sparse_batch, _kernels.py:277-294:
+ *                             same outputs for any lattice size)
+ *   dses_refine_batch      <- _kernels.refine_batch       (_kernels.py:297-324)
+ *   dses_alignment_error   <- _kernels.alignment_error_kernel (_kernels.py:83-89)
+ *                             applied after RigidTransform.apply (metrics.py:133-140)
+ *   dses_plan_* + dses_search / dses_stage_*
+ *                          <- engines.dses                (engines.py:229-301),
+ *                             split into the stages a multi-GPU caller needs
+ *                             between its collectives.
+ *
+ * Every function returns 0 on success or a negative DSES_E* code; the text of
+ * the last error on the calling thread is available from dses_last_error().
+ * Validation that the reference performs in Python (shapes, finiteness, grid
+ * extent, caps) stays in the Python host layer, which raises the reference's
+ * exception types; this layer only rejects what would be undefined behaviour.
+ */
+#ifndef DSES_B200_H
+#define DSES_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSES_OK 0
+#define DSES_E_INVALID -1   /* bad argument (would be InvalidInputError upstream) */
+#define DSES_E_CUDA -2      /* CUDA runtime / launch failure */
+#define DSES_E_NOMEM -3     /* device or host allocation failed */
+#define DSES_E_NODEVICE -4  /* no CUDA device / the sm_100a image cannot run here */
+
+/* Metric codes follow _kernels.py:15-16 (METRIC_*), plus code 4 (extension). */
+#define DSES_METRIC_L2 0
+#define DSES_METRIC_L1 1
+#define DSES_METRIC_TRUNC_L1 2
+#define DSES_METRIC_SAT_L0 3
+#define DSES_METRIC_TRUNC_L2 4 /* extension; not in the reference */
+
+typedef struct dses_plan dses_plan; /* opaque: one (source, reference, lattice) problem on one GPU */
+
+/* Rotation source: the lexicographic Euler grid of geometry.py:253-290 given by
+ * its per-axis cos/sin tables (index a in [0, 2k] <-> angle (a - k) * step,
+ * computed by the caller exactly as geometry.py:272-275 does), optionally
+ * left-multiplied by a centre rotation (engines.py:122-126). */
+typedef struct {
+  int64_t k;              /* half width; (2k+1)^3 rotations */
+  const double* cos_tab;  /* host, 2k+1 values */
+  const double* sin_tab;  /* host, 2k+1 values */
+  const double* center;   /* host, 9 values row-major, or NULL */
+} dses_grid;
+
+/* Outcome of one search (or one rank's share of it). */
+typedef struct {
+  int64_t candidates_evaluated; /* rotations with an in-window vote (engines.py:254,293) */
+  int64_t candidates_refined;   /* n_score (engines.py:270,294); 0 on the sat_l0 shortcut */
+  int64_t mstar;                /* best vote count M* */
+  int64_t winner_row;           /* flat rotation index of the winner (lexicographic grid order) */
+  int64_t winner_lin;           /* flat translation-bin index of the winner's mode */
+  int64_t winner_count;         /* its vote count */
+  double best_error;            /* metric error of the winner (refine_batch op order) */
+  int64_t best_inliers;         /* count_inliers at trans_bin (metrics.py:143-150) */
+  int64_t rescored;             /* candidates re-scored in exact fp64 */
+  /* kernel statistics */
+  int64_t pairs_evaluated;      /* (rotation, i, j) pairs the vote kernel tested */
+  int64_t votes;                /* deduplicated in-window votes (histogram increments) */
+  int64_t rechecks;             /* pairs re-binned in fp64 (fixed-point guard band) */
+  double ms_vote, ms_select, ms_score, ms_total; /* device time per stage (CUDA events) */
+} dses_result;
+
+const char* dses_last_error(void);
+int dses_device_count(int* out);
+const char* dses_build_info(void);
+
+/* ---- plan lifecycle ----------------------------------------------------- */
+/* x: source (n,3) row-major f64; y: reference (m,3).  bin_size = trans_bin;
+ * ilo/dims: inclusive lower bin index and bin counts of the translation
+ * window (engines.py:248-250).  Copies x, y to `device`. */
+int dses_plan_create(int device, const double* x, int64_t n, const double* y, int64_t m,
+                     double bin_size, const int64_t ilo[3], const int64_t dims[3],
+                     dses_plan** out);
+int dses_plan_destroy(dses_plan* plan);
+/* Fixed-point fraction bits chosen for the vote kernel (0 = exact fp64 mode). */
+int dses_plan_info(const dses_plan* plan, int64_t* frac_bits, int64_t* x_tiles, int64_t* y_tiles,
+                   int64_t* near_pairs);
+
+/* ---- the reference kernel seams ------------------------------------------ */
+/* Per-rotation histogram mode (count, flat bin, tied bins) for `nrot`
+ * rotations given explicitly (rots: host (nrot,3,3) f64) -- _kernels.py:173. */
+int dses_mode_batch(dses_plan* plan, const double* rots, int64_t nrot, int64_t* counts,
+                    int64_t* lins, int64_t* ties, void* stream);
+/* Same for rotations [r_begin, r_begin + nrot) of an Euler grid. */
+int dses_mode_grid(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t nrot,
+                   int64_t* counts, int64_t* lins, int64_t* ties, void* stream);
+/* Exact fp64 alignment error of `ncand` poses (rots (c,3,3), ts (c,3)) in
+ * refine_batch's operation order -- _kernels.py:297-324. */
+int dses_refine_batch(dses_plan* plan, const double* rots, const double* ts, int64_t ncand,
+                      int metric_code, double param, double* out, void* stream);
+/* Stand-alone mode_dense_batch with the reference's exact signature meaning
+ * (creates and destroys a transient plan on `device`). */
+int dses_mode_dense_batch(int device, const double* rots, int64_t nrot, const double* x, int64_t n,
+                          const double* y, int64_t m, double bin_size, const int64_t ilo[3],
+                          const int64_t dims[3], int64_t* counts, int64_t* lins, int64_t* ties);
+
+/* ---- the full search ---------------------------------------------------- */
+/* engines.dses phases 1-3 on one GPU over rotations [r_begin, r_begin+r_count)
+ * of `grid` (r_count < 0: the whole grid). */
+int dses_search(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t r_count, double q,
+                int metric_code, double metric_param, int skip_refine, dses_result* out,
+                void* stream);
+
+/* ---- stages for a sharded (multi-GPU) search ----------------------------- */
+/* Stage 1: vote over this rank's rotation slice; returns local M* and the
+ * local count of rotations with an in-window vote. */
+int dses_stage_vote(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t r_count,
+                    int64_t* mstar_local, int64_t* valid_local, void* stream);
+/* Stage 2 (shortcut path): smallest local row whose count equals the global
+ * M* (INT64_MAX when none). */
+int dses_stage_argmax(dses_plan* plan, int64_t mstar_global, int64_t* row_local, void* stream);
+/* Stage 2: keep local rows with count >= q*M*_global - 1e-9 (engines.py:196-201),
+ * screen them in fp32; returns the local kept count and the local fp32 minimum
+ * (+inf when none) and the screen tolerance (absolute). */
+int dses_stage_screen(dses_plan* plan, double q, int64_t mstar_global, int metric_code,
+                      double metric_param, int64_t* kept_local, double* min32_local,
+                      double* tol, void* stream);
+/* Stage 3: exact fp64 re-score of local kept rows with screen error <=
+ * threshold; returns the local (error, row) minimum (error +inf when none). */
+int dses_stage_rescore(dses_plan* plan, double threshold, int metric_code, double metric_param,
+                       double* err_local, int64_t* row_local, int64_t* rescored, void* stream);
+/* Translation-bin index (flat) of a local row's mode. */
+int dses_stage_row_info(dses_plan* plan, int64_t row, int64_t* lin, int64_t* count, void* stream);
+/* Exact fp64 error of one pose (grid row + translation bin) under a metric --
+ * metrics.alignment_error with refine_batch's operation order. */
+int dses_pose_error(dses_plan* plan, const dses_grid* grid, int64_t row, int64_t lin,
+                    int metric_code, double metric_param, double* err, void* stream);
+/* Kernel statistics accumulated since the last call (pairs, votes, rechecks). */
+int dses_stage_stats(dses_plan* plan, int64_t* pairs, int64_t* votes, int64_t* rechecks);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSES_B200_H */

@@ -1,0 +1,837 @@
+// dses_capi.cu -- host runtime and C ABI (include/dses_b200.h) of the B200 DSES path.
+//
+// The host side of a registration is native: plan construction (validation of
+// what the kernels rely on, fixed-point scaling, spatial tiling of both clouds,
+// dedup near lists, device uploads), stage orchestration with CUDA events, and
+// the small host<->device scalar traffic between stages.  The Python layer
+// (paper_2502_00115_b200/engines.py) mirrors gridreg's API and exceptions on top.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/dses_b200.h"
+#include "dses_common.cuh"
+
+#ifndef DSES_NVCC_VERSION
+#define DSES_NVCC_VERSION "unknown"
+#endif
+
+namespace dses {
+// dses_vote.cu
+cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, int threads,
+                        cudaStream_t stream);
+int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int threads);
+size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem);
+// dses_score.cu
+cudaError_t launch_select_stats(const int* counts, int64_t nrot, unsigned long long* mstar,
+                                unsigned long long* nvalid, int sms, cudaStream_t st);
+cudaError_t launch_argmax(const int* counts, int64_t nrot, int64_t r_begin, int mstar,
+                          unsigned long long* row, int sms, cudaStream_t st);
+cudaError_t launch_compact(const int* counts, const int* lins, int64_t nrot, int64_t r_begin,
+                           double cutoff, int64_t* rows, int* cl, unsigned long long* ncand, int sms,
+                           cudaStream_t st);
+cudaError_t launch_screen(const ScoreParams& s, const int64_t* rows, const int* lins, int64_t ncand,
+                          double* partial, double* err, unsigned long long* minbits, cudaStream_t st);
+cudaError_t launch_rescore_compact(const double* err, int64_t ncand, double thr, int* sel,
+                                   unsigned long long* nsel, cudaStream_t st);
+cudaError_t launch_exact(const ScoreParams& s, const int64_t* rows, const int* lins, const int* sel,
+                         int64_t nsel, double* vals, double* out, cudaStream_t st);
+cudaError_t launch_winner(const double* err64, const int* sel, const int64_t* rows, int64_t nsel,
+                          double* best_err, int64_t* best_row, int* best_c, cudaStream_t st);
+int screen_threads();
+int exact_threads();
+}  // namespace dses
+
+using namespace dses;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? DSES_E_NOMEM : DSES_E_CUDA,           \
+                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+extern "C" const char* dses_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char* dses_build_info(void) {
+  return "dses_b200: sm_100a, nvcc " DSES_NVCC_VERSION ", fixed-point vote + fp32 screen + fp64 exact";
+}
+
+extern "C" int dses_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) { *out = 0; return fail(DSES_E_NODEVICE, "%s", cudaGetErrorString(e)); }
+  *out = n;
+  return DSES_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device buffers
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+template <class T>
+static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
+  cudaError_t e = b.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
+  if (e != cudaSuccess || v.empty()) return e;
+  return cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st);
+}
+
+// ---------------------------------------------------------------------------
+// the plan
+// ---------------------------------------------------------------------------
+struct dses_plan {
+  int device = 0, sms = 0;
+  size_t smem_optin = 0;
+  int64_t n = 0, m = 0;
+  double bin = 0, inv_bin = 0;
+  int64_t ilo[3] = {0, 0, 0}, dims[3] = {1, 1, 1};
+  int F = 0;
+  int64_t near_pairs = 0;
+  double bx = 0, by = 0;             // max |p| bound (|x|_2 + |t|) and max |y| (screen error bound)
+  VoteParams vp{};
+  bool hsmem = true, psmem = true;
+  int vote_grid = 0, vote_threads = kVoteThreads;
+  // device data
+  DevBuf xs, ys, yq, near_off, near_idx, xt, yt;       // vote (tile order)
+  DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
+  DevBuf cth, sth, rots;                               // rotation sources
+  DevBuf counts, lins, ties;                           // per-rotation outputs
+  DevBuf hist_g, p_g;                                  // global fallbacks
+  DevBuf stats, scal;                                  // counters / scalar outputs
+  DevBuf cand_rows, cand_lins, err32, partial, sel, vals, err64;
+  DevBuf win_err, win_row, win_c, tmp_rows, tmp_lins, tvec;
+  // stage state
+  int64_t cur_r_begin = 0, cur_r_count = 0, cur_k = 0;
+  RotSource cur_rot{};
+  int64_t kept = 0;
+  cudaEvent_t ev[8];
+};
+
+namespace {
+
+// round-half-away-from-zero integer of v (host side fixed-point conversion)
+inline int64_t rint64(double v) { return (int64_t)std::llrint(v); }
+
+// recursive median split until tiles hold <= kTile points; splits at a
+// multiple of kTile so that all but the last tile of each branch are full.
+void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
+              std::vector<std::pair<int, int>>& tiles) {
+  const int64_t cnt = hi - lo;
+  if (cnt <= kTile) {
+    if (cnt > 0) tiles.emplace_back((int)lo, (int)cnt);
+    return;
+  }
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t q = lo; q < hi; ++q)
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = std::min(mn[k], pts[3 * perm[q] + k]);
+      mx[k] = std::max(mx[k], pts[3 * perm[q] + k]);
+    }
+  int axis = 0;
+  for (int k = 1; k < 3; ++k)
+    if (mx[k] - mn[k] > mx[axis] - mn[axis]) axis = k;
+  const int64_t ntile = (cnt + kTile - 1) / kTile;
+  const int64_t left = (ntile / 2) * kTile;
+  std::nth_element(perm.begin() + lo, perm.begin() + lo + left, perm.begin() + hi,
+                   [&](int a, int b) {
+                     const double va = pts[3 * a + axis], vb = pts[3 * b + axis];
+                     return va < vb || (va == vb && a < b);
+                   });
+  kd_tiles(pts, lo, lo + left, perm, tiles);
+  kd_tiles(pts, lo + left, hi, perm, tiles);
+}
+
+int build_plan(dses_plan* P, const double* x, const double* y) {
+  const int64_t n = P->n, m = P->m;
+  cudaStream_t st = 0;
+  // ---- fixed-point scale
+  double ymax = 0, xnorm = 0;
+  for (int64_t j = 0; j < m; ++j)
+    for (int k = 0; k < 3; ++k) ymax = std::max(ymax, std::fabs(y[3 * j + k]));
+  for (int64_t i = 0; i < n; ++i)
+    xnorm = std::max(xnorm, std::sqrt(x[3 * i] * x[3 * i] + x[3 * i + 1] * x[3 * i + 1] +
+                                      x[3 * i + 2] * x[3 * i + 2]));
+  double lomax = 0;
+  for (int k = 0; k < 3; ++k)
+    lomax = std::max(lomax, std::max(std::fabs((double)P->ilo[k]),
+                                     std::fabs((double)(P->ilo[k] + P->dims[k]))));
+  const double A = ymax * P->inv_bin + 3.0 * xnorm * P->inv_bin + lomax + 8.0;
+  int F = 0;
+  if (std::isfinite(A) && A > 0) F = (int)std::floor(std::log2(std::ldexp(1.0, 29) / A));
+  F = std::min(F, 20);
+  if (F < 6) F = 0;  // exact mode: every pair re-binned in binary64
+  P->F = F;
+  const double S = std::ldexp(1.0, F);
+  P->by = ymax;
+  double tmax = 0;
+  for (int k = 0; k < 3; ++k)
+    tmax = std::max(tmax, (std::fabs((double)P->ilo[k]) + (double)P->dims[k]) * P->bin);
+  P->bx = xnorm + tmax;
+
+  // ---- spatial tiles
+  std::vector<int> px(n), py(m);
+  std::iota(px.begin(), px.end(), 0);
+  std::iota(py.begin(), py.end(), 0);
+  std::vector<std::pair<int, int>> tx, ty;
+  kd_tiles(x, 0, n, px, tx);
+  kd_tiles(y, 0, m, py, ty);
+  std::vector<double> xs(3 * n), ys(3 * m);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
+  for (int64_t j = 0; j < m; ++j)
+    for (int k = 0; k < 3; ++k) ys[3 * j + k] = y[3 * py[j] + k];
+  const double inv_s = P->inv_bin * S;
+  std::vector<XTile> xt(tx.size());
+  for (size_t t = 0; t < tx.size(); ++t) {
+    XTile& T = xt[t];
+    T.start = tx[t].first;
+    T.count = tx[t].second;
+    T.pad = 0;
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int q = T.start; q < T.start + T.count; ++q)
+      for (int k = 0; k < 3; ++k) {
+        mn[k] = std::min(mn[k], xs[3 * q + k]);
+        mx[k] = std::max(mx[k], xs[3 * q + k]);
+      }
+    for (int k = 0; k < 3; ++k) T.c[k] = 0.5 * (mn[k] + mx[k]);
+    double rad = 0;
+    for (int q = T.start; q < T.start + T.count; ++q) {
+      double d2 = 0;
+      for (int k = 0; k < 3; ++k) d2 += (xs[3 * q + k] - T.c[k]) * (xs[3 * q + k] - T.c[k]);
+      rad = std::max(rad, std::sqrt(d2));
+    }
+    T.rad = F ? (int)std::ceil(rad * inv_s * (1.0 + 1e-9)) + 3 : 0;
+  }
+  // fixed-point reference: Yq = rint(fl(y*inv)*S) - lo*S + S/2 + G
+  std::vector<int4> yq(m);
+  const int64_t Si = (int64_t)1 << F;
+  for (int64_t j = 0; j < m; ++j) {
+    int v[3];
+    for (int k = 0; k < 3; ++k) {
+      int64_t q = F ? rint64((ys[3 * j + k] * P->inv_bin) * S) - P->ilo[k] * Si + Si / 2 + kGuard : 0;
+      if (q > (1ll << 30) || q < -(1ll << 30)) {
+        return fail(DSES_E_INVALID, "internal: fixed-point overflow (F=%d)", F);
+      }
+      v[k] = (int)q;
+    }
+    yq[j] = make_int4(v[0], v[1], v[2], 0);
+  }
+  std::vector<YTile> yt(ty.size());
+  for (size_t t = 0; t < ty.size(); ++t) {
+    YTile& T = yt[t];
+    T.start = ty[t].first;
+    T.count = ty[t].second;
+    for (int k = 0; k < 3; ++k) { T.lo[k] = INT32_MAX; T.hi[k] = INT32_MIN; }
+    for (int q = T.start; q < T.start + T.count; ++q) {
+      const int v[3] = {yq[q].x, yq[q].y, yq[q].z};
+      for (int k = 0; k < 3; ++k) { T.lo[k] = std::min(T.lo[k], v[k]); T.hi[k] = std::max(T.hi[k], v[k]); }
+    }
+  }
+  // ---- dedup near lists (tile order): j' < j with |y_j - y_j'|_inf < bin (1 + 1e-6)
+  const double thr = P->bin * (1.0 + 1e-6);
+  std::vector<int> o0(m);
+  std::iota(o0.begin(), o0.end(), 0);
+  std::sort(o0.begin(), o0.end(), [&](int a, int b) {
+    return ys[3 * a] < ys[3 * b] || (ys[3 * a] == ys[3 * b] && a < b);
+  });
+  std::vector<std::vector<int>> nl(m);
+  int64_t npairs = 0;
+  for (int64_t a = 0; a < m; ++a) {
+    const int ja = o0[a];
+    for (int64_t b = a + 1; b < m; ++b) {
+      const int jb = o0[b];
+      if (ys[3 * jb] - ys[3 * ja] >= thr) break;
+      if (std::fabs(ys[3 * jb + 1] - ys[3 * ja + 1]) < thr &&
+          std::fabs(ys[3 * jb + 2] - ys[3 * ja + 2]) < thr) {
+        if (ja < jb) nl[jb].push_back(ja); else nl[ja].push_back(jb);
+        ++npairs;
+      }
+    }
+  }
+  std::vector<int> noff(m + 1, 0), nidx;
+  nidx.reserve((size_t)npairs);
+  for (int64_t j = 0; j < m; ++j) {
+    std::sort(nl[j].begin(), nl[j].end());
+    noff[j] = (int)nidx.size();
+    nidx.insert(nidx.end(), nl[j].begin(), nl[j].end());
+  }
+  noff[m] = (int)nidx.size();
+  P->near_pairs = npairs;
+  // ---- scoring layout: x original order, y sorted by axis 0 (stable)
+  std::vector<int> sy(m);
+  std::iota(sy.begin(), sy.end(), 0);
+  std::stable_sort(sy.begin(), sy.end(), [&](int a, int b) { return y[3 * a] < y[3 * b]; });
+  std::vector<double> c0(m), c1(m), c2(m);
+  std::vector<float4> yf(m);
+  for (int64_t j = 0; j < m; ++j) {
+    c0[j] = y[3 * sy[j]];
+    c1[j] = y[3 * sy[j] + 1];
+    c2[j] = y[3 * sy[j] + 2];
+    yf[j] = make_float4((float)c0[j], (float)c1[j], (float)c2[j], 0.f);
+  }
+  std::vector<double> xv(x, x + 3 * n);
+  // ---- uploads
+  CK(upload(P->xs, xs, st));
+  CK(upload(P->ys, ys, st));
+  CK(upload(P->yq, yq, st));
+  CK(upload(P->near_off, noff, st));
+  if (nidx.empty()) nidx.push_back(0);
+  CK(upload(P->near_idx, nidx, st));
+  CK(upload(P->xt, xt, st));
+  CK(upload(P->yt, yt, st));
+  CK(upload(P->x0, xv, st));
+  CK(upload(P->ys0, c0, st));
+  CK(upload(P->ys1, c1, st));
+  CK(upload(P->ys2, c2, st));
+  CK(upload(P->ysf, yf, st));
+  CK(P->stats.ensure(4 * sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(P->stats.p, 0, 4 * sizeof(unsigned long long), st));
+  CK(P->scal.ensure(64));
+  CK(cudaStreamSynchronize(st));
+
+  // ---- vote kernel parameters
+  VoteParams& v = P->vp;
+  v.d0 = (int)P->dims[0]; v.d1 = (int)P->dims[1]; v.d2 = (int)P->dims[2];
+  v.nbins = v.d0 * v.d1 * v.d2;
+  v.F = F;
+  v.fmask = F ? (unsigned)(Si - 1) : 0u;
+  v.D0 = (unsigned)(P->dims[0] * Si); v.D1 = (unsigned)(P->dims[1] * Si); v.D2 = (unsigned)(P->dims[2] * Si);
+  v.W0 = v.D0 + 2 * kGuard; v.W1 = v.D1 + 2 * kGuard; v.W2 = v.D2 + 2 * kGuard;
+  if (!F) { v.W0 = v.W1 = v.W2 = 0xffffffffu; }
+  v.inv_bin = P->inv_bin;
+  v.inv_s = inv_s;
+  v.flo0 = (double)P->ilo[0]; v.flo1 = (double)P->ilo[1]; v.flo2 = (double)P->ilo[2];
+  v.fd0 = (double)P->dims[0]; v.fd1 = (double)P->dims[1]; v.fd2 = (double)P->dims[2];
+  v.n = (int)n; v.m = (int)m;
+  v.nxt = (int)xt.size(); v.nyt = (int)yt.size();
+  v.xs = P->xs.as<double>(); v.ys = P->ys.as<double>(); v.yq = P->yq.as<int4>();
+  v.near_off = P->near_off.as<int>(); v.near_idx = P->near_idx.as<int>();
+  v.xt = P->xt.as<XTile>(); v.yt = P->yt.as<YTile>();
+  v.stats = P->stats.as<unsigned long long>();
+  v.count16 = n < 65536 ? 1 : 0;
+  const int64_t words = v.count16 ? (v.nbins + 1) / 2 : v.nbins;
+  v.hist_words = (int)((words + 3) / 4 * 4);
+  v.n_pad = (int)((n + 3) / 4 * 4);
+  // shared-memory placement
+  const size_t fixed = vote_smem_bytes(v, false, false);
+  const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)n * 16;
+  const size_t lim = P->smem_optin;
+  P->hsmem = v.count16 && fixed + hb <= lim;
+  P->psmem = fixed + pb + (P->hsmem ? hb : 0) <= lim;
+  if (!P->hsmem && !P->psmem && fixed + pb <= lim) P->psmem = true;
+  int per_sm = vote_max_ctas_per_sm(v, P->hsmem, P->psmem, P->vote_threads);
+  if (per_sm < 1) {
+    P->vote_threads = 512;
+    per_sm = vote_max_ctas_per_sm(v, P->hsmem, P->psmem, P->vote_threads);
+  }
+  if (per_sm < 1) return fail(DSES_E_CUDA, "vote kernel cannot be resident (smem %zu)",
+                              vote_smem_bytes(v, P->hsmem, P->psmem));
+  P->vote_grid = per_sm * P->sms;
+  return DSES_OK;
+}
+
+int set_grid(dses_plan* P, const dses_grid* g, RotSource* rs, cudaStream_t st) {
+  std::memset(rs, 0, sizeof(*rs));
+  if (!g || g->k < 0 || !g->cos_tab || !g->sin_tab) return fail(DSES_E_INVALID, "bad rotation grid");
+  const size_t nt = (size_t)(2 * g->k + 1);
+  CK(P->cth.ensure(nt * 8));
+  CK(P->sth.ensure(nt * 8));
+  CK(cudaMemcpyAsync(P->cth.p, g->cos_tab, nt * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P->sth.p, g->sin_tab, nt * 8, cudaMemcpyHostToDevice, st));
+  rs->cth = P->cth.as<double>();
+  rs->sth = P->sth.as<double>();
+  rs->rots = nullptr;
+  rs->k = g->k;
+  rs->has_center = g->center ? 1 : 0;
+  if (g->center) std::memcpy(rs->center, g->center, sizeof(rs->center));
+  return DSES_OK;
+}
+
+int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
+  CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  CK(P->lins.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  VoteParams v = P->vp;
+  v.rot = rs;
+  v.r_begin = r_begin;
+  v.r_count = r_count;
+  v.counts = P->counts.as<int>();
+  v.lins = P->lins.as<int>();
+  v.ties = P->ties.as<int>();
+  P->cur_r_begin = r_begin;
+  P->cur_r_count = r_count;
+  P->cur_rot = rs;
+  if (r_count <= 0) return DSES_OK;
+  int grid = (int)std::min<int64_t>(P->vote_grid, r_count);
+  // global-memory fallbacks: one slab per CTA, at most ~4 GiB in total
+  const size_t per_cta = (P->hsmem ? 0 : (size_t)v.hist_words * 4) + (P->psmem ? 0 : (size_t)v.n_pad * 16);
+  if (per_cta) {
+    const size_t budget = (size_t)4 << 30;
+    grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)grid, budget / per_cta));
+    if (!P->hsmem) {
+      CK(P->hist_g.ensure((size_t)grid * v.hist_words * 4));
+      v.hist_global = P->hist_g.as<unsigned>();
+    }
+    if (!P->psmem) {
+      CK(P->p_g.ensure((size_t)grid * v.n_pad * 16));
+      v.p_global = P->p_g.as<int4>();
+    }
+  }
+  CK(launch_vote(v, P->hsmem, P->psmem, grid, P->vote_threads, st));
+  return DSES_OK;
+}
+
+ScoreParams score_params(const dses_plan* P, const RotSource& rs, int code, double param) {
+  ScoreParams s{};
+  s.n = (int)P->n;
+  s.m = (int)P->m;
+  s.x = P->x0.as<double>();
+  s.ys0 = P->ys0.as<double>();
+  s.ys1 = P->ys1.as<double>();
+  s.ys2 = P->ys2.as<double>();
+  s.ysf = P->ysf.as<float4>();
+  s.rot = rs;
+  s.bin_size = P->bin;
+  s.ilo0 = P->ilo[0]; s.ilo1 = P->ilo[1]; s.ilo2 = P->ilo[2];
+  s.d1 = (int)P->dims[1]; s.d2 = (int)P->dims[2];
+  s.code = code;
+  s.param = param;
+  s.paramf = (float)param;
+  s.halff = (float)(0.5 * param);
+  // per-axis |d32 - d64| <= 2^-24 (|y| + |p| + |d|) <= 2^-23 (bx + by); margin x2
+  s.amb = (float)(2.0 * std::ldexp(P->bx + P->by, -23));
+  s.tvec = nullptr;
+  return s;
+}
+
+// rigorous bound on |screen - exact| per candidate
+double screen_tolerance(const dses_plan* P, int code) {
+  if (code == kSatL0) return 0.0;
+  const double e_pt = 8.0 * std::ldexp(P->bx + P->by, -23);
+  return 2.0 * (double)P->n * e_pt;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" int dses_plan_create(int device, const double* x, int64_t n, const double* y, int64_t m,
+                                double bin_size, const int64_t ilo[3], const int64_t dims[3],
+                                dses_plan** out) {
+  if (!out) return fail(DSES_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!x || !y || n < 1 || m < 1) return fail(DSES_E_INVALID, "empty cloud");
+  if (n >= (1ll << 31) || m >= (1ll << 30)) return fail(DSES_E_INVALID, "cloud too large");
+  if (!(bin_size > 0) || !std::isfinite(bin_size)) return fail(DSES_E_INVALID, "bad bin size");
+  for (int k = 0; k < 3; ++k)
+    if (dims[k] < 1) return fail(DSES_E_INVALID, "dims must be positive");
+  const double nbins = (double)dims[0] * (double)dims[1] * (double)dims[2];
+  if (nbins > 2147483647.0) return fail(DSES_E_INVALID, "translation lattice too large");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(DSES_E_NODEVICE, "no CUDA device");
+  if (device < 0 || device >= ndev) return fail(DSES_E_INVALID, "bad device %d", device);
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(DSES_E_NODEVICE, "sm_100a build cannot run on sm_%d%d", prop.major, prop.minor);
+  dses_plan* P = new dses_plan();
+  P->device = device;
+  P->sms = prop.multiProcessorCount;
+  P->smem_optin = prop.sharedMemPerBlockOptin;
+  P->n = n;
+  P->m = m;
+  P->bin = bin_size;
+  P->inv_bin = 1.0 / bin_size;  // mode_search.py:158 (inv_bin = 1.0 / bin_size)
+  for (int k = 0; k < 3; ++k) { P->ilo[k] = ilo[k]; P->dims[k] = dims[k]; }
+  for (auto& e : P->ev) cudaEventCreate(&e);
+  const int rc = build_plan(P, x, y);
+  if (rc != DSES_OK) { dses_plan_destroy(P); return rc; }
+  *out = P;
+  return DSES_OK;
+}
+
+extern "C" int dses_plan_destroy(dses_plan* P) {
+  if (!P) return DSES_OK;
+  cudaSetDevice(P->device);
+  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->yt,
+                    &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->cth, &P->sth, &P->rots,
+                    &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
+                    &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,
+                    &P->err64, &P->win_err, &P->win_row, &P->win_c, &P->tmp_rows, &P->tmp_lins,
+                    &P->tvec};
+  for (DevBuf* b : bufs) b->release();
+  for (auto& e : P->ev) cudaEventDestroy(e);
+  delete P;
+  return DSES_OK;
+}
+
+extern "C" int dses_plan_info(const dses_plan* P, int64_t* frac_bits, int64_t* x_tiles,
+                              int64_t* y_tiles, int64_t* near_pairs) {
+  if (!P) return fail(DSES_E_INVALID, "null plan");
+  if (frac_bits) *frac_bits = P->F;
+  if (x_tiles) *x_tiles = P->vp.nxt;
+  if (y_tiles) *y_tiles = P->vp.nyt;
+  if (near_pairs) *near_pairs = P->near_pairs;
+  return DSES_OK;
+}
+
+static int fetch_modes(dses_plan* P, int64_t nrot, int64_t* counts, int64_t* lins, int64_t* ties,
+                       cudaStream_t st) {
+  std::vector<int> c(nrot), l(nrot), t(nrot);
+  if (nrot > 0) {
+    CK(cudaMemcpyAsync(c.data(), P->counts.p, 4 * nrot, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(l.data(), P->lins.p, 4 * nrot, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(t.data(), P->ties.p, 4 * nrot, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  for (int64_t r = 0; r < nrot; ++r) {
+    if (counts) counts[r] = c[r];
+    if (lins) lins[r] = l[r];
+    if (ties) ties[r] = t[r];
+  }
+  return DSES_OK;
+}
+
+extern "C" int dses_mode_batch(dses_plan* P, const double* rots, int64_t nrot, int64_t* counts,
+                               int64_t* lins, int64_t* ties, void* stream) {
+  if (!P || (!rots && nrot > 0) || nrot < 0) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(P->rots.ensure(sizeof(double) * 9 * std::max<int64_t>(nrot, 1)));
+  if (nrot > 0) CK(cudaMemcpyAsync(P->rots.p, rots, sizeof(double) * 9 * nrot, cudaMemcpyHostToDevice, st));
+  RotSource rs{};
+  rs.rots = P->rots.as<double>();
+  int rc = run_vote(P, rs, 0, nrot, st);
+  if (rc) return rc;
+  return fetch_modes(P, nrot, counts, lins, ties, st);
+}
+
+extern "C" int dses_mode_grid(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t nrot,
+                              int64_t* counts, int64_t* lins, int64_t* ties, void* stream) {
+  if (!P || nrot < 0 || r_begin < 0) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  RotSource rs;
+  int rc = set_grid(P, g, &rs, st);
+  if (rc) return rc;
+  const int64_t total = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);
+  if (r_begin + nrot > total) return fail(DSES_E_INVALID, "rotation range beyond the grid");
+  rc = run_vote(P, rs, r_begin, nrot, st);
+  if (rc) return rc;
+  return fetch_modes(P, nrot, counts, lins, ties, st);
+}
+
+extern "C" int dses_mode_dense_batch(int device, const double* rots, int64_t nrot, const double* x,
+                                     int64_t n, const double* y, int64_t m, double bin_size,
+                                     const int64_t ilo[3], const int64_t dims[3], int64_t* counts,
+                                     int64_t* lins, int64_t* ties) {
+  dses_plan* P = nullptr;
+  int rc = dses_plan_create(device, x, n, y, m, bin_size, ilo, dims, &P);
+  if (rc) return rc;
+  rc = dses_mode_batch(P, rots, nrot, counts, lins, ties, nullptr);
+  dses_plan_destroy(P);
+  return rc;
+}
+
+extern "C" int dses_refine_batch(dses_plan* P, const double* rots, const double* ts, int64_t ncand,
+                                 int code, double param, double* out, void* stream) {
+  if (!P || ncand < 0 || (ncand > 0 && (!rots || !ts || !out)) || code < 0 || code > 4)
+    return fail(DSES_E_INVALID, "bad arguments");
+  if (ncand == 0) return DSES_OK;
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(P->rots.ensure(sizeof(double) * 9 * ncand));
+  CK(P->tvec.ensure(sizeof(double) * 3 * ncand));
+  CK(P->tmp_rows.ensure(sizeof(int64_t) * ncand));
+  CK(P->tmp_lins.ensure(sizeof(int) * ncand));
+  CK(P->vals.ensure(sizeof(double) * P->n * ncand));
+  CK(P->err64.ensure(sizeof(double) * ncand));
+  std::vector<int64_t> rows(ncand);
+  std::iota(rows.begin(), rows.end(), 0);
+  std::vector<int> zeros(ncand, 0);
+  CK(cudaMemcpyAsync(P->rots.p, rots, sizeof(double) * 9 * ncand, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P->tvec.p, ts, sizeof(double) * 3 * ncand, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P->tmp_rows.p, rows.data(), sizeof(int64_t) * ncand, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P->tmp_lins.p, zeros.data(), sizeof(int) * ncand, cudaMemcpyHostToDevice, st));
+  RotSource rs{};
+  rs.rots = P->rots.as<double>();
+  ScoreParams s = score_params(P, rs, code, param);
+  s.tvec = P->tvec.as<double>();
+  CK(launch_exact(s, P->tmp_rows.as<int64_t>(), P->tmp_lins.as<int>(), nullptr, ncand,
+                  P->vals.as<double>(), P->err64.as<double>(), st));
+  CK(cudaMemcpyAsync(out, P->err64.p, sizeof(double) * ncand, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return DSES_OK;
+}
+
+// ---- stages -------------------------------------------------------------
+extern "C" int dses_stage_vote(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t r_count,
+                               int64_t* mstar_local, int64_t* valid_local, void* stream) {
+  if (!P || !g) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t total = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);
+  if (r_count < 0) r_count = total - r_begin;
+  if (r_begin < 0 || r_begin + r_count > total) return fail(DSES_E_INVALID, "rotation range beyond the grid");
+  RotSource rs;
+  int rc = set_grid(P, g, &rs, st);
+  if (rc) return rc;
+  P->cur_k = g->k;
+  rc = run_vote(P, rs, r_begin, r_count, st);
+  if (rc) return rc;
+  unsigned long long* sc = P->scal.as<unsigned long long>();
+  CK(cudaMemsetAsync(sc, 0, 2 * sizeof(unsigned long long), st));
+  if (r_count > 0) CK(launch_select_stats(P->counts.as<int>(), r_count, sc, sc + 1, P->sms, st));
+  unsigned long long h[2];
+  CK(cudaMemcpyAsync(h, sc, sizeof h, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (mstar_local) *mstar_local = (int64_t)h[0];
+  if (valid_local) *valid_local = (int64_t)h[1];
+  return DSES_OK;
+}
+
+extern "C" int dses_stage_argmax(dses_plan* P, int64_t mstar_global, int64_t* row_local, void* stream) {
+  if (!P || !row_local) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* sc = P->scal.as<unsigned long long>() + 2;
+  CK(cudaMemsetAsync(sc, 0xff, sizeof(unsigned long long), st));
+  if (P->cur_r_count > 0)
+    CK(launch_argmax(P->counts.as<int>(), P->cur_r_count, P->cur_r_begin, (int)mstar_global, sc,
+                     P->sms, st));
+  unsigned long long h;
+  CK(cudaMemcpyAsync(&h, sc, sizeof h, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *row_local = h == ~0ull ? INT64_MAX : (int64_t)h;
+  return DSES_OK;
+}
+
+extern "C" int dses_stage_screen(dses_plan* P, double q, int64_t mstar_global, int code,
+                                 double param, int64_t* kept_local, double* min32_local, double* tol,
+                                 void* stream) {
+  if (!P || code < 0 || code > 4) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nr = P->cur_r_count;
+  // engines.py:196-201 in binary64: cutoff = q * M* - 1e-9
+  const double cutoff = q * (double)mstar_global - 1e-9;
+  CK(P->cand_rows.ensure(sizeof(int64_t) * std::max<int64_t>(nr, 1)));
+  CK(P->cand_lins.ensure(sizeof(int) * std::max<int64_t>(nr, 1)));
+  unsigned long long* sc = P->scal.as<unsigned long long>() + 3;
+  CK(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), st));
+  if (nr > 0)
+    CK(launch_compact(P->counts.as<int>(), P->lins.as<int>(), nr, P->cur_r_begin, cutoff,
+                      P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), sc, P->sms, st));
+  unsigned long long kept;
+  CK(cudaMemcpyAsync(&kept, sc, sizeof kept, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  P->kept = (int64_t)kept;
+  if (kept_local) *kept_local = (int64_t)kept;
+  if (tol) *tol = screen_tolerance(P, code);
+  if (kept == 0) {
+    if (min32_local) *min32_local = INFINITY;
+    return DSES_OK;
+  }
+  const int nblk = (int)((P->n + screen_threads() - 1) / screen_threads());
+  CK(P->partial.ensure(sizeof(double) * nblk * kept));
+  CK(P->err32.ensure(sizeof(double) * kept));
+  unsigned long long* mb = P->scal.as<unsigned long long>() + 4;
+  CK(cudaMemsetAsync(mb, 0x7f, sizeof(unsigned long long), st));
+  ScoreParams s = score_params(P, P->cur_rot, code, param);
+  CK(launch_screen(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), (int64_t)kept,
+                   P->partial.as<double>(), P->err32.as<double>(), mb, st));
+  double mn;
+  CK(cudaMemcpyAsync(&mn, mb, sizeof mn, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (min32_local) *min32_local = mn;
+  return DSES_OK;
+}
+
+extern "C" int dses_stage_rescore(dses_plan* P, double threshold, int code, double param,
+                                  double* err_local, int64_t* row_local, int64_t* rescored,
+                                  void* stream) {
+  if (!P || code < 0 || code > 4) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (err_local) *err_local = INFINITY;
+  if (row_local) *row_local = INT64_MAX;
+  if (rescored) *rescored = 0;
+  if (P->kept <= 0) return DSES_OK;
+  CK(P->sel.ensure(sizeof(int) * P->kept));
+  unsigned long long* ns = P->scal.as<unsigned long long>() + 5;
+  CK(cudaMemsetAsync(ns, 0, sizeof(unsigned long long), st));
+  CK(launch_rescore_compact(P->err32.as<double>(), P->kept, threshold, P->sel.as<int>(), ns, st));
+  unsigned long long nsel;
+  CK(cudaMemcpyAsync(&nsel, ns, sizeof nsel, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (rescored) *rescored = (int64_t)nsel;
+  if (nsel == 0) return DSES_OK;
+  CK(P->vals.ensure(sizeof(double) * P->n * nsel));
+  CK(P->err64.ensure(sizeof(double) * nsel));
+  CK(P->win_err.ensure(sizeof(double)));
+  CK(P->win_row.ensure(sizeof(int64_t)));
+  CK(P->win_c.ensure(sizeof(int)));
+  ScoreParams s = score_params(P, P->cur_rot, code, param);
+  CK(launch_exact(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->sel.as<int>(),
+                  (int64_t)nsel, P->vals.as<double>(), P->err64.as<double>(), st));
+  CK(launch_winner(P->err64.as<double>(), P->sel.as<int>(), P->cand_rows.as<int64_t>(),
+                   (int64_t)nsel, P->win_err.as<double>(), P->win_row.as<int64_t>(),
+                   P->win_c.as<int>(), st));
+  double e;
+  int64_t r;
+  CK(cudaMemcpyAsync(&e, P->win_err.p, sizeof e, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&r, P->win_row.p, sizeof r, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (err_local) *err_local = e;
+  if (row_local) *row_local = r;
+  return DSES_OK;
+}
+
+extern "C" int dses_stage_row_info(dses_plan* P, int64_t row, int64_t* lin, int64_t* count,
+                                   void* stream) {
+  if (!P) return fail(DSES_E_INVALID, "null plan");
+  const int64_t rr = row - P->cur_r_begin;
+  if (rr < 0 || rr >= P->cur_r_count) return fail(DSES_E_INVALID, "row %lld not in this plan's slice", (long long)row);
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int l, c;
+  CK(cudaMemcpyAsync(&l, P->lins.as<int>() + rr, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&c, P->counts.as<int>() + rr, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (lin) *lin = l;
+  if (count) *count = c;
+  return DSES_OK;
+}
+
+extern "C" int dses_pose_error(dses_plan* P, const dses_grid* g, int64_t row, int64_t lin, int code,
+                               double param, double* err, void* stream) {
+  if (!P || !err || code < 0 || code > 4 || lin < 0) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  RotSource rs;
+  int rc = set_grid(P, g, &rs, st);
+  if (rc) return rc;
+  CK(P->tmp_rows.ensure(sizeof(int64_t)));
+  CK(P->tmp_lins.ensure(sizeof(int)));
+  CK(P->vals.ensure(sizeof(double) * P->n));
+  CK(P->err64.ensure(sizeof(double)));
+  const int l32 = (int)lin;
+  CK(cudaMemcpyAsync(P->tmp_rows.p, &row, sizeof row, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(P->tmp_lins.p, &l32, sizeof l32, cudaMemcpyHostToDevice, st));
+  ScoreParams s = score_params(P, rs, code, param);
+  CK(launch_exact(s, P->tmp_rows.as<int64_t>(), P->tmp_lins.as<int>(), nullptr, 1,
+                  P->vals.as<double>(), P->err64.as<double>(), st));
+  CK(cudaMemcpyAsync(err, P->err64.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return DSES_OK;
+}
+
+extern "C" int dses_stage_stats(dses_plan* P, int64_t* pairs, int64_t* votes, int64_t* rechecks) {
+  if (!P) return fail(DSES_E_INVALID, "null plan");
+  CK(cudaSetDevice(P->device));
+  unsigned long long h[3];
+  CK(cudaMemcpy(h, P->stats.p, sizeof h, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(P->stats.p, 0, sizeof h));
+  if (pairs) *pairs = (int64_t)h[0];
+  if (votes) *votes = (int64_t)h[1];
+  if (rechecks) *rechecks = (int64_t)h[2];
+  return DSES_OK;
+}
+
+extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t r_count,
+                           double q, int code, double param, int skip_refine, dses_result* out,
+                           void* stream) {
+  if (!P || !g || !out) return fail(DSES_E_INVALID, "bad arguments");
+  std::memset(out, 0, sizeof(*out));
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaEventRecord(P->ev[0], st));
+  int64_t mstar = 0, nvalid = 0;
+  int rc = dses_stage_vote(P, g, r_begin, r_count, &mstar, &nvalid, stream);
+  if (rc) return rc;
+  CK(cudaEventRecord(P->ev[1], st));
+  out->mstar = mstar;
+  out->candidates_evaluated = nvalid;
+  out->winner_row = -1;
+  if (nvalid == 0) return DSES_OK;  // caller raises NoCandidateError (engines.py:255-259)
+  int64_t row;
+  double best_err = 0.0;
+  if (skip_refine) {
+    rc = dses_stage_argmax(P, mstar, &row, stream);
+    if (rc) return rc;
+    CK(cudaEventRecord(P->ev[2], st));
+    CK(cudaEventRecord(P->ev[3], st));
+    out->candidates_refined = 0;
+  } else {
+    int64_t kept;
+    double mn, tol;
+    rc = dses_stage_screen(P, q, mstar, code, param, &kept, &mn, &tol, stream);
+    if (rc) return rc;
+    CK(cudaEventRecord(P->ev[2], st));
+    int64_t rescored;
+    rc = dses_stage_rescore(P, mn + tol, code, param, &best_err, &row, &rescored, stream);
+    if (rc) return rc;
+    CK(cudaEventRecord(P->ev[3], st));
+    out->candidates_refined = std::max<int64_t>(1, kept);
+    out->rescored = rescored;
+  }
+  int64_t lin, cnt;
+  rc = dses_stage_row_info(P, row, &lin, &cnt, stream);
+  if (rc) return rc;
+  double miss;
+  rc = dses_pose_error(P, g, row, lin, kSatL0, P->bin, &miss, stream);
+  if (rc) return rc;
+  CK(cudaEventRecord(P->ev[4], st));
+  CK(cudaEventSynchronize(P->ev[4]));
+  out->winner_row = row;
+  out->winner_lin = lin;
+  out->winner_count = cnt;
+  out->best_error = skip_refine ? miss : best_err;
+  out->best_inliers = P->n - (int64_t)std::llround(miss);
+  float ms;
+  cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]); out->ms_vote = ms;
+  cudaEventElapsedTime(&ms, P->ev[1], P->ev[2]); out->ms_select = ms;
+  cudaEventElapsedTime(&ms, P->ev[2], P->ev[3]); out->ms_score = ms;
+  cudaEventElapsedTime(&ms, P->ev[0], P->ev[4]); out->ms_total = ms;
+  return dses_stage_stats(P, &out->pairs_evaluated, &out->votes, &out->rechecks);
+}

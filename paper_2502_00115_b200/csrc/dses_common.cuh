@@ -1,0 +1,169 @@
+// dses_common.cuh -- shared device-side definitions for the B200 DSES kernels.
+//
+// Numerics contract:
+//  * The reference bins a vote (i, j) in binary64 as
+//      p  = R x_i                      ((r0*x0 + r1*x1) + r2*x2, no FMA)
+//      q  = (y_j - p) * inv_bin        (_kernels.py:135-149)
+//      f  = copysign(floor(|q| + 0.5), q) - lo
+//    exact_bin() below reproduces that sequence with explicit __dmul_rn /
+//    __dadd_rn intrinsics so nvcc cannot contract it into FMAs.
+//  * The fast path bins in 32-bit fixed point (F fraction bits per bin):
+//      Yq = rint(fl(y*inv_bin) * 2^F) - lo*2^F + 2^(F-1) + G     (host, exact int64)
+//      Pq = rint(fl(p*inv_bin*2^F))                              (device, per rotation)
+//      u  = Yq - Pq                                              (exact int32)
+//    |u - (U + G) 2^F| <= 1 unit, U = (y-p)*inv_bin - lo + 1/2, so a pair whose
+//    fraction lies >= G units from a bin edge is binned exactly by u >> F; the
+//    rest (probability ~4G/2^F per axis) are re-binned by exact_bin().
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dses {
+
+constexpr int kTile = 32;        // points per spatial tile (one per lane)
+constexpr int kGuard = 2;        // guard band in fixed-point units
+constexpr int kVoteThreads = 1024;
+
+enum Metric { kL2 = 0, kL1 = 1, kTruncL1 = 2, kSatL0 = 3, kTruncL2 = 4 };
+
+struct XTile {          // spatial tile of the (sorted) source cloud
+  int start, count;
+  int rad;              // bounding-sphere radius in fixed-point units (+ rounding margin)
+  int pad;
+  double c[3];          // sphere centre (metres)
+};
+
+struct YTile {          // spatial tile of the (sorted) reference cloud
+  int start, count;
+  int lo[3], hi[3];     // fixed-point bounding box of Yq over the tile
+};
+
+struct RotSource {      // where rotation r comes from
+  const double* cth;    // grid tables (device), 2k+1 values; NULL -> explicit
+  const double* sth;
+  const double* rots;   // explicit matrices (device), r x 9
+  int64_t k;
+  int has_center;
+  double center[9];
+};
+
+struct VoteParams {
+  // lattice
+  int d0, d1, d2, nbins;
+  int F;                 // fraction bits; 0 => exact mode (every pair re-binned in fp64)
+  unsigned fmask;        // 2^F - 1
+  unsigned W0, W1, W2;   // prefilter: (unsigned)u < d*2^F + 2G
+  unsigned D0, D1, D2;   // d*2^F
+  double inv_bin, inv_s; // 1/bin (as the reference computes it) and inv_bin*2^F
+  double flo0, flo1, flo2, fd0, fd1, fd2;
+  // clouds (tile-sorted)
+  int n, m, nxt, nyt;
+  const double* xs;      // (n,3) f64, X tile order
+  const double* ys;      // (m,3) f64, Y tile order
+  const int4* yq;        // (m) fixed-point Yq (w unused)
+  const int* near_off;   // (m+1) CSR offsets of the dedup near lists (Y tile order)
+  const int* near_idx;   // near neighbours j' < j with |y_j - y_j'|_inf < bin (1+1e-6)
+  const XTile* xt;
+  const YTile* yt;
+  RotSource rot;
+  int64_t r_begin, r_count;
+  // outputs (indexed r - r_begin)
+  int* counts;
+  int* lins;
+  int* ties;
+  unsigned long long* stats;  // [pairs, votes, rechecks]
+  // global fallbacks when the histogram / rotated points do not fit shared memory
+  unsigned* hist_global;      // per-CTA slabs of hist_words (u32 counts when !count16)
+  int4* p_global;             // per-CTA slabs of n_pad entries
+  int hist_words;             // u32 words per histogram (padded to a multiple of 4)
+  int n_pad;
+  int count16;                // two 16-bit counts per word (n < 65536)
+};
+
+struct ScoreParams {     // scoring kernels (dses_score.cu)
+  int n, m;
+  const double* x;        // (n,3) source, ORIGINAL order (the serial sum order)
+  const double* ys0;      // reference columns sorted by axis 0 (engines.py:133-140)
+  const double* ys1;
+  const double* ys2;
+  const float4* ysf;      // same order, fp32 (screen)
+  RotSource rot;
+  double bin_size;
+  int64_t ilo0, ilo1, ilo2;
+  int d1, d2;
+  int code;
+  double param;
+  float paramf, halff;    // fp32 metric parameter and sat_l0 half width
+  float amb;              // sat_l0 fp32 ambiguity margin (absolute)
+  const double* tvec;     // explicit translations (row-indexed) instead of decoding bins
+};
+
+// ---------------------------------------------------------------------------
+// exact binary64 helpers (no contraction)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// p_k = (r_k0*x0 + r_k1*x1) + r_k2*x2  (_kernels.py:135-137, 320-322 without t)
+__device__ __forceinline__ double rot_row(const double* R, int k, double x0, double x1, double x2) {
+  return dadd(dadd(dmul(R[3 * k], x0), dmul(R[3 * k + 1], x1)), dmul(R[3 * k + 2], x2));
+}
+
+// Grid entry e (row-major) of Rz(xi) Ry(phi) Rx(theta) for angle indices (a,b,c),
+// in numpy's evaluation order (geometry.py:279-287).
+__device__ __forceinline__ double grid_entry(const double* cth, const double* sth, int64_t a,
+                                             int64_t b, int64_t c, int e) {
+  const double c1 = cth[a], s1 = sth[a], c2 = cth[b], s2 = sth[b], c3 = cth[c], s3 = sth[c];
+  switch (e) {
+    case 0: return dmul(c3, c2);
+    case 1: return dadd(dmul(-s3, c1), dmul(dmul(c3, s2), s1));
+    case 2: return dadd(dmul(s3, s1), dmul(dmul(c3, s2), c1));
+    case 3: return dmul(s3, c2);
+    case 4: return dadd(dmul(c3, c1), dmul(dmul(s3, s2), s1));
+    case 5: return dadd(dmul(-c3, s1), dmul(dmul(s3, s2), c1));
+    case 6: return -s2;
+    case 7: return dmul(c2, s1);
+    default: return dmul(c2, c1);
+  }
+}
+
+// Entry e of rotation r: grid (optionally centre-multiplied, engines.py:122-126,
+// summation ((C a0 G 0c + C a1 G 1c) + C a2 G 2c)) or explicit.
+__device__ __forceinline__ double rotation_entry(const RotSource& rs, int64_t r, int e) {
+  if (rs.rots) return rs.rots[9 * r + e];
+  const int64_t n = 2 * rs.k + 1;
+  const int64_t a = r / (n * n), b = (r / n) % n, c = r % n;
+  if (!rs.has_center) return grid_entry(rs.cth, rs.sth, a, b, c, e);
+  const int row = e / 3, col = e % 3;
+  const double g0 = grid_entry(rs.cth, rs.sth, a, b, c, col);
+  const double g1 = grid_entry(rs.cth, rs.sth, a, b, c, 3 + col);
+  const double g2 = grid_entry(rs.cth, rs.sth, a, b, c, 6 + col);
+  return dadd(dadd(dmul(rs.center[3 * row], g0), dmul(rs.center[3 * row + 1], g1)),
+              dmul(rs.center[3 * row + 2], g2));
+}
+
+// Reference binning of one pair, _kernels.py:144-152.  Returns true when the
+// vote lands inside the window; *lin gets the flat bin (f0*d1 + f1)*d2 + f2.
+__device__ __forceinline__ bool exact_bin(const VoteParams& p, double p0, double p1, double p2,
+                                          const double* yj, int* lin) {
+  const double q0 = dmul(dsub(yj[0], p0), p.inv_bin);
+  const double f0 = dsub(copysign(floor(dadd(fabs(q0), 0.5)), q0), p.flo0);
+  const double q1 = dmul(dsub(yj[1], p1), p.inv_bin);
+  const double f1 = dsub(copysign(floor(dadd(fabs(q1), 0.5)), q1), p.flo1);
+  const double q2 = dmul(dsub(yj[2], p2), p.inv_bin);
+  const double f2 = dsub(copysign(floor(dadd(fabs(q2), 0.5)), q2), p.flo2);
+  const bool ok = (f0 >= 0.0) & (f0 < p.fd0) & (f1 >= 0.0) & (f1 < p.fd1) & (f2 >= 0.0) &
+                  (f2 < p.fd2);
+  if (ok) *lin = (int)dadd(dmul(dadd(dmul(f0, p.fd1), f1), p.fd2), f2);
+  return ok;
+}
+
+// Combine (best, lin, ties) triples: higher count wins, equal counts keep the
+// smaller flat bin and add their tie counts (_kernels.py:159-170).
+__device__ __forceinline__ void mode_combine(int& best, int& lin, int& ties, int ob, int ol, int ot) {
+  if (ob > best) { best = ob; lin = ol; ties = ot; }
+  else if (ob == best) { lin = min(lin, ol); ties += ot; }
+}
+
+}  // namespace dses

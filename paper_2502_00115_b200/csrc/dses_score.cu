@@ -1,0 +1,425 @@
+// dses_score.cu -- phases 2 and 3 of DSES on B200: selection and scoring.
+//
+// Replaces, from engines.dses (engines.py:254-285):
+//   * the valid filter + stable argsort + M* (phase 2): select_stats_kernel,
+//     compact_kernel (the sort order is unobservable: the winner rule is
+//     order-free, engines.py:276-280, and n_score is a count);
+//   * _refine_cutoff (engines.py:196-201): compact_kernel keeps
+//     count >= fl(fl(q*M*) - 1e-9) in binary64, exactly as the reference;
+//   * _score_poses -> refine_batch/_point_best (_kernels.py:34-80, 297-324):
+//     an fp32 screen over all kept candidates (screen_kernel), then an exact
+//     binary64 re-score (exact_points_kernel + exact_sum_kernel: reference
+//     operation order, serial sum over i) of every candidate whose screened
+//     error is within a rigorous bound of the screened minimum;
+//   * the min-error / lexicographic-grid winner (winner_kernel).
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+#include <math_constants.h>
+#include "dses_common.cuh"
+
+namespace dses {
+
+
+// ---------------------------------------------------------------------------
+// phase 2
+// ---------------------------------------------------------------------------
+__global__ void select_stats_kernel(const int* counts, int64_t nrot, unsigned long long* mstar,
+                                    unsigned long long* nvalid) {
+  int best = 0, nv = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrot;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int c = counts[r];
+    best = max(best, c);
+    nv += c > 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    nv += __shfl_xor_sync(0xffffffffu, nv, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(mstar, (unsigned long long)best);
+    atomicAdd(nvalid, (unsigned long long)nv);
+  }
+}
+
+// smallest row whose count equals mstar (the first entry of the stable order)
+__global__ void argmax_kernel(const int* counts, int64_t nrot, int64_t r_begin, int mstar,
+                              unsigned long long* row) {
+  unsigned long long best = ULLONG_MAX;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrot;
+       r += (int64_t)gridDim.x * blockDim.x)
+    if (counts[r] == mstar && mstar > 0) best = min(best, (unsigned long long)(r + r_begin));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best != ULLONG_MAX) atomicMin(row, best);
+}
+
+__global__ void compact_kernel(const int* counts, const int* lins, int64_t nrot, int64_t r_begin,
+                               double cutoff, int64_t* rows, int* cand_lins,
+                               unsigned long long* ncand) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrot;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int c = counts[r];
+    const bool keep = c > 0 && (double)c >= cutoff;
+    const unsigned m = __ballot_sync(__activemask(), keep);
+    if (!m) continue;
+    // warp-aggregated slot reservation
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(ncand, (unsigned long long)__popc(m));
+    base = __shfl_sync(m | (1u << leader), base, leader);
+    if (keep) {
+      const int k = (int)base + __popc(m & ((1u << lane) - 1));
+      rows[k] = r + r_begin;
+      cand_lins[k] = lins[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pose helpers
+// ---------------------------------------------------------------------------
+// t = bin_center(_decode_flat(lin)) = (f + ilo) * bin  (mode_search.py:51-54,167-171)
+__device__ __forceinline__ void decode_translation(const ScoreParams& s, int lin, double* t) {
+  const int a = lin / (s.d1 * s.d2), rem = lin % (s.d1 * s.d2), b = rem / s.d2, c = rem % s.d2;
+  t[0] = dmul((double)(a + s.ilo0), s.bin_size);
+  t[1] = dmul((double)(b + s.ilo1), s.bin_size);
+  t[2] = dmul((double)(c + s.ilo2), s.bin_size);
+}
+
+// p = ((r0 x0 + r1 x1) + r2 x2) + t  (_kernels.py:320-322)
+__device__ __forceinline__ void pose_point(const double* R, const double* t, const double* x,
+                                           double* pp) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) pp[k] = dadd(rot_row(R, k, x[0], x[1], x[2]), t[k]);
+}
+
+__device__ __forceinline__ int lower_bound_d(const double* a, int n, double v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// _point_best (_kernels.py:34-80) in binary64, reference semantics (windows
+// over the axis-0-sorted reference, strict sat_l0 test), plus code 4.
+__device__ double exact_point_best(const ScoreParams& s, double p0, double p1, double p2) {
+  const double* y0 = s.ys0;
+  const double* y1 = s.ys1;
+  const double* y2 = s.ys2;
+  const int m = s.m;
+  if (s.code == kTruncL1 || s.code == kTruncL2) {
+    const int jlo = lower_bound_d(y0, m, dsub(p0, s.param));
+    const int jhi = lower_bound_d(y0, m, dadd(p0, s.param));
+    if (s.code == kTruncL1) {
+      double best = s.param;
+      for (int j = jlo; j < jhi; ++j) {
+        const double v = dadd(dadd(fabs(dsub(y0[j], p0)), fabs(dsub(y1[j], p1))), fabs(dsub(y2[j], p2)));
+        if (v < best) best = v;
+      }
+      return best;
+    }
+    const double cap = dmul(s.param, s.param);
+    double best = cap;
+    for (int j = jlo; j < jhi; ++j) {
+      const double a = dsub(y0[j], p0), b = dsub(y1[j], p1), c = dsub(y2[j], p2);
+      const double v = dadd(dadd(dmul(a, a), dmul(b, b)), dmul(c, c));
+      if (v < best) best = v;
+    }
+    return best < cap ? sqrt(best) : s.param;
+  }
+  if (s.code == kSatL0) {
+    const double half = dmul(0.5, s.param);
+    const int jlo = lower_bound_d(y0, m, dsub(p0, half));
+    const int jhi = lower_bound_d(y0, m, dadd(p0, half));
+    for (int j = jlo; j < jhi; ++j)
+      if (fabs(dsub(y0[j], p0)) < half && fabs(dsub(y1[j], p1)) < half && fabs(dsub(y2[j], p2)) < half)
+        return 0.0;
+    return 1.0;
+  }
+  double best = CUDART_INF;
+  if (s.code == kL1) {
+    for (int j = 0; j < m; ++j) {
+      const double v = dadd(dadd(fabs(dsub(y0[j], p0)), fabs(dsub(y1[j], p1))), fabs(dsub(y2[j], p2)));
+      if (v < best) best = v;
+    }
+    return best;
+  }
+  for (int j = 0; j < m; ++j) {
+    const double a = dsub(y0[j], p0), b = dsub(y1[j], p1), c = dsub(y2[j], p2);
+    const double v = dadd(dadd(dmul(a, a), dmul(b, b)), dmul(c, c));
+    if (v < best) best = v;
+  }
+  return sqrt(best);
+}
+
+__device__ __forceinline__ void load_pose(const ScoreParams& s, int64_t row, int lin, double* R,
+                                          double* t) {
+  if (threadIdx.x < 9) R[threadIdx.x] = rotation_entry(s.rot, row, threadIdx.x);
+  if (threadIdx.x == 0) {
+    if (s.tvec) { t[0] = s.tvec[3 * row]; t[1] = s.tvec[3 * row + 1]; t[2] = s.tvec[3 * row + 2]; }
+    else decode_translation(s, lin, t);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// phase 3a: fp32 screen.  grid (ceil(n/kScreenThreads), ncand); one source
+// point per thread; the reference cloud streams through shared memory in
+// chunks (broadcast reads).  For windowed metrics the block only visits the
+// reference slice whose axis-0 coordinate can fall inside some thread's window.
+// ---------------------------------------------------------------------------
+constexpr int kScreenThreads = 256;
+constexpr int kScreenChunk = 2048;  // reference points per shared-memory chunk (32 KB)
+
+__global__ void __launch_bounds__(kScreenThreads) screen_kernel(ScoreParams s, const int64_t* rows,
+                                                                const int* lins, double* partial) {
+  __shared__ double R[9], t[3];
+  __shared__ float4 ych[kScreenChunk];
+  __shared__ float wred[2][kScreenThreads / 32];
+  __shared__ int jrange[2];
+  __shared__ double sred[kScreenThreads / 32];
+  const int c = blockIdx.y;
+  load_pose(s, rows[c], lins[c], R, t);
+  const int i = blockIdx.x * kScreenThreads + threadIdx.x;
+  const bool active = i < s.n;
+  double pp[3] = {0.0, 0.0, 0.0};
+  if (active) pose_point(R, t, s.x + 3 * i, pp);
+  const float p0 = (float)pp[0], p1 = (float)pp[1], p2 = (float)pp[2];
+  const bool windowed = (s.code == kTruncL1 || s.code == kTruncL2 || s.code == kSatL0);
+  const float wr = s.code == kSatL0 ? s.halff : s.paramf;
+  int jlo = 0, jhi = s.m;
+  if (windowed) {
+    float lo = active ? p0 : FLT_MAX, hi = active ? p0 : -FLT_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) { wred[0][threadIdx.x >> 5] = lo; wred[1][threadIdx.x >> 5] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      lo = wred[0][0]; hi = wred[1][0];
+      for (int w = 1; w < kScreenThreads / 32; ++w) { lo = fminf(lo, wred[0][w]); hi = fmaxf(hi, wred[1][w]); }
+      // widen by the window and an fp32 slack; the exact re-score uses exact windows
+      const double slack = 1e-5 * (1.0 + fabs((double)lo) + fabs((double)hi)) + s.amb;
+      jrange[0] = lower_bound_d(s.ys0, s.m, (double)lo - (double)wr - slack);
+      jrange[1] = lower_bound_d(s.ys0, s.m, (double)hi + (double)wr + slack);
+    }
+    __syncthreads();
+    jlo = jrange[0];
+    jhi = jrange[1];
+  }
+  float best = FLT_MAX;
+  bool inlier = false, ambiguous = false;
+  const float half = s.halff, amb = s.amb;
+  for (int base = jlo; base < jhi; base += kScreenChunk) {
+    const int cnt = min(kScreenChunk, jhi - base);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cnt; k += kScreenThreads) ych[k] = s.ysf[base + k];
+    __syncthreads();
+    if (s.code == kL1 || s.code == kTruncL1) {
+#pragma unroll 8
+      for (int k = 0; k < cnt; ++k) {
+        const float4 y = ych[k];
+        best = fminf(best, fabsf(y.x - p0) + fabsf(y.y - p1) + fabsf(y.z - p2));
+      }
+    } else if (s.code == kL2 || s.code == kTruncL2) {
+#pragma unroll 8
+      for (int k = 0; k < cnt; ++k) {
+        const float4 y = ych[k];
+        const float a = y.x - p0, b = y.y - p1, d = y.z - p2;
+        best = fminf(best, fmaf(d, d, fmaf(b, b, a * a)));
+      }
+    } else {
+      for (int k = 0; k < cnt; ++k) {
+        const float4 y = ych[k];
+        const float m = fmaxf(fmaxf(fabsf(y.x - p0), fabsf(y.y - p1)), fabsf(y.z - p2));
+        inlier |= m < half - amb;
+        ambiguous |= m < half + amb;
+      }
+    }
+  }
+  double v = 0.0;
+  if (active) {
+    if (s.code == kL1) v = best;
+    else if (s.code == kTruncL1) v = fminf(best, s.paramf);
+    else if (s.code == kL2) v = sqrtf(best);
+    else if (s.code == kTruncL2) v = fminf(sqrtf(best), s.paramf);
+    else v = inlier ? 0.0 : (ambiguous ? exact_point_best(s, pp[0], pp[1], pp[2]) : 1.0);
+  }
+  // deterministic block sum in binary64
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < kScreenThreads / 32; ++w) tot += sred[w];
+    partial[(size_t)c * gridDim.x + blockIdx.x] = tot;
+  }
+}
+
+// err32[c] = sum of the block partials in block order; atomicMin of the
+// (non-negative) binary64 bits gives the minimum.
+__global__ void screen_reduce_kernel(const double* partial, int nblk, int64_t ncand, double* err,
+                                     unsigned long long* minbits) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncand) return;
+  double tot = 0.0;
+  for (int b = 0; b < nblk; ++b) tot += partial[c * nblk + b];
+  err[c] = tot;
+  atomicMin(minbits, (unsigned long long)__double_as_longlong(tot));
+}
+
+__global__ void rescore_compact_kernel(const double* err, int64_t ncand, double threshold,
+                                       int* sel, unsigned long long* nsel) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncand) return;
+  if (err[c] <= threshold) sel[atomicAdd(nsel, 1ull)] = (int)c;
+}
+
+// ---------------------------------------------------------------------------
+// phase 3b: exact binary64 re-score, reference semantics and operation order.
+// grid (ceil(n/128), nsel): per-point values; then one thread per candidate
+// sums them serially in source order (_kernels.py:315-324).
+// ---------------------------------------------------------------------------
+constexpr int kExactThreads = 128;
+
+__global__ void __launch_bounds__(kExactThreads) exact_points_kernel(ScoreParams s,
+                                                                     const int64_t* rows,
+                                                                     const int* lins,
+                                                                     const int* sel, int64_t c_off,
+                                                                     double* vals) {
+  __shared__ double R[9], t[3];
+  const int64_t k = c_off + blockIdx.y;
+  const int64_t c = sel ? sel[k] : k;
+  load_pose(s, rows[c], lins[c], R, t);
+  const int i = blockIdx.x * kExactThreads + threadIdx.x;
+  if (i >= s.n) return;
+  double pp[3];
+  pose_point(R, t, s.x + 3 * i, pp);
+  vals[(size_t)k * s.n + i] = exact_point_best(s, pp[0], pp[1], pp[2]);
+}
+
+__global__ void exact_sum_kernel(const double* vals, int n, int64_t nsel, double* out) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nsel) return;
+  const double* v = vals + (size_t)c * n;
+  double total = 0.0;
+  for (int i = 0; i < n; ++i) total = dadd(total, v[i]);
+  out[c] = total;
+}
+
+// lexicographic (error, row) minimum over the re-scored set; single block.
+__global__ void winner_kernel(const double* err64, const int* sel, const int64_t* rows,
+                              int64_t nsel, double* best_err, int64_t* best_row, int* best_c) {
+  __shared__ double se[32];
+  __shared__ int64_t sr[32];
+  __shared__ int sc[32];
+  double e = CUDART_INF;
+  int64_t r = INT64_MAX;
+  int cc = -1;
+  for (int64_t k = threadIdx.x; k < nsel; k += blockDim.x) {
+    const int c = sel ? sel[k] : (int)k;
+    const double ek = err64[k];
+    const int64_t rk = rows[c];
+    if (ek < e || (ek == e && rk < r)) { e = ek; r = rk; cc = c; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oe = __shfl_xor_sync(0xffffffffu, e, o);
+    const int64_t orr = __shfl_xor_sync(0xffffffffu, r, o);
+    const int oc = __shfl_xor_sync(0xffffffffu, cc, o);
+    if (oe < e || (oe == e && orr < r)) { e = oe; r = orr; cc = oc; }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { se[w] = e; sr[w] = r; sc[w] = cc; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    e = se[0]; r = sr[0]; cc = sc[0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (se[k] < e || (se[k] == e && sr[k] < r)) { e = se[k]; r = sr[k]; cc = sc[k]; }
+    *best_err = e;
+    *best_row = r;
+    *best_c = cc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+int screen_threads() { return kScreenThreads; }
+int exact_threads() { return kExactThreads; }
+
+cudaError_t launch_select_stats(const int* counts, int64_t nrot, unsigned long long* mstar,
+                                unsigned long long* nvalid, int sms, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((nrot + 255) / 256, (int64_t)sms * 8);
+  select_stats_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(counts, nrot, mstar, nvalid);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax(const int* counts, int64_t nrot, int64_t r_begin, int mstar,
+                          unsigned long long* row, int sms, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((nrot + 255) / 256, (int64_t)sms * 8);
+  argmax_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(counts, nrot, r_begin, mstar, row);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const int* counts, const int* lins, int64_t nrot, int64_t r_begin,
+                           double cutoff, int64_t* rows, int* cl, unsigned long long* ncand, int sms,
+                           cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((nrot + 255) / 256, (int64_t)sms * 8);
+  compact_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(counts, lins, nrot, r_begin, cutoff, rows, cl,
+                                                      ncand);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_screen(const ScoreParams& s, const int64_t* rows, const int* lins,
+                          int64_t ncand, double* partial, double* err,
+                          unsigned long long* minbits, cudaStream_t st) {
+  if (ncand <= 0) return cudaSuccess;
+  const int nblk = (s.n + kScreenThreads - 1) / kScreenThreads;
+  for (int64_t c0 = 0; c0 < ncand; c0 += 65535) {
+    const int64_t cn = std::min<int64_t>(65535, ncand - c0);
+    screen_kernel<<<dim3(nblk, (unsigned)cn), kScreenThreads, 0, st>>>(s, rows + c0, lins + c0,
+                                                                     partial + c0 * nblk);
+  }
+  screen_reduce_kernel<<<(int)((ncand + 255) / 256), 256, 0, st>>>(partial, nblk, ncand, err,
+                                                                   minbits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rescore_compact(const double* err, int64_t ncand, double thr, int* sel,
+                                   unsigned long long* nsel, cudaStream_t st) {
+  if (ncand <= 0) return cudaSuccess;
+  rescore_compact_kernel<<<(int)((ncand + 255) / 256), 256, 0, st>>>(err, ncand, thr, sel, nsel);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact(const ScoreParams& s, const int64_t* rows, const int* lins, const int* sel,
+                         int64_t nsel, double* vals, double* out, cudaStream_t st) {
+  if (nsel <= 0) return cudaSuccess;
+  const int nblk = (s.n + kExactThreads - 1) / kExactThreads;
+  for (int64_t c0 = 0; c0 < nsel; c0 += 65535) {
+    const int64_t cn = std::min<int64_t>(65535, nsel - c0);
+    exact_points_kernel<<<dim3(nblk, (unsigned)cn), kExactThreads, 0, st>>>(s, rows, lins, sel,
+                                                                              c0, vals);
+  }
+  exact_sum_kernel<<<(int)((nsel + 127) / 128), 128, 0, st>>>(vals, s.n, nsel, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_winner(const double* err64, const int* sel, const int64_t* rows, int64_t nsel,
+                          double* best_err, int64_t* best_row, int* best_c, cudaStream_t st) {
+  winner_kernel<<<1, 1024, 0, st>>>(err64, sel, rows, nsel, best_err, best_row, best_c);
+  return cudaGetLastError();
+}
+
+}  // namespace dses

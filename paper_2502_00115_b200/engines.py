@@ -1,0 +1,177 @@
+"""DSES on the B200: the drop-in for gridreg.engines.dses (engines.py:229-301).
+
+``dses(source, reference, cfg)`` keeps the reference's signature, argument
+surface (``SearchConfig``: k_rot, rot_step, k_trans, trans_bin, q, metric,
+center, pose_cap), result type (``RegistrationResult``), exceptions and
+tie-break rules.  Everything after input validation runs on one GPU through
+the C ABI (include/dses_b200.h, ``dses_search``):
+
+  phase 1  vote kernel: per grid rotation, histogram mode of the translation
+           votes (counts / flat bin), rotations generated on device;
+  phase 2  M*, the q*M* cutoff (engines.py:196-201) and the kept-candidate
+           compaction;
+  phase 3  fp32 screen of the kept candidates, exact binary64 re-score of the
+           near-minimum ones, min-error / lexicographic-grid winner;
+  final    exact inlier count of the winner.
+
+The multi-GPU variant (rotation range sharded over ranks) is
+``paper_2502_00115_b200.distributed.dses_sharded``.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import InvalidInputError, NoCandidateError, SearchSpaceTooLargeError
+from .geometry import RigidTransform, as_point_cloud, check_grid_args, grid_index, grid_rotation, grid_tables
+from .metrics import ErrorMetric
+from .mode_search import bin_center, bin_index, check_key_space, decode_flat
+
+DEFAULT_POSE_CAP = 100_000_000  # engines.py:45
+CUTOFF_EPS = 1e-9               # engines.py:49
+
+
+@dataclass(frozen=True)
+class SearchConfig:
+    """Pose-grid geometry plus refinement policy (engines.py:52-98)."""
+
+    k_rot: int
+    rot_step: float
+    k_trans: int
+    trans_bin: float
+    q: float = 0.5
+    metric: ErrorMetric | None = None
+    center: RigidTransform | None = None
+    pose_cap: int = DEFAULT_POSE_CAP
+
+    def __post_init__(self):
+        for name in ("k_rot", "k_trans"):
+            v = getattr(self, name)
+            if int(v) != v or v < 0:
+                raise InvalidInputError(f"{name} must be a non-negative integer")
+            object.__setattr__(self, name, int(v))
+        for name in ("rot_step", "trans_bin"):
+            v = float(getattr(self, name))
+            if not (v > 0) or not math.isfinite(v):
+                raise InvalidInputError(f"{name} must be positive and finite")
+            object.__setattr__(self, name, v)
+        if not (0.0 < self.q <= 1.0):
+            raise InvalidInputError("q must lie in (0, 1]")
+        if self.metric is None:
+            object.__setattr__(self, "metric", ErrorMetric.truncated_l1(5.0 * self.trans_bin))
+        if self.pose_cap < 1:
+            raise InvalidInputError("pose_cap must be positive")
+
+    @property
+    def rotation_count(self) -> int:
+        return (2 * self.k_rot + 1) ** 3
+
+    @property
+    def translation_count(self) -> int:
+        return (2 * self.k_trans + 1) ** 3
+
+
+@dataclass(frozen=True)
+class PoseCandidate:
+    transform: RigidTransform
+    inlier_count: int
+    refined_error: float | None = None
+
+
+@dataclass(frozen=True)
+class RegistrationResult:
+    best: RigidTransform
+    best_error: float
+    best_inliers: int
+    candidates_evaluated: int
+    candidates_refined: int
+    elapsed: dict
+
+
+@dataclass
+class Prepared:
+    """Host-side preparation shared by the single- and multi-GPU drivers."""
+
+    x: np.ndarray
+    y: np.ndarray
+    cos_tab: np.ndarray
+    sin_tab: np.ndarray
+    center_rot: np.ndarray | None
+    ilo: np.ndarray
+    dims: np.ndarray
+    code: int
+    param: float
+    skip_refine: bool
+
+
+def prepare(source, reference, cfg: SearchConfig) -> Prepared:
+    """Validation and lattice set-up of engines.py:241-250 plus the grid
+    tables (geometry.py:259-275)."""
+    x = as_point_cloud(source)
+    y = as_point_cloud(reference)
+    if cfg.rotation_count > cfg.pose_cap:
+        raise SearchSpaceTooLargeError(
+            f"{cfg.rotation_count} rotations exceed the cap of {cfg.pose_cap}")
+    check_grid_args(cfg.k_rot, cfg.rot_step)
+    cos_tab, sin_tab = grid_tables(cfg.k_rot, cfg.rot_step)
+    if cfg.center is not None:
+        center_rot = np.ascontiguousarray(cfg.center.rotation, dtype=np.float64)
+        t_center = np.asarray(cfg.center.translation, dtype=np.float64)
+    else:
+        center_rot = None
+        t_center = np.zeros(3)
+    cbin = bin_index(t_center, cfg.trans_bin)
+    ilo = cbin - cfg.k_trans
+    dims = np.full(3, 2 * cfg.k_trans + 1, dtype=np.int64)
+    nbins = int(dims[0]) ** 3
+    check_key_space(nbins, x.shape[0])
+    if nbins > 2**31 - 1:
+        raise InvalidInputError("translation window exceeds 2^31 bins")
+    code, param = cfg.metric._code_param()
+    skip = cfg.metric.kind == "sat_l0" and cfg.metric.param == cfg.trans_bin  # engines.py:265
+    return Prepared(x, y, cos_tab, sin_tab, center_rot, ilo, dims, code, param, skip)
+
+
+def winner_transform(prep: Prepared, cfg: SearchConfig, row: int, lin: int) -> RigidTransform:
+    """engines.py:282-285: the winner's rotation, bin-centre translation and
+    grid coordinates."""
+    rot = grid_rotation(prep.cos_tab, prep.sin_tab, cfg.k_rot, row, prep.center_rot)
+    t = bin_center(decode_flat(lin, prep.ilo, prep.dims), cfg.trans_bin)
+    return RigidTransform(rot, t, grid_coords=tuple(grid_index(cfg.k_rot, row)))
+
+
+def dses(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationResult:
+    """Direct semi-exhaustive search on one B200 (engines.py:229-301)."""
+    from . import _native
+
+    t0 = time.perf_counter()
+    prep = prepare(source, reference, cfg)
+    grid = _native.make_grid(cfg.k_rot, prep.cos_tab, prep.sin_tab, prep.center_rot)
+    with _native.Plan(prep.x, prep.y, cfg.trans_bin, prep.ilo, prep.dims, device) as plan:
+        res = plan.search(grid, cfg.q, prep.code, prep.param, prep.skip_refine)
+    if res["candidates_evaluated"] == 0:
+        raise NoCandidateError(
+            "no rotation produced an in-bounds translation vote; widen k_trans "
+            "or move the search center")
+    best = winner_transform(prep, cfg, res["winner_row"], res["winner_lin"])
+    t_end = time.perf_counter()
+    ms = 1e-3
+    return RegistrationResult(
+        best=best,
+        best_error=float(res["best_error"]),
+        best_inliers=int(res["best_inliers"]),
+        candidates_evaluated=int(res["candidates_evaluated"]),
+        candidates_refined=int(res["candidates_refined"]),
+        elapsed={
+            "phase1": res["ms_vote"] * ms,
+            "sort": res["ms_select"] * ms,
+            "refine": (res["ms_total"] - res["ms_vote"] - res["ms_select"]) * ms,
+            "total": t_end - t0,
+            "device_total": res["ms_total"] * ms,
+            "stats": {k: res[k] for k in ("pairs_evaluated", "votes", "rechecks", "rescored",
+                                          "mstar")},
+        },
+    )

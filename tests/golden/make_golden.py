@@ -1,0 +1,246 @@
+"""Generate the golden fixtures that pin the CPU oracle (and, through it, the
+B200 kernels) to the UNMODIFIED reference implementation.
+
+Run in the build container only (it imports the reference read-only from
+/root/reference/pkg/src; nothing under tests/ reads /root/reference at test
+time):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Every array written here comes from the reference's own code path
+(`gridreg.benchgen.make_instance`, `gridreg.mode_search._mode_batch`,
+`gridreg.engines._score_poses`, `gridreg.engines.dses`, ...).  The
+outlier-injection step for config 3 follows SURVEY.md D4 / section 8(d)
+(the reference benchgen has none).
+"""
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+from gridreg import benchgen, engines, geometry, mode_search  # noqa: E402
+from gridreg.engines import SearchConfig  # noqa: E402
+from gridreg.metrics import ErrorMetric  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def inject_outliers(x, frac, seed):
+    """replace round(frac*N) source rows, chosen by
+    default_rng(SeedSequence([0x0071, seed])), with uniform samples in the
+    source bounding box."""
+    rng = np.random.default_rng(np.random.SeedSequence([0x0071, seed]))
+    x = x.copy()
+    n = x.shape[0]
+    k = int(round(frac * n))
+    rows = np.sort(rng.choice(n, size=k, replace=False))
+    lo, hi = x.min(axis=0), x.max(axis=0)
+    x[rows] = rng.uniform(lo, hi, (k, 3))
+    return x
+
+
+def votes(x, y, cfg):
+    grid, rots, t_center = engines._prepare(x, y, cfg)
+    cbin = mode_search.bin_index(t_center, cfg.trans_bin)
+    ilo = cbin - cfg.k_trans
+    dims = np.full(3, 2 * cfg.k_trans + 1, dtype=np.int64)
+    return mode_search._mode_batch(rots, x, y, cfg.trans_bin, ilo, dims)
+
+
+def dses_record(x, y, cfg, prefix, rec, with_votes=True):
+    res = engines.dses(x, y, cfg)
+    rec[f"{prefix}_R"] = np.asarray(res.best.rotation)
+    rec[f"{prefix}_t"] = np.asarray(res.best.translation)
+    rec[f"{prefix}_grid"] = np.asarray(res.best.grid_coords, dtype=np.int64)
+    rec[f"{prefix}_best_error"] = np.float64(res.best_error)
+    rec[f"{prefix}_best_inliers"] = np.int64(res.best_inliers)
+    rec[f"{prefix}_evaluated"] = np.int64(res.candidates_evaluated)
+    rec[f"{prefix}_refined"] = np.int64(res.candidates_refined)
+    if with_votes:
+        c, l, t = votes(x, y, cfg)
+        rec[f"{prefix}_counts"] = c.astype(np.int32)
+        rec[f"{prefix}_lins"] = l.astype(np.int32)
+        rec[f"{prefix}_ties"] = t.astype(np.int32)
+    print(f"  {prefix}: grid {res.best.grid_coords} err {res.best_error:.6g} "
+          f"inl {res.best_inliers} eval {res.candidates_evaluated} ref {res.candidates_refined}")
+
+
+def metric_fields(m: ErrorMetric):
+    return np.array(m.kind), np.float64(np.nan if m.param is None else m.param)
+
+
+def save(name, rec):
+    path = os.path.join(OUT, f"{name}.npz")
+    np.savez_compressed(path, **rec)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KB)")
+
+
+def cfg_fields(rec, prefix, cfg: SearchConfig):
+    rec[f"{prefix}_k_rot"] = np.int64(cfg.k_rot)
+    rec[f"{prefix}_rot_step"] = np.float64(cfg.rot_step)
+    rec[f"{prefix}_k_trans"] = np.int64(cfg.k_trans)
+    rec[f"{prefix}_trans_bin"] = np.float64(cfg.trans_bin)
+    rec[f"{prefix}_q"] = np.float64(cfg.q)
+    k, p = metric_fields(cfg.metric)
+    rec[f"{prefix}_metric_kind"] = k
+    rec[f"{prefix}_metric_param"] = p
+    if cfg.center is not None:
+        rec[f"{prefix}_center_R"] = np.asarray(cfg.center.rotation)
+        rec[f"{prefix}_center_t"] = np.asarray(cfg.center.translation)
+
+
+def make_c1():
+    """config 1: 1024-pt full / 512-pt partial, coarse grid, inliers metric."""
+    scn = benchgen.ScenarioConfig(shape="blob", points_pool=2048, points_reference=1024,
+                                  points_source=1024, keep_fraction=0.5, rng_seed=0)
+    inst = benchgen.make_instance(scn)
+    rec = {"x": inst.source, "y": inst.reference}
+    cfg = SearchConfig(k_rot=5, rot_step=math.radians(9.0), k_trans=20, trans_bin=0.025,
+                       metric=ErrorMetric.from_name("inliers", 0.025))
+    cfg_fields(rec, "a", cfg)
+    dses_record(inst.source, inst.reference, cfg, "a", rec)
+    save("c1", rec)
+
+
+def make_c2():
+    """config 2: ModelNet40-shaped 1024 / 717, medium grid (29,791 rotations),
+    truncated-L1 (reference default); plus the other metrics on a smaller grid."""
+    inst = benchgen.make_instance(benchgen.ScenarioConfig(rng_seed=0))
+    x, y = inst.source, inst.reference
+    rec = {"x": x, "y": y}
+    cfg = SearchConfig(k_rot=15, rot_step=math.radians(3.0), k_trans=20, trans_bin=0.025, q=0.5)
+    cfg_fields(rec, "a", cfg)
+    dses_record(x, y, cfg, "a", rec)
+    for tag, metric in (("l1", ErrorMetric.l1()), ("l2", ErrorMetric.l2()),
+                        ("sat2", ErrorMetric.saturated_l0(0.05)),
+                        ("inl", ErrorMetric.saturated_l0(0.025))):
+        cfg = SearchConfig(k_rot=4, rot_step=math.radians(5.0), k_trans=20, trans_bin=0.025,
+                           q=0.5, metric=metric)
+        cfg_fields(rec, tag, cfg)
+        dses_record(x, y, cfg, tag, rec, with_votes=(tag == "l1"))
+    # centre path (engines.py:120-130): rotations C @ G, window around C.t's bin
+    gt = inst.gt_aligner
+    cen = geometry.RigidTransform(
+        geometry.rotation_from_euler(np.array(gt.euler().as_array()) + np.radians([2.0, -1.0, 1.5])),
+        gt.translation + np.array([0.013, -0.021, 0.008]))
+    cfg = SearchConfig(k_rot=3, rot_step=math.radians(1.0), k_trans=6, trans_bin=0.025,
+                       center=cen)
+    cfg_fields(rec, "cen", cfg)
+    dses_record(x, y, cfg, "cen", rec)
+    save("c2", rec)
+
+
+def make_c3():
+    """config 3 (reduced grid): sigma 0.02, 20% outliers, L1."""
+    inst = benchgen.make_instance(benchgen.ScenarioConfig(noise_sigma=0.02, rng_seed=1))
+    x = inject_outliers(inst.source, 0.2, 1)
+    y = inst.reference
+    rec = {"x": x, "y": y}
+    cfg = SearchConfig(k_rot=6, rot_step=math.radians(1.0), k_trans=20, trans_bin=0.025,
+                       metric=ErrorMetric.l1())
+    cfg_fields(rec, "a", cfg)
+    dses_record(x, y, cfg, "a", rec)
+    save("c3", rec)
+
+
+def make_c4():
+    """config 4 (reduced grid): l-bracket 20k reference / 5k partial, 4 mm bins."""
+    scn = benchgen.ScenarioConfig(shape="l-bracket", points_pool=40000, points_reference=20000,
+                                  points_source=7143, keep_fraction=0.7, rot_range_deg=5.0,
+                                  trans_range=0.016, noise_sigma=0.002, noise_clip=0.01,
+                                  rng_seed=0)
+    inst = benchgen.make_instance(scn)
+    x, y = inst.source, inst.reference
+    rec = {"x": x, "y": y}
+    cfg = SearchConfig(k_rot=1, rot_step=math.radians(0.5), k_trans=4, trans_bin=0.004)
+    cfg_fields(rec, "a", cfg)
+    dses_record(x, y, cfg, "a", rec)
+    save("c4", rec)
+
+
+def make_small():
+    """Many small random cases for the vote kernel (dense and sparse lattice
+    paths, arbitrary rotations, bounds) and the refine kernel (all metrics)."""
+    rng = np.random.default_rng(20250200)
+    rec = {}
+    ncase = 0
+    for case in range(60):
+        n = int(rng.integers(1, 40))
+        m = int(rng.integers(1, 50))
+        x = rng.uniform(-1, 1, (n, 3))
+        y = rng.uniform(-1, 1, (m, 3))
+        if case % 3 == 0:   # shared structure so modes are non-trivial
+            rot = geometry.random_rotation(rng)
+            k = min(n, m)
+            y[:k] = x[:k] @ rot.T + rng.uniform(-0.3, 0.3, 3)
+        b = float(rng.uniform(0.03, 0.4))
+        rots = np.stack([geometry.random_rotation(rng) for _ in range(int(rng.integers(1, 6)))])
+        if case % 5 == 0:
+            rots[0] = np.eye(3)
+        kt = int(rng.integers(0, 30))
+        ilo = rng.integers(-5, 5, 3) - kt
+        dims = np.array([2 * kt + 1 + int(rng.integers(0, 3)) for _ in range(3)], dtype=np.int64)
+        counts, lins, ties = mode_search._mode_batch(rots, x, y, b, ilo, dims)
+        key = f"m{ncase}"
+        rec.update({f"{key}_x": x, f"{key}_y": y, f"{key}_rots": rots, f"{key}_b": np.float64(b),
+                    f"{key}_ilo": ilo.astype(np.int64), f"{key}_dims": dims,
+                    f"{key}_counts": counts, f"{key}_lins": lins, f"{key}_ties": ties})
+        ncase += 1
+    rec["n_mode_cases"] = np.int64(ncase)
+    # refine / alignment error cases (engines._score_poses -> refine_batch)
+    nref = 0
+    for case in range(24):
+        n = int(rng.integers(1, 30))
+        m = int(rng.integers(1, 40))
+        x = rng.uniform(-1, 1, (n, 3))
+        y = rng.uniform(-1, 1, (m, 3))
+        c = int(rng.integers(1, 8))
+        rots = np.stack([geometry.random_rotation(rng) for _ in range(c)])
+        ts = rng.uniform(-0.3, 0.3, (c, 3))
+        kind = ["l2", "l1", "trunc_l1", "sat_l0"][case % 4]
+        metric = ErrorMetric(kind, None if kind in ("l2", "l1") else float(rng.uniform(0.1, 0.6)))
+        errs = engines._score_poses(rots, ts, x, y, metric)
+        key = f"r{nref}"
+        code, param = metric._code_param()
+        rec.update({f"{key}_x": x, f"{key}_y": y, f"{key}_rots": rots, f"{key}_ts": ts,
+                    f"{key}_code": np.int64(code), f"{key}_param": np.float64(param),
+                    f"{key}_errs": errs})
+        nref += 1
+    rec["n_refine_cases"] = np.int64(nref)
+    # end-to-end small dses cases (tests/test_engines.py-style shapes)
+    nd = 0
+    for case in range(16):
+        n = int(rng.integers(3, 25))
+        x = rng.uniform(-1, 1, (n, 3))
+        if case % 2 == 0:
+            ridx = rng.integers(-1, 2, 3)
+            tidx = rng.integers(-2, 3, 3)
+            tf = geometry.RigidTransform(geometry.rotation_from_euler(ridx.astype(float) * 0.3),
+                                         tidx.astype(float) * 0.25)
+            y = tf.apply(x) + rng.normal(0.0, 0.01, (n, 3))
+        else:
+            y = rng.uniform(-1, 1, (int(rng.integers(3, 25)), 3))
+        kind = ["trunc_l1", "l1", "l2", "sat_l0"][case % 4]
+        metric = None if kind == "trunc_l1" else ErrorMetric(kind, 0.25 if kind == "sat_l0" else None)
+        cfg = SearchConfig(k_rot=1, rot_step=0.3, k_trans=3, trans_bin=0.25,
+                           q=[0.5, 1.0, 1e-9, 0.3][case % 4], metric=metric)
+        key = f"d{nd}"
+        rec.update({f"{key}_x": x, f"{key}_y": y})
+        cfg_fields(rec, key, cfg)
+        dses_record(x, y, cfg, key, rec, with_votes=True)
+        nd += 1
+    rec["n_dses_cases"] = np.int64(nd)
+    save("small", rec)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4"]
+    for w in which:
+        print(w)
+        globals()[f"make_{w}"]()
