@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""DSES throughput on B200: rotation candidates/s and registrations/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+One step = one full DSES registration (phase 1 vote over every grid rotation,
+phase 2 selection, phase 3 screen + exact re-score, winner inlier count) of one
+synthetic ModelNet40-shaped pair.  Default workload = BASELINE.json configs[1]
+(SURVEY.md 8(d) c2): 1024-pt reference / 717-pt partial, k_rot=15 @ 3 deg
+(29,791 rotations), k_trans=20 @ 25 mm (41^3 bins), truncated-L1 at 5 bins.
+
+Under torchrun every rank registers its own pairs (replicas, weak scaling, no
+data-path collective); the timed region is bracketed by a
+barrier + synchronize, timed with CUDA events on the launching stream, and the
+max over ranks is reported.  Rank 0 prints ONE JSON line.
+
+`--impl reference` times the CPU oracle (oracle/, the C restatement of the
+reference's numba kernels, all host threads) on a bounded sample of the same
+workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rotation_candidates_per_sec"
+UNIT = "rot/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--metric", default=None, help="override the config's metric name")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=6.0,
+                    help="wall-clock budget of the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(name, metric_override=None):
+    from paper_2502_00115_b200.synth import CONFIGS
+    c = dict(CONFIGS[name])
+    if metric_override:
+        c["metric"] = metric_override
+    return c
+
+
+def search_config(c):
+    from paper_2502_00115_b200 import ErrorMetric, SearchConfig
+    metric = ErrorMetric.from_name(c["metric"], c["trans_bin"])
+    return SearchConfig(k_rot=c["k_rot"], rot_step=math.radians(c["rot_step_deg"]),
+                        k_trans=c["k_trans"], trans_bin=c["trans_bin"], metric=metric)
+
+
+def describe(name, c, cfg, n, m):
+    return (f"{name}: synthetic ModelNet40-shaped pair, {m}-pt reference / {n}-pt partial source, "
+            f"k_rot={c['k_rot']} @ {c['rot_step_deg']} deg ({cfg.rotation_count} rotations), "
+            f"k_trans={c['k_trans']} @ {c['trans_bin'] * 1000:g} mm ({2 * c['k_trans'] + 1}^3 bins), "
+            f"metric {cfg.metric.kind}" + (f" (param {cfg.metric.param:g})" if cfg.metric.param else ""))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"dses_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [v.strip() for v in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": max(smax),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def cpu_baseline(x, y, cfg, c, budget_s, gpu_check=None):
+    """Oracle C port (all host threads) on a contiguous slice of the grid."""
+    from oracle import oracle as O
+    nthreads = O.max_threads()
+    ilo = np.full(3, -cfg.k_trans, dtype=np.int64)
+    dims = np.full(3, 2 * cfg.k_trans + 1, dtype=np.int64)
+    grid = (cfg.k_rot, cfg.rot_step, None)
+    total = cfg.rotation_count
+    t0 = time.perf_counter()
+    cal = min(total, 8 * nthreads)
+    O.mode_batch(x, y, cfg.trans_bin, ilo, dims, grid=grid, r_begin=0, r_count=cal,
+                 nthreads=nthreads)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    sample = int(min(total, max(cal, budget_s * cal / dt)))
+    t0 = time.perf_counter()
+    counts, lins, ties = O.mode_batch(x, y, cfg.trans_bin, ilo, dims, grid=grid, r_begin=0,
+                                      r_count=sample, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    rate = sample / dt
+    out = {"value": rate, "unit": UNIT, "cores": nthreads, "kind": "port",
+           "sample": (f"phase 1 (vote, {100 * 0.998:.1f}% of reference time, SURVEY.md 3) over "
+                      f"rotations [0, {sample}) of {total} of the step-0 pair, {dt:.2f} s wall; "
+                      f"registrations/s extrapolated = value / {total}"),
+           "registrations_per_sec_extrapolated": rate / total}
+    if gpu_check is not None:
+        g_counts, g_lins, g_ties = gpu_check(sample)
+        out["gpu_parity_on_sample"] = bool(np.array_equal(g_counts, counts)
+                                           and np.array_equal(g_lins, lins)
+                                           and np.array_equal(g_ties, ties))
+    return out
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, ROOT)
+    from paper_2502_00115_b200.synth import make_pair
+    c = workload(args.config, args.metric)
+    cfg = search_config(c)
+    x, y, _ = make_pair(c["spec"], 0)
+    from oracle import oracle as O
+    nthreads = O.max_threads()
+    ilo = np.full(3, -cfg.k_trans, dtype=np.int64)
+    dims = np.full(3, 2 * cfg.k_trans + 1, dtype=np.int64)
+    total = cfg.rotation_count
+    # size one step's sample so the whole --steps/--warmup run stays ~1-2 minutes
+    t0 = time.perf_counter()
+    cal = min(total, 8 * nthreads)
+    O.mode_batch(x, y, cfg.trans_bin, ilo, dims, grid=(cfg.k_rot, cfg.rot_step, None),
+                 r_count=cal, nthreads=nthreads)
+    per_rot = max(time.perf_counter() - t0, 1e-6) / cal
+    per_step_s = min(10.0, 90.0 / max(1, args.steps + args.warmup))
+    sample = int(max(nthreads, min(total, per_step_s / per_rot)))
+    times = []
+    for s in range(args.warmup + args.steps):
+        r0 = (s * sample) % max(1, total - sample + 1)
+        t0 = time.perf_counter()
+        O.mode_batch(x, y, cfg.trans_bin, ilo, dims, grid=(cfg.k_rot, cfg.rot_step, None),
+                     r_begin=r0, r_count=sample, nthreads=nthreads)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = sample * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": describe(args.config, c, cfg, x.shape[0], y.shape[0]),
+                   "metric": cfg.metric.kind, "l2_flush": "n/a (CPU)"},
+        "registrations_per_sec": value / total,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": f"each step: phase 1 over {sample} consecutive rotations of "
+                                   f"{total} (oracle/gridreg_oracle.c, the C restatement of the "
+                                   f"reference numba kernels); registrations/s = value / {total}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2502_00115_b200 import _native, dses
+    from paper_2502_00115_b200.engines import prepare
+    from paper_2502_00115_b200.synth import make_pair
+
+    c = workload(args.config, args.metric)
+    cfg = search_config(c)
+    nsteps = args.warmup + args.steps
+    pairs = [make_pair(c["spec"], 1000 * rank + s) for s in range(nsteps)]
+    stream = torch.cuda.current_stream().cuda_stream
+
+    # ---- device-resident value: plans (clouds in HBM) built before timing
+    preps = [prepare(x, y, cfg) for x, y, _ in pairs]
+    plans = [_native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims, local) for p in preps]
+    grids = [_native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot) for p in preps]
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def one(s):
+        p = preps[s]
+        plans[s].traffic(reset=True)
+        return plans[s].search(grids[s], cfg.q, p.code, p.param, p.skip_refine, stream=stream)
+
+    for s in range(args.warmup):
+        one(s)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    results = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            flush.zero_()  # evict L2 between timed steps (outside the events)
+            starts[k].record()
+            results.append(one(args.warmup + k))
+            ends[k].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    vote_ms = sum(r["ms_vote_kernel"] for r in results)
+    pairs_eval = sum(r["pairs_evaluated"] for r in results)
+    launches = sum(r["launches"] for r in results)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    R = cfg.rotation_count
+    value = args.steps * R * world / (ms_max * 1e-3)
+
+    # ---- end to end through the public API with host buffers
+    e2e_pairs = [make_pair(c["spec"], 1000 * rank + 500 + s) for s in range(args.steps)]
+    dses(e2e_pairs[0][0], e2e_pairs[0][1], cfg, device=local)  # warm
+    torch.cuda.synchronize()
+    e_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    h2d = d2h = 0
+    if world > 1:
+        dist.barrier()
+    for k in range(args.steps):
+        flush.zero_()
+        e_start[k].record()
+        res = dses(e2e_pairs[k][0], e2e_pairs[k][1], cfg, device=local)
+        e_end[k].record()
+        st = res.elapsed["stats"]
+        h2d += st["h2d_bytes"]
+        d2h += st["d2h_bytes"]
+    torch.cuda.synchronize()
+    e_ms = sum(a.elapsed_time(b) for a, b in zip(e_start, e_end))
+    te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e_value = args.steps * R * world / (float(te.item()) * 1e-3)
+
+    if rank == 0:
+        ffma_s, _ = _native.probe_fp32_peak(local)
+        n_src = preps[0].x.shape[0]
+        flops = 2.0 * (3.0 * pairs_eval + 9.0 * R * n_src * args.steps)
+        achieved = flops / (vote_ms * 1e-3) / 1e12
+        peak = 2.0 * ffma_s / 1e12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", f"ncu_vote_{args.config}.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            except (OSError, ValueError):
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "i32 fixed-point vote / f32 screen / f64 exact",
+            "data": "synthetic (seeded ModelNet40-shaped pairs, paper_2502_00115_b200/synth.py)",
+            "config": {"workload": describe(args.config, c, cfg, n_src, preps[0].y.shape[0]),
+                       "metric": cfg.metric.kind, "rotations": R,
+                       "parallelism": f"replicas x{world} (registrations sharded, no collective)",
+                       "l2_flush": "512 MiB buffer zeroed between timed steps"},
+            "registrations_per_sec": args.steps * world / (ms_max * 1e-3),
+            "e2e": {"value": e_value, "unit": UNIT,
+                    "registrations_per_sec": args.steps * world / (float(te.item()) * 1e-3),
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                    "path": "paper_2502_00115_b200.dses(numpy source, numpy reference, SearchConfig)"},
+            "gpu_launches": launches,
+            "roofline": {"bound": "fp32", "kernel": "vote_kernel", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": traffic,
+                         "algorithmic": "2*(3 FFMA per evaluated (rotation,i,j) pair + 9 per "
+                                        "(rotation,i)) / vote-kernel time (SURVEY.md 8(d))",
+                         "peak_source": "live FFMA probe on this GPU (MEASURED_PEAKS.json has no FP32)",
+                         "pairs_evaluated_per_step": pairs_eval / args.steps,
+                         "nominal_pairs_per_step": R * n_src * preps[0].y.shape[0],
+                         "vote_kernel_ms_per_step": vote_ms / args.steps},
+            "stages_ms_per_step": {
+                "vote": sum(r["ms_vote"] for r in results) / args.steps,
+                "select": sum(r["ms_select"] for r in results) / args.steps,
+                "score": sum(r["ms_score"] for r in results) / args.steps,
+                "total_device": sum(r["ms_total"] for r in results) / args.steps},
+            "winner_example": {"row": results[0]["winner_row"], "count": results[0]["winner_count"],
+                               "refined": results[0]["candidates_refined"],
+                               "rescored": results[0]["rescored"]},
+            "clocks": clocks.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            x0, y0, _ = pairs[0]
+
+            def gpu_check(sample):
+                return plans[0].mode_grid(grids[0], 0, sample)
+
+            line["cpu_baseline"] = cpu_baseline(x0, y0, cfg, c, args.cpu_seconds, gpu_check)
+        print(json.dumps(line), flush=True)
+    for p in plans:
+        p.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -11,9 +11,9 @@
  *   dses_mode_dense_batch  <- _kernels.mode_dense_batch   (_kernels.py:173-193)
  *                             (and mode_sparse_batch, _kernels.py:277-294:
  *                             same outputs for any lattice size)
- *   dses_refine_batch      <- _kernels.refine_batch       (_kernels.py:297-324)
- *   dses_alignment_error   <- _kernels.alignment_error_kernel (_kernels.py:83-89)
- *                             applied after RigidTransform.apply (metrics.py:133-140)
+ *   dses_refine_batch      <- _kernels.refine_batch       (_kernels.py:297-324); with one
+ *                             pose it is alignment_error_kernel (_kernels.py:83-89)
+ *                             after RigidTransform.apply (metrics.py:133-140)
  *   dses_plan_* + dses_search / dses_stage_*
  *                          <- engines.dses                (engines.py:229-301),
  *                             split into the stages a multi-GPU caller needs
@@ -76,6 +76,9 @@ typedef struct {
   int64_t votes;                /* deduplicated in-window votes (histogram increments) */
   int64_t rechecks;             /* pairs re-binned in fp64 (fixed-point guard band) */
   double ms_vote, ms_select, ms_score, ms_total; /* device time per stage (CUDA events) */
+  double ms_vote_kernel;        /* the vote kernel alone (events around its launch) */
+  int64_t launches;             /* kernels this plan launched since its counters were reset */
+  int64_t h2d_bytes, d2h_bytes; /* host<->device bytes copied for this plan since the reset */
 } dses_result;
 
 const char* dses_last_error(void);
@@ -145,6 +148,15 @@ int dses_pose_error(dses_plan* plan, const dses_grid* grid, int64_t row, int64_t
                     int metric_code, double metric_param, double* err, void* stream);
 /* Kernel statistics accumulated since the last call (pairs, votes, rechecks). */
 int dses_stage_stats(dses_plan* plan, int64_t* pairs, int64_t* votes, int64_t* rechecks);
+/* Host<->device bytes and kernel launches attributed to this plan (plan
+ * creation included); reset != 0 zeroes the counters after reading. */
+int dses_plan_traffic(dses_plan* plan, int64_t* h2d_bytes, int64_t* d2h_bytes, int64_t* launches,
+                      int reset);
+
+/* ---- measurement ---------------------------------------------------------- */
+/* FP32 FFMA throughput of `device` measured live (independent FFMA chains on
+ * every SM, CUDA events): the roofline denominator bench.py reports against. */
+int dses_probe_fp32_peak(int device, double* ffma_per_s, double* ms);
 
 #ifdef __cplusplus
 }

@@ -174,14 +174,16 @@ static void mode_dense_one(const double* rot, const double* x, int64_t n, const 
       const double q2 = (y2[j] - p2) * inv_bin;
       const double f2 = copysign(floor(fabs(q2) + 0.5), q2) - flo2;
       const int ok = (f0 >= 0.0) & (f0 < fd0) & (f1 >= 0.0) & (f1 < fd1) & (f2 >= 0.0) & (f2 < fd2);
-      linf[j] = ok ? (f0 * fd1 + f1) * fd2 + f2 : dump;
+      const double v = (f0 * fd1 + f1) * fd2 + f2;
+      linf[j] = ok ? v : dump;
     }
+    /* _kernels.py:153-158, branch-free: `last[lin] = i` is a no-op when it
+     * already holds i, and the dump slot (lin == nbins) is never read back. */
     for (int64_t j = jlo; j < jhi; ++j) {
       const int64_t lin = (int64_t)linf[j];
-      if (last[lin] != (int32_t)i) {
-        last[lin] = (int32_t)i;
-        if (lin < nbins) counts[lin] += 1;
-      }
+      const int32_t prev = last[lin];
+      last[lin] = (int32_t)i;
+      counts[lin] += (prev != (int32_t)i);
     }
   }
   int64_t best = 0, best_lin = -1, ties = 0;

@@ -49,6 +49,8 @@ class Result(ctypes.Structure):
         ("pairs_evaluated", _i64), ("votes", _i64), ("rechecks", _i64),
         ("ms_vote", ctypes.c_double), ("ms_select", ctypes.c_double),
         ("ms_score", ctypes.c_double), ("ms_total", ctypes.c_double),
+        ("ms_vote_kernel", ctypes.c_double), ("launches", _i64), ("h2d_bytes", _i64),
+        ("d2h_bytes", _i64),
     ]
 
     def as_dict(self):
@@ -83,6 +85,8 @@ _SIGS = [
     ("dses_pose_error", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, ctypes.c_int,
                                        ctypes.c_double, _dp, _vp]),
     ("dses_stage_stats", ctypes.c_int, [_vp, _ip, _ip, _ip]),
+    ("dses_plan_traffic", ctypes.c_int, [_vp, _ip, _ip, _ip, ctypes.c_int]),
+    ("dses_probe_fp32_peak", ctypes.c_int, [ctypes.c_int, _dp, _dp]),
 ]
 EXPORTED = tuple(name for name, _, _ in _SIGS)
 
@@ -133,6 +137,14 @@ def device_count() -> int:
     n = ctypes.c_int(0)
     rc = load().dses_device_count(ctypes.byref(n))
     return n.value if rc == DSES_OK else 0
+
+
+def probe_fp32_peak(device: int = 0):
+    """Live FFMA/s of the device (independent FFMA chains on every SM)."""
+    f, ms = ctypes.c_double(), ctypes.c_double()
+    check(load().dses_probe_fp32_peak(int(device), ctypes.byref(f), ctypes.byref(ms)),
+          "dses_probe_fp32_peak")
+    return f.value, ms.value
 
 
 def dptr(a: np.ndarray):
@@ -269,6 +281,12 @@ class Plan:
         check(self._L.dses_pose_error(self._h, ctypes.byref(grid), int(row), int(lin), int(code),
                                       float(param), ctypes.byref(e), stream), "dses_pose_error")
         return e.value
+
+    def traffic(self, reset=False):
+        v = [ctypes.c_int64() for _ in range(3)]
+        check(self._L.dses_plan_traffic(self._h, *[ctypes.byref(a) for a in v], int(reset)),
+              "dses_plan_traffic")
+        return {"h2d_bytes": v[0].value, "d2h_bytes": v[1].value, "launches": v[2].value}
 
     def stats(self):
         v = [ctypes.c_int64() for _ in range(3)]

@@ -107,11 +107,30 @@ struct DevBuf {
   void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
 };
 
+// host<->device traffic is counted per plan (bench.py reports it as e2e bytes)
+struct Traffic {
+  int64_t h2d = 0, d2h = 0, launches = 0;
+};
+static thread_local Traffic* g_traffic = nullptr;
+
+static cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (g_traffic) g_traffic->h2d += (int64_t)bytes;
+  return h2d(dst, src, bytes, st);
+}
+static cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (g_traffic) g_traffic->d2h += (int64_t)bytes;
+  return d2h(dst, src, bytes, st);
+}
+static inline cudaError_t launched(cudaError_t e, int n = 1) {
+  if (g_traffic) g_traffic->launches += n;
+  return e;
+}
+
 template <class T>
 static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
   cudaError_t e = b.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
   if (e != cudaSuccess || v.empty()) return e;
-  return cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st);
+  return h2d(b.p, v.data(), sizeof(T) * v.size(), st);
 }
 
 // ---------------------------------------------------------------------------
@@ -143,6 +162,15 @@ struct dses_plan {
   RotSource cur_rot{};
   int64_t kept = 0;
   cudaEvent_t ev[8];
+  Traffic traffic;       // counters since the last dses_stage_stats / dses_search
+  bool vote_timed = false;
+};
+
+// RAII: route the copy/launch counters of this call to the plan
+struct TrafficScope {
+  Traffic* prev;
+  explicit TrafficScope(dses_plan* P) : prev(g_traffic) { g_traffic = P ? &P->traffic : nullptr; }
+  ~TrafficScope() { g_traffic = prev; }
 };
 
 namespace {
@@ -374,8 +402,8 @@ int set_grid(dses_plan* P, const dses_grid* g, RotSource* rs, cudaStream_t st) {
   const size_t nt = (size_t)(2 * g->k + 1);
   CK(P->cth.ensure(nt * 8));
   CK(P->sth.ensure(nt * 8));
-  CK(cudaMemcpyAsync(P->cth.p, g->cos_tab, nt * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(P->sth.p, g->sin_tab, nt * 8, cudaMemcpyHostToDevice, st));
+  CK(h2d(P->cth.p, g->cos_tab, nt * 8, st));
+  CK(h2d(P->sth.p, g->sin_tab, nt * 8, st));
   rs->cth = P->cth.as<double>();
   rs->sth = P->sth.as<double>();
   rs->rots = nullptr;
@@ -415,7 +443,10 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
       v.p_global = P->p_g.as<int4>();
     }
   }
-  CK(launch_vote(v, P->hsmem, P->psmem, grid, P->vote_threads, st));
+  CK(cudaEventRecord(P->ev[5], st));
+  CK(launched(launch_vote(v, P->hsmem, P->psmem, grid, P->vote_threads, st)));
+  CK(cudaEventRecord(P->ev[6], st));
+  P->vote_timed = true;
   return DSES_OK;
 }
 
@@ -484,6 +515,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
   P->inv_bin = 1.0 / bin_size;  // mode_search.py:158 (inv_bin = 1.0 / bin_size)
   for (int k = 0; k < 3; ++k) { P->ilo[k] = ilo[k]; P->dims[k] = dims[k]; }
   for (auto& e : P->ev) cudaEventCreate(&e);
+  TrafficScope ts_(P);
   const int rc = build_plan(P, x, y);
   if (rc != DSES_OK) { dses_plan_destroy(P); return rc; }
   *out = P;
@@ -519,9 +551,9 @@ static int fetch_modes(dses_plan* P, int64_t nrot, int64_t* counts, int64_t* lin
                        cudaStream_t st) {
   std::vector<int> c(nrot), l(nrot), t(nrot);
   if (nrot > 0) {
-    CK(cudaMemcpyAsync(c.data(), P->counts.p, 4 * nrot, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(l.data(), P->lins.p, 4 * nrot, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(t.data(), P->ties.p, 4 * nrot, cudaMemcpyDeviceToHost, st));
+    CK(d2h(c.data(), P->counts.p, 4 * nrot, st));
+    CK(d2h(l.data(), P->lins.p, 4 * nrot, st));
+    CK(d2h(t.data(), P->ties.p, 4 * nrot, st));
   }
   CK(cudaStreamSynchronize(st));
   for (int64_t r = 0; r < nrot; ++r) {
@@ -534,11 +566,12 @@ static int fetch_modes(dses_plan* P, int64_t nrot, int64_t* counts, int64_t* lin
 
 extern "C" int dses_mode_batch(dses_plan* P, const double* rots, int64_t nrot, int64_t* counts,
                                int64_t* lins, int64_t* ties, void* stream) {
+  TrafficScope ts_(P);
   if (!P || (!rots && nrot > 0) || nrot < 0) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
   CK(P->rots.ensure(sizeof(double) * 9 * std::max<int64_t>(nrot, 1)));
-  if (nrot > 0) CK(cudaMemcpyAsync(P->rots.p, rots, sizeof(double) * 9 * nrot, cudaMemcpyHostToDevice, st));
+  if (nrot > 0) CK(h2d(P->rots.p, rots, sizeof(double) * 9 * nrot, st));
   RotSource rs{};
   rs.rots = P->rots.as<double>();
   int rc = run_vote(P, rs, 0, nrot, st);
@@ -548,6 +581,7 @@ extern "C" int dses_mode_batch(dses_plan* P, const double* rots, int64_t nrot, i
 
 extern "C" int dses_mode_grid(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t nrot,
                               int64_t* counts, int64_t* lins, int64_t* ties, void* stream) {
+  TrafficScope ts_(P);
   if (!P || nrot < 0 || r_begin < 0) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -575,6 +609,7 @@ extern "C" int dses_mode_dense_batch(int device, const double* rots, int64_t nro
 
 extern "C" int dses_refine_batch(dses_plan* P, const double* rots, const double* ts, int64_t ncand,
                                  int code, double param, double* out, void* stream) {
+  TrafficScope ts_(P);
   if (!P || ncand < 0 || (ncand > 0 && (!rots || !ts || !out)) || code < 0 || code > 4)
     return fail(DSES_E_INVALID, "bad arguments");
   if (ncand == 0) return DSES_OK;
@@ -589,17 +624,18 @@ extern "C" int dses_refine_batch(dses_plan* P, const double* rots, const double*
   std::vector<int64_t> rows(ncand);
   std::iota(rows.begin(), rows.end(), 0);
   std::vector<int> zeros(ncand, 0);
-  CK(cudaMemcpyAsync(P->rots.p, rots, sizeof(double) * 9 * ncand, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(P->tvec.p, ts, sizeof(double) * 3 * ncand, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(P->tmp_rows.p, rows.data(), sizeof(int64_t) * ncand, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(P->tmp_lins.p, zeros.data(), sizeof(int) * ncand, cudaMemcpyHostToDevice, st));
+  CK(h2d(P->rots.p, rots, sizeof(double) * 9 * ncand, st));
+  CK(h2d(P->tvec.p, ts, sizeof(double) * 3 * ncand, st));
+  CK(h2d(P->tmp_rows.p, rows.data(), sizeof(int64_t) * ncand, st));
+  CK(h2d(P->tmp_lins.p, zeros.data(), sizeof(int) * ncand, st));
   RotSource rs{};
   rs.rots = P->rots.as<double>();
   ScoreParams s = score_params(P, rs, code, param);
   s.tvec = P->tvec.as<double>();
-  CK(launch_exact(s, P->tmp_rows.as<int64_t>(), P->tmp_lins.as<int>(), nullptr, ncand,
-                  P->vals.as<double>(), P->err64.as<double>(), st));
-  CK(cudaMemcpyAsync(out, P->err64.p, sizeof(double) * ncand, cudaMemcpyDeviceToHost, st));
+  CK(launched(launch_exact(s, P->tmp_rows.as<int64_t>(), P->tmp_lins.as<int>(), nullptr, ncand,
+                           P->vals.as<double>(), P->err64.as<double>(), st),
+              (int)((ncand + 65534) / 65535) + 1));
+  CK(d2h(out, P->err64.p, sizeof(double) * ncand, st));
   CK(cudaStreamSynchronize(st));
   return DSES_OK;
 }
@@ -607,6 +643,7 @@ extern "C" int dses_refine_batch(dses_plan* P, const double* rots, const double*
 // ---- stages -------------------------------------------------------------
 extern "C" int dses_stage_vote(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t r_count,
                                int64_t* mstar_local, int64_t* valid_local, void* stream) {
+  TrafficScope ts_(P);
   if (!P || !g) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -621,9 +658,9 @@ extern "C" int dses_stage_vote(dses_plan* P, const dses_grid* g, int64_t r_begin
   if (rc) return rc;
   unsigned long long* sc = P->scal.as<unsigned long long>();
   CK(cudaMemsetAsync(sc, 0, 2 * sizeof(unsigned long long), st));
-  if (r_count > 0) CK(launch_select_stats(P->counts.as<int>(), r_count, sc, sc + 1, P->sms, st));
+  if (r_count > 0) CK(launched(launch_select_stats(P->counts.as<int>(), r_count, sc, sc + 1, P->sms, st)));
   unsigned long long h[2];
-  CK(cudaMemcpyAsync(h, sc, sizeof h, cudaMemcpyDeviceToHost, st));
+  CK(d2h(h, sc, sizeof h, st));
   CK(cudaStreamSynchronize(st));
   if (mstar_local) *mstar_local = (int64_t)h[0];
   if (valid_local) *valid_local = (int64_t)h[1];
@@ -631,16 +668,17 @@ extern "C" int dses_stage_vote(dses_plan* P, const dses_grid* g, int64_t r_begin
 }
 
 extern "C" int dses_stage_argmax(dses_plan* P, int64_t mstar_global, int64_t* row_local, void* stream) {
+  TrafficScope ts_(P);
   if (!P || !row_local) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* sc = P->scal.as<unsigned long long>() + 2;
   CK(cudaMemsetAsync(sc, 0xff, sizeof(unsigned long long), st));
   if (P->cur_r_count > 0)
-    CK(launch_argmax(P->counts.as<int>(), P->cur_r_count, P->cur_r_begin, (int)mstar_global, sc,
-                     P->sms, st));
+    CK(launched(launch_argmax(P->counts.as<int>(), P->cur_r_count, P->cur_r_begin,
+                              (int)mstar_global, sc, P->sms, st)));
   unsigned long long h;
-  CK(cudaMemcpyAsync(&h, sc, sizeof h, cudaMemcpyDeviceToHost, st));
+  CK(d2h(&h, sc, sizeof h, st));
   CK(cudaStreamSynchronize(st));
   *row_local = h == ~0ull ? INT64_MAX : (int64_t)h;
   return DSES_OK;
@@ -649,6 +687,7 @@ extern "C" int dses_stage_argmax(dses_plan* P, int64_t mstar_global, int64_t* ro
 extern "C" int dses_stage_screen(dses_plan* P, double q, int64_t mstar_global, int code,
                                  double param, int64_t* kept_local, double* min32_local, double* tol,
                                  void* stream) {
+  TrafficScope ts_(P);
   if (!P || code < 0 || code > 4) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -660,10 +699,10 @@ extern "C" int dses_stage_screen(dses_plan* P, double q, int64_t mstar_global, i
   unsigned long long* sc = P->scal.as<unsigned long long>() + 3;
   CK(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), st));
   if (nr > 0)
-    CK(launch_compact(P->counts.as<int>(), P->lins.as<int>(), nr, P->cur_r_begin, cutoff,
-                      P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), sc, P->sms, st));
+    CK(launched(launch_compact(P->counts.as<int>(), P->lins.as<int>(), nr, P->cur_r_begin, cutoff,
+                               P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), sc, P->sms, st)));
   unsigned long long kept;
-  CK(cudaMemcpyAsync(&kept, sc, sizeof kept, cudaMemcpyDeviceToHost, st));
+  CK(d2h(&kept, sc, sizeof kept, st));
   CK(cudaStreamSynchronize(st));
   P->kept = (int64_t)kept;
   if (kept_local) *kept_local = (int64_t)kept;
@@ -678,10 +717,11 @@ extern "C" int dses_stage_screen(dses_plan* P, double q, int64_t mstar_global, i
   unsigned long long* mb = P->scal.as<unsigned long long>() + 4;
   CK(cudaMemsetAsync(mb, 0x7f, sizeof(unsigned long long), st));
   ScoreParams s = score_params(P, P->cur_rot, code, param);
-  CK(launch_screen(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), (int64_t)kept,
-                   P->partial.as<double>(), P->err32.as<double>(), mb, st));
+  CK(launched(launch_screen(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), (int64_t)kept,
+                            P->partial.as<double>(), P->err32.as<double>(), mb, st),
+              (int)((kept + 65534) / 65535) + 1));
   double mn;
-  CK(cudaMemcpyAsync(&mn, mb, sizeof mn, cudaMemcpyDeviceToHost, st));
+  CK(d2h(&mn, mb, sizeof mn, st));
   CK(cudaStreamSynchronize(st));
   if (min32_local) *min32_local = mn;
   return DSES_OK;
@@ -690,6 +730,7 @@ extern "C" int dses_stage_screen(dses_plan* P, double q, int64_t mstar_global, i
 extern "C" int dses_stage_rescore(dses_plan* P, double threshold, int code, double param,
                                   double* err_local, int64_t* row_local, int64_t* rescored,
                                   void* stream) {
+  TrafficScope ts_(P);
   if (!P || code < 0 || code > 4) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -700,9 +741,9 @@ extern "C" int dses_stage_rescore(dses_plan* P, double threshold, int code, doub
   CK(P->sel.ensure(sizeof(int) * P->kept));
   unsigned long long* ns = P->scal.as<unsigned long long>() + 5;
   CK(cudaMemsetAsync(ns, 0, sizeof(unsigned long long), st));
-  CK(launch_rescore_compact(P->err32.as<double>(), P->kept, threshold, P->sel.as<int>(), ns, st));
+  CK(launched(launch_rescore_compact(P->err32.as<double>(), P->kept, threshold, P->sel.as<int>(), ns, st)));
   unsigned long long nsel;
-  CK(cudaMemcpyAsync(&nsel, ns, sizeof nsel, cudaMemcpyDeviceToHost, st));
+  CK(d2h(&nsel, ns, sizeof nsel, st));
   CK(cudaStreamSynchronize(st));
   if (rescored) *rescored = (int64_t)nsel;
   if (nsel == 0) return DSES_OK;
@@ -712,15 +753,16 @@ extern "C" int dses_stage_rescore(dses_plan* P, double threshold, int code, doub
   CK(P->win_row.ensure(sizeof(int64_t)));
   CK(P->win_c.ensure(sizeof(int)));
   ScoreParams s = score_params(P, P->cur_rot, code, param);
-  CK(launch_exact(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->sel.as<int>(),
-                  (int64_t)nsel, P->vals.as<double>(), P->err64.as<double>(), st));
-  CK(launch_winner(P->err64.as<double>(), P->sel.as<int>(), P->cand_rows.as<int64_t>(),
-                   (int64_t)nsel, P->win_err.as<double>(), P->win_row.as<int64_t>(),
-                   P->win_c.as<int>(), st));
+  CK(launched(launch_exact(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->sel.as<int>(),
+                           (int64_t)nsel, P->vals.as<double>(), P->err64.as<double>(), st),
+              (int)((nsel + 65534) / 65535) + 1));
+  CK(launched(launch_winner(P->err64.as<double>(), P->sel.as<int>(), P->cand_rows.as<int64_t>(),
+                            (int64_t)nsel, P->win_err.as<double>(), P->win_row.as<int64_t>(),
+                            P->win_c.as<int>(), st)));
   double e;
   int64_t r;
-  CK(cudaMemcpyAsync(&e, P->win_err.p, sizeof e, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&r, P->win_row.p, sizeof r, cudaMemcpyDeviceToHost, st));
+  CK(d2h(&e, P->win_err.p, sizeof e, st));
+  CK(d2h(&r, P->win_row.p, sizeof r, st));
   CK(cudaStreamSynchronize(st));
   if (err_local) *err_local = e;
   if (row_local) *row_local = r;
@@ -729,14 +771,15 @@ extern "C" int dses_stage_rescore(dses_plan* P, double threshold, int code, doub
 
 extern "C" int dses_stage_row_info(dses_plan* P, int64_t row, int64_t* lin, int64_t* count,
                                    void* stream) {
+  TrafficScope ts_(P);
   if (!P) return fail(DSES_E_INVALID, "null plan");
   const int64_t rr = row - P->cur_r_begin;
   if (rr < 0 || rr >= P->cur_r_count) return fail(DSES_E_INVALID, "row %lld not in this plan's slice", (long long)row);
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
   int l, c;
-  CK(cudaMemcpyAsync(&l, P->lins.as<int>() + rr, 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&c, P->counts.as<int>() + rr, 4, cudaMemcpyDeviceToHost, st));
+  CK(d2h(&l, P->lins.as<int>() + rr, 4, st));
+  CK(d2h(&c, P->counts.as<int>() + rr, 4, st));
   CK(cudaStreamSynchronize(st));
   if (lin) *lin = l;
   if (count) *count = c;
@@ -745,6 +788,7 @@ extern "C" int dses_stage_row_info(dses_plan* P, int64_t row, int64_t* lin, int6
 
 extern "C" int dses_pose_error(dses_plan* P, const dses_grid* g, int64_t row, int64_t lin, int code,
                                double param, double* err, void* stream) {
+  TrafficScope ts_(P);
   if (!P || !err || code < 0 || code > 4 || lin < 0) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -756,17 +800,18 @@ extern "C" int dses_pose_error(dses_plan* P, const dses_grid* g, int64_t row, in
   CK(P->vals.ensure(sizeof(double) * P->n));
   CK(P->err64.ensure(sizeof(double)));
   const int l32 = (int)lin;
-  CK(cudaMemcpyAsync(P->tmp_rows.p, &row, sizeof row, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(P->tmp_lins.p, &l32, sizeof l32, cudaMemcpyHostToDevice, st));
+  CK(h2d(P->tmp_rows.p, &row, sizeof row, st));
+  CK(h2d(P->tmp_lins.p, &l32, sizeof l32, st));
   ScoreParams s = score_params(P, rs, code, param);
-  CK(launch_exact(s, P->tmp_rows.as<int64_t>(), P->tmp_lins.as<int>(), nullptr, 1,
-                  P->vals.as<double>(), P->err64.as<double>(), st));
-  CK(cudaMemcpyAsync(err, P->err64.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(launched(launch_exact(s, P->tmp_rows.as<int64_t>(), P->tmp_lins.as<int>(), nullptr, 1,
+                           P->vals.as<double>(), P->err64.as<double>(), st), 2));
+  CK(d2h(err, P->err64.p, sizeof(double), st));
   CK(cudaStreamSynchronize(st));
   return DSES_OK;
 }
 
 extern "C" int dses_stage_stats(dses_plan* P, int64_t* pairs, int64_t* votes, int64_t* rechecks) {
+  TrafficScope ts_(P);
   if (!P) return fail(DSES_E_INVALID, "null plan");
   CK(cudaSetDevice(P->device));
   unsigned long long h[3];
@@ -781,6 +826,7 @@ extern "C" int dses_stage_stats(dses_plan* P, int64_t* pairs, int64_t* votes, in
 extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t r_count,
                            double q, int code, double param, int skip_refine, dses_result* out,
                            void* stream) {
+  TrafficScope ts_(P);
   if (!P || !g || !out) return fail(DSES_E_INVALID, "bad arguments");
   std::memset(out, 0, sizeof(*out));
   CK(cudaSetDevice(P->device));
@@ -829,9 +875,23 @@ extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, in
   out->best_error = skip_refine ? miss : best_err;
   out->best_inliers = P->n - (int64_t)std::llround(miss);
   float ms;
+  cudaEventElapsedTime(&ms, P->ev[5], P->ev[6]); out->ms_vote_kernel = ms;
   cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]); out->ms_vote = ms;
   cudaEventElapsedTime(&ms, P->ev[1], P->ev[2]); out->ms_select = ms;
   cudaEventElapsedTime(&ms, P->ev[2], P->ev[3]); out->ms_score = ms;
   cudaEventElapsedTime(&ms, P->ev[0], P->ev[4]); out->ms_total = ms;
+  out->launches = P->traffic.launches;
+  out->h2d_bytes = P->traffic.h2d;
+  out->d2h_bytes = P->traffic.d2h;
   return dses_stage_stats(P, &out->pairs_evaluated, &out->votes, &out->rechecks);
+}
+
+extern "C" int dses_plan_traffic(dses_plan* P, int64_t* h2d_bytes, int64_t* d2h_bytes,
+                                 int64_t* launches, int reset) {
+  if (!P) return fail(DSES_E_INVALID, "null plan");
+  if (h2d_bytes) *h2d_bytes = P->traffic.h2d;
+  if (d2h_bytes) *d2h_bytes = P->traffic.d2h;
+  if (launches) *launches = P->traffic.launches;
+  if (reset) P->traffic = Traffic{};
+  return DSES_OK;
 }

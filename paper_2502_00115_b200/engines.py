@@ -172,6 +172,7 @@ def dses(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationR
             "total": t_end - t0,
             "device_total": res["ms_total"] * ms,
             "stats": {k: res[k] for k in ("pairs_evaluated", "votes", "rechecks", "rescored",
-                                          "mstar")},
+                                          "mstar", "launches", "h2d_bytes", "d2h_bytes",
+                                          "ms_vote_kernel")},
         },
     )
