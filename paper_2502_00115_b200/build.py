@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     exe = nvcc()
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [exe, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+    cmd = [exe, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall,-Wextra,-Winfinite-recursion", "-shared",
            f'-DDSES_NVCC_VERSION="{nvcc_version(exe)}"', "-o", OUT + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:

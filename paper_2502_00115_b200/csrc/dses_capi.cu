@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -115,11 +116,11 @@ static thread_local Traffic* g_traffic = nullptr;
 
 static cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (g_traffic) g_traffic->h2d += (int64_t)bytes;
-  return h2d(dst, src, bytes, st);
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
 }
 static cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (g_traffic) g_traffic->d2h += (int64_t)bytes;
-  return d2h(dst, src, bytes, st);
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
 }
 static inline cudaError_t launched(cudaError_t e, int n = 1) {
   if (g_traffic) g_traffic->launches += n;
@@ -175,6 +176,12 @@ struct TrafficScope {
 
 namespace {
 
+// DSES_TRACE=1 prints the plan-construction steps to stderr (debug aid)
+void trace(const char* what) {
+  static const int on = [] { const char* e = getenv("DSES_TRACE"); return e && *e == '1'; }();
+  if (on) { fprintf(stderr, "[dses] %s\n", what); fflush(stderr); }
+}
+
 // round-half-away-from-zero integer of v (host side fixed-point conversion)
 inline int64_t rint64(double v) { return (int64_t)std::llrint(v); }
 
@@ -211,6 +218,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   const int64_t n = P->n, m = P->m;
   cudaStream_t st = 0;
   // ---- fixed-point scale
+  trace("fixed-point scale");
   double ymax = 0, xnorm = 0;
   for (int64_t j = 0; j < m; ++j)
     for (int k = 0; k < 3; ++k) ymax = std::max(ymax, std::fabs(y[3 * j + k]));
@@ -235,6 +243,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   P->bx = xnorm + tmax;
 
   // ---- spatial tiles
+  trace("spatial tiles");
   std::vector<int> px(n), py(m);
   std::iota(px.begin(), px.end(), 0);
   std::iota(py.begin(), py.end(), 0);
@@ -280,7 +289,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       }
       v[k] = (int)q;
     }
-    yq[j] = make_int4(v[0], v[1], v[2], 0);
+    yq[j] = make_int4(v[0], v[1], v[2], 0);  // .w = has-near flag, set below
   }
   std::vector<YTile> yt(ty.size());
   for (size_t t = 0; t < ty.size(); ++t) {
@@ -294,6 +303,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     }
   }
   // ---- dedup near lists (tile order): j' < j with |y_j - y_j'|_inf < bin (1 + 1e-6)
+  trace("dedup near lists");
   const double thr = P->bin * (1.0 + 1e-6);
   std::vector<int> o0(m);
   std::iota(o0.begin(), o0.end(), 0);
@@ -323,7 +333,9 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   }
   noff[m] = (int)nidx.size();
   P->near_pairs = npairs;
+  for (int64_t j = 0; j < m; ++j) yq[j].w = noff[j + 1] > noff[j] ? 1 : 0;
   // ---- scoring layout: x original order, y sorted by axis 0 (stable)
+  trace("scoring layout");
   std::vector<int> sy(m);
   std::iota(sy.begin(), sy.end(), 0);
   std::stable_sort(sy.begin(), sy.end(), [&](int a, int b) { return y[3 * a] < y[3 * b]; });
@@ -356,6 +368,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   CK(cudaStreamSynchronize(st));
 
   // ---- vote kernel parameters
+  trace("vote kernel parameters");
   VoteParams& v = P->vp;
   v.d0 = (int)P->dims[0]; v.d1 = (int)P->dims[1]; v.d2 = (int)P->dims[2];
   v.nbins = v.d0 * v.d1 * v.d2;
@@ -379,12 +392,14 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.hist_words = (int)((words + 3) / 4 * 4);
   v.n_pad = (int)((n + 3) / 4 * 4);
   // shared-memory placement
+  trace("shared-memory placement");
   const size_t fixed = vote_smem_bytes(v, false, false);
   const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)n * 16;
   const size_t lim = P->smem_optin;
   P->hsmem = v.count16 && fixed + hb <= lim;
   P->psmem = fixed + pb + (P->hsmem ? hb : 0) <= lim;
   if (!P->hsmem && !P->psmem && fixed + pb <= lim) P->psmem = true;
+  trace("occupancy");
   int per_sm = vote_max_ctas_per_sm(v, P->hsmem, P->psmem, P->vote_threads);
   if (per_sm < 1) {
     P->vote_threads = 512;
@@ -501,6 +516,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(DSES_E_NODEVICE, "no CUDA device");
   if (device < 0 || device >= ndev) return fail(DSES_E_INVALID, "bad device %d", device);
+  trace("set device");
   CK(cudaSetDevice(device));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));

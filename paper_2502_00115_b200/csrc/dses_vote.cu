@@ -59,6 +59,45 @@ __device__ __forceinline__ bool pair_bin(const VoteParams& p, const double* R, c
   return exact_bin(p, p0, p1, p2, p.ys + 3 * j, lin);
 }
 
+constexpr int kQueue = 64;      // per-warp candidate queue entries
+constexpr int kUnitCap = 4096;  // (reference tile, source tile) work units per round
+
+// Bin, dedup and vote the first n (<= 32) queued candidate pairs, one per
+// lane.  Entry: Q = (u0, u1, u2, i), QJ = j | has_near << 31.
+template <bool PSMEM>
+__device__ __forceinline__ void drain_queue(const VoteParams& p, const double* R, const int4* P,
+                                            const int4* Q, const int* QJ, int n, int lane,
+                                            unsigned* hist, unsigned& votes, unsigned& rechecks) {
+  if (lane >= n) return;
+  const int4 e = Q[lane];
+  const int jt = QJ[lane];
+  const int i = e.w, j = jt & 0x7fffffff;
+  int lin;
+  bool in;
+  const int s = fast_bin(p, e.x, e.y, e.z, &lin);
+  if (s == 2) {
+    ++rechecks;
+    const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
+    in = exact_bin(p, rot_row(R, 0, x0, x1, x2), rot_row(R, 1, x0, x1, x2),
+                   rot_row(R, 2, x0, x1, x2), p.ys + 3 * j, &lin);
+  } else {
+    in = (s == 1);
+  }
+  if (!in) return;
+  if (jt < 0) {  // j has reference neighbours closer than one bin: per-source dedup
+    const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
+    const int e1 = p.near_off[j + 1];
+    for (int k = p.near_off[j]; k < e1; ++k) {
+      const int jj = p.near_idx[k];
+      int lin2;
+      if (pair_bin(p, R, Pi, i, p.yq[jj], jj, &lin2, rechecks) && lin2 == lin) return;
+    }
+  }
+  ++votes;
+  if (p.count16) atomicAdd(&hist[lin >> 1], (lin & 1) ? 0x10000u : 1u);
+  else atomicAdd(&hist[lin], 1u);
+}
+
 template <bool HSMEM, bool PSMEM>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -76,7 +115,16 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   off += (size_t)p.nxt * 32;
   double* R = reinterpret_cast<double*>(smem + off);
   off += 16 * 8;
-  int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch
+  int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + 2 counters
+  off += 4 * 32 * 4;
+  int* units = reinterpret_cast<int*>(smem + off);  // [kUnitCap] overlapping tile pairs
+  off += (size_t)kUnitCap * 4;
+  int4* Q = reinterpret_cast<int4*>(smem + off) + warp * kQueue;
+  off += (size_t)(kVoteThreads / 32) * kQueue * 16;
+  int* QJ = reinterpret_cast<int*>(smem + off) + warp * kQueue;
+  int* s_nunits = red + 96;
+  int* s_next = red + 97;
+  const unsigned lanemask_lt = (1u << lane) - 1u;
 
   uint4* hist4 = reinterpret_cast<uint4*>(hist);
   const int nw4 = p.hist_words >> 2;
@@ -87,6 +135,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   unsigned long long st_pairs = 0;
   unsigned st_votes = 0, st_rechecks = 0;
   const bool exact_mode = (p.F == 0);
+  const int npairs = p.nyt * p.nxt;
 
   for (int64_t rr = blockIdx.x; rr < p.r_count; rr += gridDim.x) {
     const int64_t r = p.r_begin + rr;
@@ -96,13 +145,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     // rotated source points in fixed point (fp64 in the reference's op order)
     for (int i = tid; i < p.n; i += nthreads) {
       const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
-      int4 q;
-      if (exact_mode) q = make_int4(0, 0, 0, 0);
-      else {
+      int4 q = make_int4(0, 0, 0, 0);
+      if (!exact_mode) {
         q.x = __double2int_rn(dmul(rot_row(R, 0, x0, x1, x2), p.inv_s));
         q.y = __double2int_rn(dmul(rot_row(R, 1, x0, x1, x2), p.inv_s));
         q.z = __double2int_rn(dmul(rot_row(R, 2, x0, x1, x2), p.inv_s));
-        q.w = 0;
       }
       if (PSMEM) P[i] = q; else __stcg(&P[i], q);
     }
@@ -117,64 +164,99 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         const int c0 = __double2int_rn(rot_row(R, 0, xt.c[0], xt.c[1], xt.c[2]) * p.inv_s);
         const int c1 = __double2int_rn(rot_row(R, 1, xt.c[0], xt.c[1], xt.c[2]) * p.inv_s);
         const int c2 = __double2int_rn(rot_row(R, 2, xt.c[0], xt.c[1], xt.c[2]) * p.inv_s);
-        lo = make_int4(c0 - xt.rad, c1 - xt.rad, c2 - xt.rad, 0);
-        hi = make_int4(c0 + xt.rad, c1 + xt.rad, c2 + xt.rad, 0);
+        lo = make_int4(c0 - xt.rad, c1 - xt.rad, c2 - xt.rad, xt.start);
+        hi = make_int4(c0 + xt.rad, c1 + xt.rad, c2 + xt.rad, xt.start + xt.count);
       }
+      if (exact_mode) { lo.w = xt.start; hi.w = xt.start + xt.count; }
       XB[2 * t] = lo;
       XB[2 * t + 1] = hi;
     }
     __syncthreads();
 
-    // ---- votes: warp w sweeps reference tiles w, w+nwarps, ...
-    for (int b = warp; b < p.nyt; b += nwarps) {
-      const YTile yt = p.yt[b];
-      const bool valid = lane < yt.count;
-      const int j = yt.start + (valid ? lane : 0);
-      const int4 Y = p.yq[j];
-      const int nlo = valid ? p.near_off[j] : 0;
-      const int nhi = valid ? p.near_off[j + 1] : 0;
-      for (int xc = 0; xc < p.nxt; xc += 32) {
-        const int a = xc + lane;
+    // ---- votes, in rounds of at most kUnitCap (reference tile, source tile) pairs:
+    //  B1  every thread tests tile pairs; the overlapping ones are compacted
+    //      into `units` (u = Yq - Pq over the two boxes can meet [0, W));
+    //  B2  warps take units dynamically; lane = reference point j (registers),
+    //      loop over the source tile's points i (broadcast from shared memory).
+    //      Candidates passing the per-pair window prefilter are compacted into
+    //      the warp's queue and binned/voted 32 at a time.
+    int qn = 0;  // warp-uniform queue fill (persists across units and rounds)
+    for (int base = 0; base < npairs; base += kUnitCap) {
+      if (tid == 0) { *s_nunits = 0; *s_next = 0; }
+      __syncthreads();
+      const int lim = min(kUnitCap, npairs - base);
+      for (int k0 = 0; k0 < lim; k0 += nthreads) {
+        const int k = k0 + tid;
         bool ov = false;
-        if (a < p.nxt) {
+        int unit = 0;
+        if (k < lim) {
+          unit = base + k;
+          const int b = unit / p.nxt, a = unit - b * p.nxt;
+          const YTile& yt = p.yt[b];
           const int4 lo = XB[2 * a], hi = XB[2 * a + 1];
-          // u = Yq - Pq ranges over [ylo - phi, yhi - plo]; need overlap with [0, W)
-          ov = (yt.hi[0] - lo.x >= 0) & (yt.lo[0] - hi.x < (int)p.W0) &
-               (yt.hi[1] - lo.y >= 0) & (yt.lo[1] - hi.y < (int)p.W1) &
-               (yt.hi[2] - lo.z >= 0) & (yt.lo[2] - hi.z < (int)p.W2);
-          if (exact_mode) ov = true;
+          ov = exact_mode ||
+               ((yt.hi[0] - lo.x >= 0) & (yt.lo[0] - hi.x < (int)p.W0) &
+                (yt.hi[1] - lo.y >= 0) & (yt.lo[1] - hi.y < (int)p.W1) &
+                (yt.hi[2] - lo.z >= 0) & (yt.lo[2] - hi.z < (int)p.W2));
         }
-        unsigned mask = __ballot_sync(0xffffffffu, ov);
-        while (mask) {
-          const int t = xc + __ffs(mask) - 1;
-          mask &= mask - 1;
-          const int i0 = p.xt[t].start, i1 = i0 + p.xt[t].count;
-          if (lane == 0) st_pairs += (unsigned long long)(i1 - i0) * yt.count;
-          for (int i = i0; i < i1; ++i) {
-            const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
-            const int u0 = Y.x - Pi.x, u1 = Y.y - Pi.y, u2 = Y.z - Pi.z;
-            const bool cand = valid & ((unsigned)u0 < p.W0) & ((unsigned)u1 < p.W1) &
-                              ((unsigned)u2 < p.W2);
+        const unsigned m = __ballot_sync(0xffffffffu, ov);
+        if (m) {
+          int slot = 0;
+          if (lane == 0) slot = atomicAdd(s_nunits, __popc(m));
+          slot = __shfl_sync(0xffffffffu, slot, 0);
+          if (ov) units[slot + __popc(m & lanemask_lt)] = unit;
+        }
+      }
+      __syncthreads();
+      const int nunits = *s_nunits;
+      for (;;) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(s_next, 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= nunits) break;
+        const int unit = units[u];
+        const int b = unit / p.nxt, a = unit - b * p.nxt;
+        const int ystart = p.yt[b].start, ycount = p.yt[b].count;
+        const bool valid = lane < ycount;
+        const int j = ystart + (valid ? lane : 0);
+        const int4 Y = p.yq[j];
+        const int jtag = j | (Y.w ? (int)0x80000000u : 0);
+        const int i0 = XB[2 * a].w, i1 = XB[2 * a + 1].w;
+        if (lane == 0) st_pairs += (unsigned long long)(i1 - i0) * ycount;
+        for (int i = i0; i < i1; ++i) {
+          const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
+          const int u0 = Y.x - Pi.x, u1 = Y.y - Pi.y, u2 = Y.z - Pi.z;
+          const bool cand = valid & ((unsigned)u0 < p.W0) & ((unsigned)u1 < p.W1) &
+                            ((unsigned)u2 < p.W2);
+          const unsigned cm = __ballot_sync(0xffffffffu, cand);
+          if (cm) {
             if (cand) {
-              int lin;
-              if (pair_bin(p, R, Pi, i, Y, j, &lin, st_rechecks)) {
-                bool dup = false;
-                for (int e = nlo; e < nhi && !dup; ++e) {
-                  const int jj = p.near_idx[e];
-                  int lin2;
-                  if (pair_bin(p, R, Pi, i, p.yq[jj], jj, &lin2, st_rechecks) && lin2 == lin)
-                    dup = true;
-                }
-                if (!dup) {
-                  ++st_votes;
-                  if (p.count16) atomicAdd(&hist[lin >> 1], (lin & 1) ? 0x10000u : 1u);
-                  else atomicAdd(&hist[lin], 1u);
-                }
-              }
+              const int pos = qn + __popc(cm & lanemask_lt);
+              Q[pos] = make_int4(u0, u1, u2, i);
+              QJ[pos] = jtag;
+            }
+            qn += __popc(cm);
+            if (qn >= 32) {
+              __syncwarp();
+              drain_queue<PSMEM>(p, R, P, Q, QJ, 32, lane, hist, st_votes, st_rechecks);
+              const int rem = qn - 32;
+              int4 t4 = make_int4(0, 0, 0, 0);
+              int tj = 0;
+              if (lane < rem) { t4 = Q[32 + lane]; tj = QJ[32 + lane]; }
+              __syncwarp();
+              if (lane < rem) { Q[lane] = t4; QJ[lane] = tj; }
+              __syncwarp();
+              qn = rem;
             }
           }
         }
       }
+      __syncthreads();  // units[] is rebuilt by the next round
+    }
+    if (qn > 0) {
+      __syncwarp();
+      drain_queue<PSMEM>(p, R, P, Q, QJ, qn, lane, hist, st_votes, st_rechecks);
+      __syncwarp();
     }
     __syncthreads();
 
@@ -249,7 +331,8 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem) {
   size_t b = 0;
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n * 16;
-  b += (size_t)p.nxt * 32 + 16 * 8 + 3 * 32 * 4;
+  b += (size_t)p.nxt * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)kUnitCap * 4;
+  b += (size_t)(kVoteThreads / 32) * kQueue * (16 + 4);
   return b;
 }
 
