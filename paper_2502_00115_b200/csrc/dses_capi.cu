@@ -6,6 +6,7 @@
 // the small host<->device scalar traffic between stages.  The Python layer
 // (paper_2502_00115_b200/engines.py) mirrors gridreg's API and exceptions on top.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -91,21 +92,36 @@ extern "C" int dses_device_count(int* out) {
 // ---------------------------------------------------------------------------
 // device buffers
 // ---------------------------------------------------------------------------
+// Device buffers come from the device's stream-ordered memory pool
+// (cudaMallocAsync on the legacy stream, release threshold = unlimited), so
+// a registration that creates a fresh plan reuses cached memory instead of
+// paying cudaMalloc/cudaFree device synchronisations.
+static void keep_pool(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap && p) return cudaSuccess;
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
     p = nullptr;
     cap = 0;
-    size_t want = std::max<size_t>(bytes, 256);
-    cudaError_t e = cudaMalloc(&p, want);
+    size_t want = std::max<size_t>(bytes + bytes / 2, 256);
+    cudaError_t e = cudaMallocAsync(&p, want, 0);
     if (e == cudaSuccess) cap = want;
     return e;
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
-  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+  void release() { if (p) cudaFreeAsync(p, 0); p = nullptr; cap = 0; }
 };
 
 // host<->device traffic is counted per plan (bench.py reports it as e2e bytes)
@@ -179,7 +195,12 @@ namespace {
 // DSES_TRACE=1 prints the plan-construction steps to stderr (debug aid)
 void trace(const char* what) {
   static const int on = [] { const char* e = getenv("DSES_TRACE"); return e && *e == '1'; }();
-  if (on) { fprintf(stderr, "[dses] %s\n", what); fflush(stderr); }
+  if (on) {
+    static auto t0 = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[dses %10.3f ms] %s\n", ms, what);
+    fflush(stderr);
+  }
 }
 
 // round-half-away-from-zero integer of v (host side fixed-point conversion)
@@ -408,6 +429,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   if (per_sm < 1) return fail(DSES_E_CUDA, "vote kernel cannot be resident (smem %zu)",
                               vote_smem_bytes(v, P->hsmem, P->psmem));
   P->vote_grid = per_sm * P->sms;
+  trace("plan ready");
   return DSES_OK;
 }
 
@@ -518,13 +540,18 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
   if (device < 0 || device >= ndev) return fail(DSES_E_INVALID, "bad device %d", device);
   trace("set device");
   CK(cudaSetDevice(device));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, device));
-  if (prop.major != 10) return fail(DSES_E_NODEVICE, "sm_100a build cannot run on sm_%d%d", prop.major, prop.minor);
+  keep_pool(device);
+  // individual attributes: cudaGetDeviceProperties costs up to tens of ms per call
+  int major = 0, minor = 0, sms = 0, optin = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  if (major != 10) return fail(DSES_E_NODEVICE, "sm_100a build cannot run on sm_%d%d", major, minor);
   dses_plan* P = new dses_plan();
   P->device = device;
-  P->sms = prop.multiProcessorCount;
-  P->smem_optin = prop.sharedMemPerBlockOptin;
+  P->sms = sms;
+  P->smem_optin = (size_t)optin;
   P->n = n;
   P->m = m;
   P->bin = bin_size;
