@@ -166,7 +166,7 @@ struct dses_plan {
   bool hsmem = true, psmem = true;
   int vote_grid = 0, vote_threads = kVoteThreads;
   // device data
-  DevBuf xs, ys, yq, near_off, near_idx, xt, yt;       // vote (tile order)
+  DevBuf xs, ys, yq, near_off, near_idx, xt, xsub, yt; // vote (tile order)
   DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
   DevBuf cth, sth, rots;                               // rotation sources
   DevBuf counts, lins, ties;                           // per-rotation outputs
@@ -209,9 +209,9 @@ inline int64_t rint64(double v) { return (int64_t)std::llrint(v); }
 // recursive median split until tiles hold <= kTile points; splits at a
 // multiple of kTile so that all but the last tile of each branch are full.
 void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
-              std::vector<std::pair<int, int>>& tiles) {
+              std::vector<std::pair<int, int>>& tiles, int tile) {
   const int64_t cnt = hi - lo;
-  if (cnt <= kTile) {
+  if (cnt <= tile) {
     if (cnt > 0) tiles.emplace_back((int)lo, (int)cnt);
     return;
   }
@@ -224,15 +224,15 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
   int axis = 0;
   for (int k = 1; k < 3; ++k)
     if (mx[k] - mn[k] > mx[axis] - mn[axis]) axis = k;
-  const int64_t ntile = (cnt + kTile - 1) / kTile;
-  const int64_t left = (ntile / 2) * kTile;
+  const int64_t ntile = (cnt + tile - 1) / tile;
+  const int64_t left = (ntile / 2) * tile;
   std::nth_element(perm.begin() + lo, perm.begin() + lo + left, perm.begin() + hi,
                    [&](int a, int b) {
                      const double va = pts[3 * a + axis], vb = pts[3 * b + axis];
                      return va < vb || (va == vb && a < b);
                    });
-  kd_tiles(pts, lo, lo + left, perm, tiles);
-  kd_tiles(pts, lo + left, hi, perm, tiles);
+  kd_tiles(pts, lo, lo + left, perm, tiles, tile);
+  kd_tiles(pts, lo + left, hi, perm, tiles, tile);
 }
 
 int build_plan(dses_plan* P, const double* x, const double* y) {
@@ -269,20 +269,16 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   std::iota(px.begin(), px.end(), 0);
   std::iota(py.begin(), py.end(), 0);
   std::vector<std::pair<int, int>> tx, ty;
-  kd_tiles(x, 0, n, px, tx);
-  kd_tiles(y, 0, m, py, ty);
+  kd_tiles(x, 0, n, px, tx, kSub);   // source sub-tiles; units = kSubPerUnit consecutive ones
+  kd_tiles(y, 0, m, py, ty, kTile);
   std::vector<double> xs(3 * n), ys(3 * m);
   for (int64_t i = 0; i < n; ++i)
     for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
   for (int64_t j = 0; j < m; ++j)
     for (int k = 0; k < 3; ++k) ys[3 * j + k] = y[3 * py[j] + k];
   const double inv_s = P->inv_bin * S;
-  std::vector<XTile> xt(tx.size());
-  for (size_t t = 0; t < tx.size(); ++t) {
-    XTile& T = xt[t];
-    T.start = tx[t].first;
-    T.count = tx[t].second;
-    T.pad = 0;
+  // sphere (bbox centre, max distance) of source points [start, start+count)
+  auto sphere = [&](XTile& T) {
     double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int q = T.start; q < T.start + T.count; ++q)
       for (int k = 0; k < 3; ++k) {
@@ -297,6 +293,23 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       rad = std::max(rad, std::sqrt(d2));
     }
     T.rad = F ? (int)std::ceil(rad * inv_s * (1.0 + 1e-9)) + 3 : 0;
+  };
+  std::vector<XTile> xsub(tx.size()), xt;
+  for (size_t t = 0; t < tx.size(); ++t) {
+    XTile& T = xsub[t];
+    T = XTile{};
+    T.start = tx[t].first;
+    T.count = tx[t].second;
+    sphere(T);
+  }
+  for (size_t t0 = 0; t0 < xsub.size(); t0 += kSubPerUnit) {
+    XTile U{};
+    U.sub = (int)t0;
+    U.nsub = (int)std::min<size_t>(kSubPerUnit, xsub.size() - t0);
+    U.start = xsub[t0].start;
+    U.count = xsub[t0 + U.nsub - 1].start + xsub[t0 + U.nsub - 1].count - U.start;
+    sphere(U);
+    xt.push_back(U);
   }
   // fixed-point reference: Yq = rint(fl(y*inv)*S) - lo*S + S/2 + G
   std::vector<int4> yq(m);
@@ -354,7 +367,25 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   }
   noff[m] = (int)nidx.size();
   P->near_pairs = npairs;
-  for (int64_t j = 0; j < m; ++j) yq[j].w = noff[j + 1] > noff[j] ? 1 : 0;
+  // dedup partners resolved inside the warp: up to two near neighbours j' < j
+  // in the same reference tile (their lanes); anything else sets the "far" bit
+  std::vector<int> tile_of(m);
+  for (size_t t = 0; t < yt.size(); ++t)
+    for (int q = yt[t].start; q < yt[t].start + yt[t].count; ++q) tile_of[q] = (int)t;
+  for (int64_t j = 0; j < m; ++j) {
+    int w = 0, nin = 0;
+    bool far = false;
+    for (int k = noff[j]; k < noff[j + 1]; ++k) {
+      const int jj = nidx[k];
+      if (tile_of[jj] == tile_of[j] && nin < 2) {
+        w |= (jj - yt[tile_of[j]].start + 1) << (6 * nin);
+        ++nin;
+      } else {
+        far = true;
+      }
+    }
+    yq[j].w = w | (far ? (1 << 12) : 0);
+  }
   // ---- scoring layout: x original order, y sorted by axis 0 (stable)
   trace("scoring layout");
   std::vector<int> sy(m);
@@ -377,6 +408,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   if (nidx.empty()) nidx.push_back(0);
   CK(upload(P->near_idx, nidx, st));
   CK(upload(P->xt, xt, st));
+  CK(upload(P->xsub, xsub, st));
   CK(upload(P->yt, yt, st));
   CK(upload(P->x0, xv, st));
   CK(upload(P->ys0, c0, st));
@@ -407,6 +439,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.xs = P->xs.as<double>(); v.ys = P->ys.as<double>(); v.yq = P->yq.as<int4>();
   v.near_off = P->near_off.as<int>(); v.near_idx = P->near_idx.as<int>();
   v.xt = P->xt.as<XTile>(); v.yt = P->yt.as<YTile>();
+  v.xsub = P->xsub.as<XTile>(); v.nxs = (int)xsub.size();
   v.stats = P->stats.as<unsigned long long>();
   v.count16 = n < 65536 ? 1 : 0;
   const int64_t words = v.count16 ? (v.nbins + 1) / 2 : v.nbins;
@@ -568,7 +601,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
 extern "C" int dses_plan_destroy(dses_plan* P) {
   if (!P) return DSES_OK;
   cudaSetDevice(P->device);
-  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->yt,
+  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->xsub, &P->yt,
                     &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->cth, &P->sth, &P->rots,
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,

@@ -20,7 +20,9 @@
 
 namespace dses {
 
-constexpr int kTile = 32;        // points per spatial tile (one per lane)
+constexpr int kTile = 32;        // reference points per tile (one per lane)
+constexpr int kSub = 4;          // source points per sub-tile
+constexpr int kSubPerUnit = 8;   // sub-tiles per source unit (<= 32 points)
 constexpr int kGuard = 2;        // guard band in fixed-point units
 constexpr int kVoteThreads = 1024;
 
@@ -29,6 +31,7 @@ enum Metric { kL2 = 0, kL1 = 1, kTruncL1 = 2, kSatL0 = 3, kTruncL2 = 4 };
 struct XTile {          // spatial tile of the (sorted) source cloud
   int start, count;
   int rad;              // bounding-sphere radius in fixed-point units (+ rounding margin)
+  int sub, nsub;        // units: first sub-tile and sub-tile count (sub-tiles: unused)
   int pad;
   double c[3];          // sphere centre (metres)
 };
@@ -60,10 +63,14 @@ struct VoteParams {
   int n, m, nxt, nyt;
   const double* xs;      // (n,3) f64, X tile order
   const double* ys;      // (m,3) f64, Y tile order
-  const int4* yq;        // (m) fixed-point Yq (w unused)
+  const int4* yq;        // (m) fixed-point Yq; w = dedup partners: bits 0-5 / 6-11 = lane+1
+                         // of up to two near neighbours j' < j in the same tile, bit 12 =
+                         // "has near neighbours outside the tile / more than two"
   const int* near_off;   // (m+1) CSR offsets of the dedup near lists (Y tile order)
   const int* near_idx;   // near neighbours j' < j with |y_j - y_j'|_inf < bin (1+1e-6)
-  const XTile* xt;
+  const XTile* xt;        // units: groups of <= kSubPerUnit consecutive sub-tiles
+  const XTile* xsub;      // sub-tiles of <= kSub source points
+  int nxs;
   const YTile* yt;
   RotSource rot;
   int64_t r_begin, r_count;

@@ -59,50 +59,86 @@ __device__ __forceinline__ bool pair_bin(const VoteParams& p, const double* R, c
   return exact_bin(p, p0, p1, p2, p.ys + 3 * j, lin);
 }
 
-constexpr int kQueue = 64;      // per-warp candidate queue entries
-constexpr int kUnitCap = 4096;  // (reference tile, source tile) work units per round
+constexpr int kUnitCap = 4096;  // (reference tile, source unit) work units per round
 
-// Bin, dedup and vote the first n (<= 32) queued candidate pairs, one per
-// lane.  Entry: Q = (u0, u1, u2, i), QJ = j | has_near << 31.
-template <bool PSMEM>
-__device__ __forceinline__ void drain_queue(const VoteParams& p, const double* R, const int4* P,
-                                            const int4* Q, const int* QJ, int n, int lane,
-                                            unsigned* hist, unsigned& votes, unsigned& rechecks) {
-  if (lane >= n) return;
-  const int4 e = Q[lane];
-  const int jt = QJ[lane];
-  const int i = e.w, j = jt & 0x7fffffff;
-  int lin;
-  bool in;
-  const int s = fast_bin(p, e.x, e.y, e.z, &lin);
-  if (s == 2) {
-    ++rechecks;
-    const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
-    in = exact_bin(p, rot_row(R, 0, x0, x1, x2), rot_row(R, 1, x0, x1, x2),
-                   rot_row(R, 2, x0, x1, x2), p.ys + 3 * j, &lin);
-  } else {
-    in = (s == 1);
+// Rotated sphere (centre +- radius, a rotation preserves |x - c|) of a source
+// tile as a fixed-point box; .w carries the tile's point range.
+__device__ __forceinline__ void tile_box(const VoteParams& p, const double* R, const XTile& t,
+                                         bool exact_mode, int4& lo, int4& hi) {
+  if (exact_mode) {
+    lo = make_int4(INT_MIN / 4, INT_MIN / 4, INT_MIN / 4, t.start);
+    hi = make_int4(INT_MAX / 4, INT_MAX / 4, INT_MAX / 4, t.start + t.count);
+    return;
   }
-  if (!in) return;
-  if (jt < 0) {  // j has reference neighbours closer than one bin: per-source dedup
-    const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
-    const int e1 = p.near_off[j + 1];
-    for (int k = p.near_off[j]; k < e1; ++k) {
-      const int jj = p.near_idx[k];
-      int lin2;
-      if (pair_bin(p, R, Pi, i, p.yq[jj], jj, &lin2, rechecks) && lin2 == lin) return;
+  const int c0 = __double2int_rn(rot_row(R, 0, t.c[0], t.c[1], t.c[2]) * p.inv_s);
+  const int c1 = __double2int_rn(rot_row(R, 1, t.c[0], t.c[1], t.c[2]) * p.inv_s);
+  const int c2 = __double2int_rn(rot_row(R, 2, t.c[0], t.c[1], t.c[2]) * p.inv_s);
+  lo = make_int4(c0 - t.rad, c1 - t.rad, c2 - t.rad, t.start);
+  hi = make_int4(c0 + t.rad, c1 + t.rad, c2 + t.rad, t.start + t.count);
+}
+
+// Can a source box [lo, hi] and the reference tile bbox produce u = Yq - Pq in [0, W)?
+__device__ __forceinline__ bool boxes_meet(const VoteParams& p, const YTile& yt, const int4& lo,
+                                           const int4& hi) {
+  return (yt.hi[0] - lo.x >= 0) & (yt.lo[0] - hi.x < (int)p.W0) & (yt.hi[1] - lo.y >= 0) &
+         (yt.lo[1] - hi.y < (int)p.W1) & (yt.hi[2] - lo.z >= 0) & (yt.lo[2] - hi.z < (int)p.W2);
+}
+
+// One source point i against the warp's 32 reference points (one per lane).
+// Branch-free fast path; the rare guard-band re-bin and the rare
+// out-of-tile dedup are divergent branches entered only when some lane needs
+// them.  Dedup (_kernels.py:153-158): the vote (i, j) is dropped when a near
+// neighbour j' < j lands in the same bin for the same i; in-tile neighbours
+// are other lanes of this warp, so their bins arrive by shuffle.
+template <bool PSMEM>
+__device__ __forceinline__ void vote_slot(const VoteParams& p, const double* R, const int4* P,
+                                          unsigned* hist, const int4& Y, int j, int lane, int i,
+                                          unsigned& votes, unsigned& rechecks) {
+  const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
+  const int u0 = Y.x - Pi.x, u1 = Y.y - Pi.y, u2 = Y.z - Pi.z;
+  const bool cand = ((unsigned)u0 < p.W0) & ((unsigned)u1 < p.W1) & ((unsigned)u2 < p.W2);
+  if (!__any_sync(0xffffffffu, cand)) return;
+  const unsigned g2 = 2u * kGuard;
+  const bool near = cand & ((((unsigned)u0 & p.fmask) < g2) | (((unsigned)u1 & p.fmask) < g2) |
+                            (((unsigned)u2 & p.fmask) < g2));
+  bool in = cand & !near & ((unsigned)u0 < p.D0) & ((unsigned)u1 < p.D1) & ((unsigned)u2 < p.D2);
+  int lin = ((u0 >> p.F) * p.d1 + (u1 >> p.F)) * p.d2 + (u2 >> p.F);
+  if (__any_sync(0xffffffffu, near)) {
+    if (near) {
+      ++rechecks;
+      const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
+      in = exact_bin(p, rot_row(R, 0, x0, x1, x2), rot_row(R, 1, x0, x1, x2),
+                     rot_row(R, 2, x0, x1, x2), p.ys + 3 * j, &lin);
     }
   }
-  ++votes;
-  if (p.count16) atomicAdd(&hist[lin >> 1], (lin & 1) ? 0x10000u : 1u);
-  else atomicAdd(&hist[lin], 1u);
+  const int key = in ? lin : -1;
+  const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
+  const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
+  const int k1 = __shfl_sync(0xffffffffu, key, l1 & 31);
+  bool dup = in & (((l0 >= 0) & (k0 == key)) | ((l1 >= 0) & (k1 == key)));
+  const bool far = in & !dup & ((Y.w >> 12) & 1);
+  if (__any_sync(0xffffffffu, far)) {
+    if (far) {
+      const int e1 = p.near_off[j + 1];
+      for (int k = p.near_off[j]; k < e1 && !dup; ++k) {
+        const int jj = p.near_idx[k];
+        int lin2;
+        dup = pair_bin(p, R, Pi, i, p.yq[jj], jj, &lin2, rechecks) && lin2 == lin;
+      }
+    }
+  }
+  if (in & !dup) {
+    ++votes;
+    if (p.count16) atomicAdd(&hist[lin >> 1], (lin & 1) ? 0x10000u : 1u);
+    else atomicAdd(&hist[lin], 1u);
+  }
 }
 
 template <bool HSMEM, bool PSMEM>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nthreads = blockDim.x, nwarps = nthreads >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nthreads = blockDim.x, nwarps = nthreads >> 5, warp = tid >> 5;
 
   size_t off = 0;
   unsigned* hist;
@@ -111,17 +147,15 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   int4* P;
   if (PSMEM) { P = reinterpret_cast<int4*>(smem + off); off += (size_t)p.n * 16; }
   else P = p.p_global + (size_t)blockIdx.x * p.n_pad;
-  int4* XB = reinterpret_cast<int4*>(smem + off);  // [2*nxt]: lo, hi of each rotated tile box
+  int4* XB = reinterpret_cast<int4*>(smem + off);  // [2*nxt] rotated unit boxes (lo, hi)
   off += (size_t)p.nxt * 32;
+  int4* XS = reinterpret_cast<int4*>(smem + off);  // [2*nxs] rotated sub-tile boxes
+  off += (size_t)p.nxs * 32;
   double* R = reinterpret_cast<double*>(smem + off);
   off += 16 * 8;
-  int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + 2 counters
+  int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + counters
   off += 4 * 32 * 4;
   int* units = reinterpret_cast<int*>(smem + off);  // [kUnitCap] overlapping tile pairs
-  off += (size_t)kUnitCap * 4;
-  int4* Q = reinterpret_cast<int4*>(smem + off) + warp * kQueue;
-  off += (size_t)(kVoteThreads / 32) * kQueue * 16;
-  int* QJ = reinterpret_cast<int*>(smem + off) + warp * kQueue;
   int* s_nunits = red + 96;
   int* s_next = red + 97;
   const unsigned lanemask_lt = (1u << lane) - 1u;
@@ -142,7 +176,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     if (tid < 9) R[tid] = rotation_entry(p.rot, r, tid);
     __syncthreads();
 
-    // rotated source points in fixed point (fp64 in the reference's op order)
+    // ---- A: rotated source points in fixed point (fp64, the reference's op
+    //      order) and rotated unit / sub-tile boxes
     for (int i = tid; i < p.n; i += nthreads) {
       const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
       int4 q = make_int4(0, 0, 0, 0);
@@ -153,34 +188,25 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       }
       if (PSMEM) P[i] = q; else __stcg(&P[i], q);
     }
-    // rotated source-tile boxes: centre +- radius (a rotation preserves |x - c|)
-    for (int t = tid; t < p.nxt; t += nthreads) {
-      const XTile xt = p.xt[t];
+    for (int t = tid; t < p.nxt + p.nxs; t += nthreads) {
       int4 lo, hi;
-      if (exact_mode) {
-        lo = make_int4(INT_MIN / 4, INT_MIN / 4, INT_MIN / 4, 0);
-        hi = make_int4(INT_MAX / 4, INT_MAX / 4, INT_MAX / 4, 0);
+      if (t < p.nxt) {
+        tile_box(p, R, p.xt[t], exact_mode, lo, hi);
+        XB[2 * t] = lo;
+        XB[2 * t + 1] = hi;
       } else {
-        const int c0 = __double2int_rn(rot_row(R, 0, xt.c[0], xt.c[1], xt.c[2]) * p.inv_s);
-        const int c1 = __double2int_rn(rot_row(R, 1, xt.c[0], xt.c[1], xt.c[2]) * p.inv_s);
-        const int c2 = __double2int_rn(rot_row(R, 2, xt.c[0], xt.c[1], xt.c[2]) * p.inv_s);
-        lo = make_int4(c0 - xt.rad, c1 - xt.rad, c2 - xt.rad, xt.start);
-        hi = make_int4(c0 + xt.rad, c1 + xt.rad, c2 + xt.rad, xt.start + xt.count);
+        tile_box(p, R, p.xsub[t - p.nxt], exact_mode, lo, hi);
+        XS[2 * (t - p.nxt)] = lo;
+        XS[2 * (t - p.nxt) + 1] = hi;
       }
-      if (exact_mode) { lo.w = xt.start; hi.w = xt.start + xt.count; }
-      XB[2 * t] = lo;
-      XB[2 * t + 1] = hi;
     }
     __syncthreads();
 
-    // ---- votes, in rounds of at most kUnitCap (reference tile, source tile) pairs:
-    //  B1  every thread tests tile pairs; the overlapping ones are compacted
-    //      into `units` (u = Yq - Pq over the two boxes can meet [0, W));
-    //  B2  warps take units dynamically; lane = reference point j (registers),
-    //      loop over the source tile's points i (broadcast from shared memory).
-    //      Candidates passing the per-pair window prefilter are compacted into
-    //      the warp's queue and binned/voted 32 at a time.
-    int qn = 0;  // warp-uniform queue fill (persists across units and rounds)
+    // ---- B: votes, in rounds of at most kUnitCap (reference tile, source unit) pairs.
+    //  B1  threads test tile pairs; overlapping ones are compacted into `units`;
+    //  B2  warps take units dynamically: lane = reference point j (registers);
+    //      lanes 0..7 test the unit's sub-tiles, then each surviving sub-tile's
+    //      points i are broadcast from shared memory, one vote_slot per i.
     for (int base = 0; base < npairs; base += kUnitCap) {
       if (tid == 0) { *s_nunits = 0; *s_next = 0; }
       __syncthreads();
@@ -192,12 +218,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         if (k < lim) {
           unit = base + k;
           const int b = unit / p.nxt, a = unit - b * p.nxt;
-          const YTile& yt = p.yt[b];
-          const int4 lo = XB[2 * a], hi = XB[2 * a + 1];
-          ov = exact_mode ||
-               ((yt.hi[0] - lo.x >= 0) & (yt.lo[0] - hi.x < (int)p.W0) &
-                (yt.hi[1] - lo.y >= 0) & (yt.lo[1] - hi.y < (int)p.W1) &
-                (yt.hi[2] - lo.z >= 0) & (yt.lo[2] - hi.z < (int)p.W2));
+          ov = exact_mode || boxes_meet(p, p.yt[b], XB[2 * a], XB[2 * a + 1]);
         }
         const unsigned m = __ballot_sync(0xffffffffu, ov);
         if (m) {
@@ -216,49 +237,27 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         if (u >= nunits) break;
         const int unit = units[u];
         const int b = unit / p.nxt, a = unit - b * p.nxt;
-        const int ystart = p.yt[b].start, ycount = p.yt[b].count;
-        const bool valid = lane < ycount;
-        const int j = ystart + (valid ? lane : 0);
-        const int4 Y = p.yq[j];
-        const int jtag = j | (Y.w ? (int)0x80000000u : 0);
-        const int i0 = XB[2 * a].w, i1 = XB[2 * a + 1].w;
-        if (lane == 0) st_pairs += (unsigned long long)(i1 - i0) * ycount;
-        for (int i = i0; i < i1; ++i) {
-          const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
-          const int u0 = Y.x - Pi.x, u1 = Y.y - Pi.y, u2 = Y.z - Pi.z;
-          const bool cand = valid & ((unsigned)u0 < p.W0) & ((unsigned)u1 < p.W1) &
-                            ((unsigned)u2 < p.W2);
-          const unsigned cm = __ballot_sync(0xffffffffu, cand);
-          if (cm) {
-            if (cand) {
-              const int pos = qn + __popc(cm & lanemask_lt);
-              Q[pos] = make_int4(u0, u1, u2, i);
-              QJ[pos] = jtag;
-            }
-            qn += __popc(cm);
-            if (qn >= 32) {
-              __syncwarp();
-              drain_queue<PSMEM>(p, R, P, Q, QJ, 32, lane, hist, st_votes, st_rechecks);
-              const int rem = qn - 32;
-              int4 t4 = make_int4(0, 0, 0, 0);
-              int tj = 0;
-              if (lane < rem) { t4 = Q[32 + lane]; tj = QJ[32 + lane]; }
-              __syncwarp();
-              if (lane < rem) { Q[lane] = t4; QJ[lane] = tj; }
-              __syncwarp();
-              qn = rem;
-            }
-          }
+        const YTile yt = p.yt[b];
+        const bool valid = lane < yt.count;
+        const int j = yt.start + (valid ? lane : 0);
+        int4 Y = p.yq[j];
+        if (!valid) { Y.x = INT_MIN / 2; Y.w = 0; }  // never a candidate
+        const XTile& U = p.xt[a];
+        const int nsub = U.nsub, sub0 = U.sub;
+        bool sok = false;
+        if (lane < nsub) sok = exact_mode || boxes_meet(p, yt, XS[2 * (sub0 + lane)], XS[2 * (sub0 + lane) + 1]);
+        unsigned sm = __ballot_sync(0xffffffffu, sok);
+        while (sm) {
+          const int s = sub0 + __ffs(sm) - 1;
+          sm &= sm - 1;
+          const int i0 = XS[2 * s].w, i1 = XS[2 * s + 1].w;
+          if (lane == 0) st_pairs += (unsigned long long)(i1 - i0) * yt.count;
+          for (int i = i0; i < i1; ++i)
+            vote_slot<PSMEM>(p, R, P, hist, Y, j, lane, i, st_votes, st_rechecks);
         }
       }
       __syncthreads();  // units[] is rebuilt by the next round
     }
-    if (qn > 0) {
-      __syncwarp();
-      drain_queue<PSMEM>(p, R, P, Q, QJ, qn, lane, hist, st_votes, st_rechecks);
-      __syncwarp();
-    }
-    __syncthreads();
 
     // ---- mode: scan (and re-zero) the histogram
     int best = 0, blin = INT_MAX, bties = 0;
@@ -331,8 +330,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem) {
   size_t b = 0;
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n * 16;
-  b += (size_t)p.nxt * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)kUnitCap * 4;
-  b += (size_t)(kVoteThreads / 32) * kQueue * (16 + 4);
+  b += (size_t)(p.nxt + p.nxs) * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)kUnitCap * 4;
   return b;
 }
 
