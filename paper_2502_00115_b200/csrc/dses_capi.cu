@@ -166,7 +166,7 @@ struct dses_plan {
   bool hsmem = true, psmem = true;
   int vote_grid = 0, vote_threads = kVoteThreads;
   // device data
-  DevBuf xs, ys, yq, near_off, near_idx, xt, xsub, yt; // vote (tile order)
+  DevBuf xs, ys, yq, near_off, near_idx, xt, xsub, yt, yleaf;  // vote (tile order)
   DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
   DevBuf cth, sth, rots;                               // rotation sources
   DevBuf counts, lins, ties;                           // per-rotation outputs
@@ -270,7 +270,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   std::iota(py.begin(), py.end(), 0);
   std::vector<std::pair<int, int>> tx, ty;
   kd_tiles(x, 0, n, px, tx, kSub);   // source sub-tiles; units = kSubPerUnit consecutive ones
-  kd_tiles(y, 0, m, py, ty, kTile);
+  kd_tiles(y, 0, m, py, ty, kLeaf);  // reference leaves; groups = kLeafPerGroup consecutive ones
   std::vector<double> xs(3 * n), ys(3 * m);
   for (int64_t i = 0; i < n; ++i)
     for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
@@ -325,17 +325,32 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     }
     yq[j] = make_int4(v[0], v[1], v[2], 0);  // .w = has-near flag, set below
   }
-  std::vector<YTile> yt(ty.size());
-  for (size_t t = 0; t < ty.size(); ++t) {
-    YTile& T = yt[t];
-    T.start = ty[t].first;
-    T.count = ty[t].second;
+  auto ybox = [&](YTile& T) {
     for (int k = 0; k < 3; ++k) { T.lo[k] = INT32_MAX; T.hi[k] = INT32_MIN; }
     for (int q = T.start; q < T.start + T.count; ++q) {
       const int v[3] = {yq[q].x, yq[q].y, yq[q].z};
       for (int k = 0; k < 3; ++k) { T.lo[k] = std::min(T.lo[k], v[k]); T.hi[k] = std::max(T.hi[k], v[k]); }
     }
+  };
+  std::vector<YTile> yleaf(ty.size()), yt;
+  for (size_t t = 0; t < ty.size(); ++t) {
+    YTile& T = yleaf[t];
+    T = YTile{};
+    T.start = ty[t].first;
+    T.count = ty[t].second;
+    ybox(T);
   }
+  for (size_t t0 = 0; t0 < yleaf.size(); t0 += kLeafPerGroup) {
+    YTile G{};
+    G.leaf = (int)t0;
+    G.nleaf = (int)std::min<size_t>(kLeafPerGroup, yleaf.size() - t0);
+    G.start = yleaf[t0].start;
+    G.count = yleaf[t0 + G.nleaf - 1].start + yleaf[t0 + G.nleaf - 1].count - G.start;
+    ybox(G);
+    yt.push_back(G);
+  }
+  if (yt.size() >= 65536 || xt.size() >= 65536)
+    return fail(DSES_E_INVALID, "cloud too large for the 16-bit work-unit encoding");
   // ---- dedup near lists (tile order): j' < j with |y_j - y_j'|_inf < bin (1 + 1e-6)
   trace("dedup near lists");
   const double thr = P->bin * (1.0 + 1e-6);
@@ -368,17 +383,17 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   noff[m] = (int)nidx.size();
   P->near_pairs = npairs;
   // dedup partners resolved inside the warp: up to two near neighbours j' < j
-  // in the same reference tile (their lanes); anything else sets the "far" bit
-  std::vector<int> tile_of(m);
+  // in the same reference group (their lanes); anything else sets "far"
+  std::vector<int> group_of(m);
   for (size_t t = 0; t < yt.size(); ++t)
-    for (int q = yt[t].start; q < yt[t].start + yt[t].count; ++q) tile_of[q] = (int)t;
+    for (int q = yt[t].start; q < yt[t].start + yt[t].count; ++q) group_of[q] = (int)t;
   for (int64_t j = 0; j < m; ++j) {
     int w = 0, nin = 0;
     bool far = false;
     for (int k = noff[j]; k < noff[j + 1]; ++k) {
       const int jj = nidx[k];
-      if (tile_of[jj] == tile_of[j] && nin < 2) {
-        w |= (jj - yt[tile_of[j]].start + 1) << (6 * nin);
+      if (group_of[jj] == group_of[j] && nin < 2) {
+        w |= (jj - yt[group_of[j]].start + 1) << (6 * nin);
         ++nin;
       } else {
         far = true;
@@ -410,6 +425,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   CK(upload(P->xt, xt, st));
   CK(upload(P->xsub, xsub, st));
   CK(upload(P->yt, yt, st));
+  CK(upload(P->yleaf, yleaf, st));
   CK(upload(P->x0, xv, st));
   CK(upload(P->ys0, c0, st));
   CK(upload(P->ys1, c1, st));
@@ -440,6 +456,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.near_off = P->near_off.as<int>(); v.near_idx = P->near_idx.as<int>();
   v.xt = P->xt.as<XTile>(); v.yt = P->yt.as<YTile>();
   v.xsub = P->xsub.as<XTile>(); v.nxs = (int)xsub.size();
+  v.yleaf = P->yleaf.as<YTile>();
   v.stats = P->stats.as<unsigned long long>();
   v.count16 = n < 65536 ? 1 : 0;
   const int64_t words = v.count16 ? (v.nbins + 1) / 2 : v.nbins;
@@ -451,6 +468,10 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)n * 16;
   const size_t lim = P->smem_optin;
   P->hsmem = v.count16 && fixed + hb <= lim;
+  if (!P->hsmem) {  // global-memory histograms always use 32-bit counts
+    v.count16 = 0;
+    v.hist_words = (int)((v.nbins + 3) / 4 * 4);
+  }
   P->psmem = fixed + pb + (P->hsmem ? hb : 0) <= lim;
   if (!P->hsmem && !P->psmem && fixed + pb <= lim) P->psmem = true;
   trace("occupancy");
@@ -601,7 +622,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
 extern "C" int dses_plan_destroy(dses_plan* P) {
   if (!P) return DSES_OK;
   cudaSetDevice(P->device);
-  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->xsub, &P->yt,
+  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->xsub, &P->yt, &P->yleaf,
                     &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->cth, &P->sth, &P->rots,
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,

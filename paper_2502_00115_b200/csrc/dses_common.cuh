@@ -20,11 +20,16 @@
 
 namespace dses {
 
-constexpr int kTile = 32;        // reference points per tile (one per lane)
+constexpr int kTile = 32;        // reference points per group (one per lane)
+constexpr int kLeaf = 8;         // reference points per leaf (an 8-lane slice of a warp)
+constexpr int kLeafPerGroup = 4; // leaves per reference group
 constexpr int kSub = 4;          // source points per sub-tile
 constexpr int kSubPerUnit = 8;   // sub-tiles per source unit (<= 32 points)
 constexpr int kGuard = 2;        // guard band in fixed-point units
-constexpr int kVoteThreads = 1024;
+#ifndef DSES_VOTE_THREADS
+#define DSES_VOTE_THREADS 768
+#endif
+constexpr int kVoteThreads = DSES_VOTE_THREADS;
 
 enum Metric { kL2 = 0, kL1 = 1, kTruncL1 = 2, kSatL0 = 3, kTruncL2 = 4 };
 
@@ -39,6 +44,7 @@ struct XTile {          // spatial tile of the (sorted) source cloud
 struct YTile {          // spatial tile of the (sorted) reference cloud
   int start, count;
   int lo[3], hi[3];     // fixed-point bounding box of Yq over the tile
+  int leaf, nleaf;      // groups: first leaf and leaf count (leaves: unused)
 };
 
 struct RotSource {      // where rotation r comes from
@@ -64,14 +70,15 @@ struct VoteParams {
   const double* xs;      // (n,3) f64, X tile order
   const double* ys;      // (m,3) f64, Y tile order
   const int4* yq;        // (m) fixed-point Yq; w = dedup partners: bits 0-5 / 6-11 = lane+1
-                         // of up to two near neighbours j' < j in the same tile, bit 12 =
-                         // "has near neighbours outside the tile / more than two"
+                         // (within the group) of up to two near neighbours j' < j of the same
+                         // group, bit 12 = "has near neighbours outside the group / more than two"
   const int* near_off;   // (m+1) CSR offsets of the dedup near lists (Y tile order)
   const int* near_idx;   // near neighbours j' < j with |y_j - y_j'|_inf < bin (1+1e-6)
   const XTile* xt;        // units: groups of <= kSubPerUnit consecutive sub-tiles
   const XTile* xsub;      // sub-tiles of <= kSub source points
   int nxs;
-  const YTile* yt;
+  const YTile* yt;        // reference groups of <= kLeafPerGroup leaves
+  const YTile* yleaf;     // reference leaves of <= kLeaf points
   RotSource rot;
   int64_t r_begin, r_count;
   // outputs (indexed r - r_begin)

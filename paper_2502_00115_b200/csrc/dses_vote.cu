@@ -59,7 +59,8 @@ __device__ __forceinline__ bool pair_bin(const VoteParams& p, const double* R, c
   return exact_bin(p, p0, p1, p2, p.ys + 3 * j, lin);
 }
 
-constexpr int kUnitCap = 4096;  // (reference tile, source unit) work units per round
+constexpr int kUnitCap = 2048;  // (reference group, source unit) work units per round
+constexpr int kRare = 64;       // per-warp list of deferred (i, j) pairs
 
 // Rotated sphere (centre +- radius, a rotation preserves |x - c|) of a source
 // tile as a fixed-point box; .w carries the tile's point range.
@@ -84,53 +85,112 @@ __device__ __forceinline__ bool boxes_meet(const VoteParams& p, const YTile& yt,
          (yt.lo[1] - hi.y < (int)p.W1) & (yt.hi[2] - lo.z >= 0) & (yt.lo[2] - hi.z < (int)p.W2);
 }
 
-// One source point i against the warp's 32 reference points (one per lane).
-// Branch-free fast path; the rare guard-band re-bin and the rare
-// out-of-tile dedup are divergent branches entered only when some lane needs
-// them.  Dedup (_kernels.py:153-158): the vote (i, j) is dropped when a near
-// neighbour j' < j lands in the same bin for the same i; in-tile neighbours
-// are other lanes of this warp, so their bins arrive by shuffle.
-template <bool PSMEM>
-__device__ __forceinline__ void vote_slot(const VoteParams& p, const double* R, const int4* P,
-                                          unsigned* hist, const int4& Y, int j, int lane, int i,
-                                          unsigned& votes, unsigned& rechecks) {
+// 32-bit shared-memory accessors (shared window addresses computed once).
+__device__ __forceinline__ int4 lds_v4(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void reds_add(uint32_t a, unsigned v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v2(uint32_t a, int x, int y) {
+  asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ int2 lds_v2(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+
+template <bool HSMEM>
+__device__ __forceinline__ void hist_inc(unsigned* hist, uint32_t hist_sh, int lin) {
+  if (HSMEM) reds_add(hist_sh + 2u * (unsigned)(lin & ~1), 1u << ((lin & 1) << 4));
+  else atomicAdd(&hist[lin], 1u);
+}
+
+// The exact general path for one deferred pair (i, j): reference binning
+// (fast fixed point, binary64 in the guard band) and the full near list of j
+// (every j' < j with |y_j - y_j'|_inf < bin): the vote counts unless some j'
+// lands in the same bin for the same i (_kernels.py:144-158).
+// Returns (votes << 16) | rechecks.
+template <bool HSMEM, bool PSMEM>
+__device__ __noinline__ unsigned vote_exact(const VoteParams& p, const double* R, const int4* P,
+                                            unsigned* hist, uint32_t hist_sh, int i, int j) {
+  unsigned rechecks = 0;
   const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
+  int lin;
+  if (!pair_bin(p, R, Pi, i, p.yq[j], j, &lin, rechecks)) return rechecks;
+  const int e1 = p.near_off[j + 1];
+  for (int k = p.near_off[j]; k < e1; ++k) {
+    const int jj = p.near_idx[k];
+    int lin2;
+    if (pair_bin(p, R, Pi, i, p.yq[jj], jj, &lin2, rechecks) && lin2 == lin) return rechecks;
+  }
+  hist_inc<HSMEM>(hist, hist_sh, lin);
+  return (1u << 16) | rechecks;
+}
+
+// Flush a warp's deferred list (n entries, <= kRare) through vote_exact.
+template <bool HSMEM, bool PSMEM>
+__device__ __noinline__ unsigned flush_rare(const VoteParams& p, const double* R, const int4* P,
+                                            unsigned* hist, uint32_t hist_sh, uint32_t rare_sh,
+                                            int n, int lane) {
+  unsigned acc = 0;
+  __syncwarp();
+  for (int e = lane; e < n; e += 32) {
+    const int2 ij = lds_v2(rare_sh + 8u * (unsigned)e);
+    acc += vote_exact<HSMEM, PSMEM>(p, R, P, hist, hist_sh, ij.x, ij.y);
+  }
+  __syncwarp();
+  return acc;
+}
+
+// One source point i against the warp's reference group (lane = j, registers).
+// Branch-free fast path.  A lane's vote is decided here unless (a) its pair
+// lies within the fixed-point guard band of a bin edge, (b) j has dedup
+// neighbours outside its group, or (c) an in-group neighbour is itself
+// undecided; those pairs are appended to the warp's deferred list and
+// finished by vote_exact.  In-group dedup (_kernels.py:153-158): the
+// neighbours j' < j of j in the same group are other lanes, so their bins
+// arrive by shuffle and an equal bin drops the vote.
+template <bool HSMEM, bool PSMEM>
+__device__ __forceinline__ void vote_slot(const VoteParams& p, const double* R, const int4* P,
+                                          uint32_t P_sh, unsigned* hist, uint32_t hist_sh,
+                                          const int4& Y, int l0, int l1, bool far, int i, int j,
+                                          unsigned lanemask_lt, int lane, uint32_t rare_sh,
+                                          int& nrare, unsigned& votes, unsigned& rechecks) {
+  const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)i) : __ldcg(&P[i]);
   const int u0 = Y.x - Pi.x, u1 = Y.y - Pi.y, u2 = Y.z - Pi.z;
   const bool cand = ((unsigned)u0 < p.W0) & ((unsigned)u1 < p.W1) & ((unsigned)u2 < p.W2);
   if (!__any_sync(0xffffffffu, cand)) return;
   const unsigned g2 = 2u * kGuard;
-  const bool near = cand & ((((unsigned)u0 & p.fmask) < g2) | (((unsigned)u1 & p.fmask) < g2) |
-                            (((unsigned)u2 & p.fmask) < g2));
-  bool in = cand & !near & ((unsigned)u0 < p.D0) & ((unsigned)u1 < p.D1) & ((unsigned)u2 < p.D2);
-  int lin = ((u0 >> p.F) * p.d1 + (u1 >> p.F)) * p.d2 + (u2 >> p.F);
-  if (__any_sync(0xffffffffu, near)) {
-    if (near) {
-      ++rechecks;
-      const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
-      in = exact_bin(p, rot_row(R, 0, x0, x1, x2), rot_row(R, 1, x0, x1, x2),
-                     rot_row(R, 2, x0, x1, x2), p.ys + 3 * j, &lin);
-    }
-  }
-  const int key = in ? lin : -1;
-  const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
+  const bool near = ((((unsigned)u0 & p.fmask) < g2) | (((unsigned)u1 & p.fmask) < g2) |
+                     (((unsigned)u2 & p.fmask) < g2));
+  const bool in = cand & ((unsigned)u0 < p.D0) & ((unsigned)u1 < p.D1) & ((unsigned)u2 < p.D2);
+  const int lin = ((u0 >> p.F) * p.d1 + (u1 >> p.F)) * p.d2 + (u2 >> p.F);
+  // key: bin when decided in window, -1 decided out, -2 undecided
+  const bool undecided = cand & near;
+  const int key = undecided ? -2 : (in ? lin : -1);
   const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
   const int k1 = __shfl_sync(0xffffffffu, key, l1 & 31);
-  bool dup = in & (((l0 >= 0) & (k0 == key)) | ((l1 >= 0) & (k1 == key)));
-  const bool far = in & !dup & ((Y.w >> 12) & 1);
-  if (__any_sync(0xffffffffu, far)) {
-    if (far) {
-      const int e1 = p.near_off[j + 1];
-      for (int k = p.near_off[j]; k < e1 && !dup; ++k) {
-        const int jj = p.near_idx[k];
-        int lin2;
-        dup = pair_bin(p, R, Pi, i, p.yq[jj], jj, &lin2, rechecks) && lin2 == lin;
-      }
-    }
-  }
-  if (in & !dup) {
+  const bool dup = ((l0 >= 0) & (k0 == key)) | ((l1 >= 0) & (k1 == key));
+  const bool defer = undecided | (in & (far | ((l0 >= 0) & (k0 == -2)) | ((l1 >= 0) & (k1 == -2))));
+  if (in & !near & !dup & !defer) {
     ++votes;
-    if (p.count16) atomicAdd(&hist[lin >> 1], (lin & 1) ? 0x10000u : 1u);
-    else atomicAdd(&hist[lin], 1u);
+    hist_inc<HSMEM>(hist, hist_sh, lin);
+  }
+  const unsigned dm = __ballot_sync(0xffffffffu, defer);
+  if (dm) {
+    if (defer) sts_v2(rare_sh + 8u * (unsigned)(nrare + __popc(dm & lanemask_lt)), i, j);
+    nrare += __popc(dm);
+    if (nrare > kRare - 32) {
+      const unsigned acc = flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, rare_sh, nrare, lane);
+      votes += acc >> 16;
+      rechecks += acc & 0xffffu;
+      nrare = 0;
+    }
   }
 }
 
@@ -156,9 +216,16 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + counters
   off += 4 * 32 * 4;
   int* units = reinterpret_cast<int*>(smem + off);  // [kUnitCap] overlapping tile pairs
+  off += (size_t)kUnitCap * 4;
+  int2* rare = reinterpret_cast<int2*>(smem + off) + warp * kRare;  // deferred pairs
+
   int* s_nunits = red + 96;
   int* s_next = red + 97;
   const unsigned lanemask_lt = (1u << lane) - 1u;
+  const uint32_t P_sh = PSMEM ? (uint32_t)__cvta_generic_to_shared(P) : 0u;
+  const uint32_t hist_sh = HSMEM ? (uint32_t)__cvta_generic_to_shared(hist) : 0u;
+  const uint32_t rare_sh = (uint32_t)__cvta_generic_to_shared(rare);
+
 
   uint4* hist4 = reinterpret_cast<uint4*>(hist);
   const int nw4 = p.hist_words >> 2;
@@ -169,7 +236,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   unsigned long long st_pairs = 0;
   unsigned st_votes = 0, st_rechecks = 0;
   const bool exact_mode = (p.F == 0);
-  const int npairs = p.nyt * p.nxt;
+  // reference tiles per round so that the round's units fit `units`
+  const int tiles_per_round = max(1, kUnitCap / max(1, p.nxt));
 
   for (int64_t rr = blockIdx.x; rr < p.r_count; rr += gridDim.x) {
     const int64_t r = p.r_begin + rr;
@@ -202,30 +270,30 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     }
     __syncthreads();
 
-    // ---- B: votes, in rounds of at most kUnitCap (reference tile, source unit) pairs.
-    //  B1  threads test tile pairs; overlapping ones are compacted into `units`;
+    // ---- B: votes, in rounds over reference tiles [b0, b1).
+    //  B1  warp w tests reference tiles b0+w, b0+w+nwarps, ... against all
+    //      source units (one per lane); overlapping (tile, unit) pairs are
+    //      compacted into `units` as b << 16 | a;
     //  B2  warps take units dynamically: lane = reference point j (registers);
     //      lanes 0..7 test the unit's sub-tiles, then each surviving sub-tile's
     //      points i are broadcast from shared memory, one vote_slot per i.
-    for (int base = 0; base < npairs; base += kUnitCap) {
+    int nrare = 0;  // warp-uniform deferred-list fill
+    for (int b0 = 0; b0 < p.nyt; b0 += tiles_per_round) {
+      const int b1 = min(p.nyt, b0 + tiles_per_round);
       if (tid == 0) { *s_nunits = 0; *s_next = 0; }
       __syncthreads();
-      const int lim = min(kUnitCap, npairs - base);
-      for (int k0 = 0; k0 < lim; k0 += nthreads) {
-        const int k = k0 + tid;
-        bool ov = false;
-        int unit = 0;
-        if (k < lim) {
-          unit = base + k;
-          const int b = unit / p.nxt, a = unit - b * p.nxt;
-          ov = exact_mode || boxes_meet(p, p.yt[b], XB[2 * a], XB[2 * a + 1]);
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, ov);
-        if (m) {
-          int slot = 0;
-          if (lane == 0) slot = atomicAdd(s_nunits, __popc(m));
-          slot = __shfl_sync(0xffffffffu, slot, 0);
-          if (ov) units[slot + __popc(m & lanemask_lt)] = unit;
+      for (int b = b0 + warp; b < b1; b += nwarps) {
+        const YTile yt = p.yt[b];
+        for (int a0 = 0; a0 < p.nxt; a0 += 32) {
+          const int a = a0 + lane;
+          const bool ov = a < p.nxt && (exact_mode || boxes_meet(p, yt, XB[2 * a], XB[2 * a + 1]));
+          const unsigned m = __ballot_sync(0xffffffffu, ov);
+          if (m) {
+            int slot = 0;
+            if (lane == 0) slot = atomicAdd(s_nunits, __popc(m));
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (ov) units[slot + __popc(m & lanemask_lt)] = (b << 16) | a;
+          }
         }
       }
       __syncthreads();
@@ -236,14 +304,15 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= nunits) break;
         const int unit = units[u];
-        const int b = unit / p.nxt, a = unit - b * p.nxt;
-        const YTile yt = p.yt[b];
+        const YTile yt = p.yt[unit >> 16];
+        const XTile& U = p.xt[unit & 0xffff];
+        const int sub0 = U.sub, nsub = U.nsub;
         const bool valid = lane < yt.count;
         const int j = yt.start + (valid ? lane : 0);
         int4 Y = p.yq[j];
         if (!valid) { Y.x = INT_MIN / 2; Y.w = 0; }  // never a candidate
-        const XTile& U = p.xt[a];
-        const int nsub = U.nsub, sub0 = U.sub;
+        const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
+        const bool far = (Y.w >> 12) & 1;
         bool sok = false;
         if (lane < nsub) sok = exact_mode || boxes_meet(p, yt, XS[2 * (sub0 + lane)], XS[2 * (sub0 + lane) + 1]);
         unsigned sm = __ballot_sync(0xffffffffu, sok);
@@ -252,12 +321,21 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
           sm &= sm - 1;
           const int i0 = XS[2 * s].w, i1 = XS[2 * s + 1].w;
           if (lane == 0) st_pairs += (unsigned long long)(i1 - i0) * yt.count;
-          for (int i = i0; i < i1; ++i)
-            vote_slot<PSMEM>(p, R, P, hist, Y, j, lane, i, st_votes, st_rechecks);
+#pragma unroll
+          for (int k = 0; k < kSub; ++k)
+            if (i0 + k < i1)
+              vote_slot<HSMEM, PSMEM>(p, R, P, P_sh, hist, hist_sh, Y, l0, l1, far, i0 + k, j,
+                                      lanemask_lt, lane, rare_sh, nrare, st_votes, st_rechecks);
         }
       }
       __syncthreads();  // units[] is rebuilt by the next round
     }
+    if (nrare > 0) {
+      const unsigned acc = flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, rare_sh, nrare, lane);
+      st_votes += acc >> 16;
+      st_rechecks += acc & 0xffffu;
+    }
+    __syncthreads();
 
     // ---- mode: scan (and re-zero) the histogram
     int best = 0, blin = INT_MAX, bties = 0;
@@ -331,6 +409,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem) {
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n * 16;
   b += (size_t)(p.nxt + p.nxs) * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)kUnitCap * 4;
+  b += (size_t)(kVoteThreads / 32) * kRare * 8;
   return b;
 }
 
