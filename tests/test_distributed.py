@@ -1,0 +1,122 @@
+"""Multi-rank DSES protocol (paper_2502_00115_b200.distributed) on CPU.
+
+world_size 2 over gloo (127.0.0.1), each rank's local stages done by the
+pinned oracle (tests/_oracle_plan.py); the sharded result must equal the
+single-process oracle dses on the same pair: winner grid coordinates and
+translation bin, candidates_evaluated / candidates_refined exactly,
+best_inliers exactly, best_error within 1e-9 relative (the reference's final
+recompute goes through a BLAS matmul).
+"""
+import math
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _case(kind):
+    from paper_2502_00115_b200 import ErrorMetric, SearchConfig
+    from paper_2502_00115_b200.synth import CONFIGS, make_pair
+    x, y, _ = make_pair(CONFIGS["c1"]["spec"], 3)
+    metric = {"trunc_l1": ErrorMetric.truncated_l1(0.125), "l1": ErrorMetric("l1"),
+              "inliers": ErrorMetric.from_name("inliers", 0.025)}[kind]
+    cfg = SearchConfig(k_rot=2, rot_step=math.radians(9.0), k_trans=20, trans_bin=0.025,
+                       metric=metric)
+    return x, y, cfg
+
+
+def _worker(rank, world, port, kind, out_path, native=False):
+    sys.path[:0] = [ROOT, HERE]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from _oracle_plan import OraclePlan
+    from paper_2502_00115_b200.distributed import dses_sharded
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, y, cfg = _case(kind)
+        if native:  # the sm_100a plan on cuda:0 for every rank; collectives on gloo (host)
+            res = dses_sharded(x, y, cfg, device=0)
+        else:
+            res = dses_sharded(x, y, cfg,
+                               plan_factory=lambda prep, c, dev: (OraclePlan(prep, c), None))
+        np.savez(f"{out_path}.{rank}.npz", grid=np.array(res.best.grid_coords),
+                 t=res.best.translation, R=res.best.rotation, err=res.best_error,
+                 inl=res.best_inliers, ev=res.candidates_evaluated,
+                 rf=res.candidates_refined, nloc=res.elapsed["rotations_local"])
+    finally:
+        dist.destroy_process_group()
+
+
+def _expected(kind):
+    from oracle import oracle as O
+    x, y, cfg = _case(kind)
+    m = cfg.metric
+    return O.dses(x, y, k_rot=cfg.k_rot, rot_step=cfg.rot_step, k_trans=cfg.k_trans,
+                  trans_bin=cfg.trans_bin, q=cfg.q, metric=(m.kind, m.param)), cfg
+
+
+def test_shard_range_partitions():
+    from paper_2502_00115_b200.distributed import shard_range
+    for total in (0, 1, 7, 125, 29791):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(total, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(e - b for b, e in spans) - min(e - b for b, e in spans) <= 1
+
+
+def _run_world(tmp_path, kind, world, native):
+    port = _free_port()
+    out = str(tmp_path / "res")
+    mp.start_processes(_worker, args=(world, port, kind, out, native), nprocs=world, join=True,
+                       start_method="spawn")
+    ref, cfg = _expected(kind)
+    nloc = 0
+    for r in range(world):
+        d = np.load(f"{out}.{r}.npz")
+        assert tuple(d["grid"]) == tuple(ref["grid_coords"])
+        assert np.array_equal(d["t"], ref["translation"])
+        assert np.array_equal(d["R"], ref["rotation"])
+        assert math.isclose(float(d["err"]), ref["best_error"], rel_tol=1e-9, abs_tol=1e-12)
+        assert int(d["inl"]) == ref["best_inliers"]
+        assert int(d["ev"]) == ref["candidates_evaluated"]
+        assert int(d["rf"]) == ref["candidates_refined"]
+        nloc += int(d["nloc"])
+    assert nloc == cfg.rotation_count
+
+
+@pytest.mark.parametrize("kind", ["trunc_l1", "l1", "inliers"])
+def test_sharded_matches_oracle_world2(tmp_path, kind):
+    _run_world(tmp_path, kind, 2, native=False)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["trunc_l1", "inliers"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_native_matches_oracle(tmp_path, kind, world):
+    """The native stages (vote / argmax / screen / re-score on the B200) under
+    the multi-rank protocol; ranks share cuda:0 but never wait on each other
+    on the device (the exchange is host-side gloo)."""
+    _run_world(tmp_path, kind, world, native=True)
+
+
+def test_single_rank_without_process_group():
+    from _oracle_plan import OraclePlan
+    from paper_2502_00115_b200.distributed import dses_sharded
+    ref, cfg = _expected("trunc_l1")
+    x, y, _ = _case("trunc_l1")
+    res = dses_sharded(x, y, cfg, plan_factory=lambda prep, c, dev: (OraclePlan(prep, c), None))
+    assert tuple(res.best.grid_coords) == tuple(ref["grid_coords"])
+    assert res.candidates_refined == ref["candidates_refined"]
