@@ -29,7 +29,7 @@ namespace dses {
 cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, int threads,
                         cudaStream_t stream);
 int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int threads);
-size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem);
+size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads);
 // dses_score.cu
 cudaError_t launch_select_stats(const int* counts, int64_t nrot, unsigned long long* mstar,
                                 unsigned long long* nvalid, int sms, cudaStream_t st);
@@ -166,7 +166,7 @@ struct dses_plan {
   bool hsmem = true, psmem = true;
   int vote_grid = 0, vote_threads = kVoteThreads;
   // device data
-  DevBuf xs, ys, yq, near_off, near_idx, xt, xsub, yt, yleaf;  // vote (tile order)
+  DevBuf xs, ys, yq, part, near_off, near_idx, xt, yt;  // vote (tile order)
   DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
   DevBuf cth, sth, rots;                               // rotation sources
   DevBuf counts, lins, ties;                           // per-rotation outputs
@@ -235,6 +235,28 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
   kd_tiles(pts, lo + left, hi, perm, tiles, tile);
 }
 
+// Unordered pairs (a, b), a != b, of reference points closer than thr in
+// every axis (sweep over the points sorted by axis 0).
+std::vector<std::pair<int, int>> near_pairs(const double* y, int64_t m, double thr) {
+  std::vector<int> o0(m);
+  std::iota(o0.begin(), o0.end(), 0);
+  std::sort(o0.begin(), o0.end(), [&](int a, int b) {
+    return y[3 * a] < y[3 * b] || (y[3 * a] == y[3 * b] && a < b);
+  });
+  std::vector<std::pair<int, int>> out;
+  for (int64_t a = 0; a < m; ++a) {
+    const int ja = o0[a];
+    for (int64_t b = a + 1; b < m; ++b) {
+      const int jb = o0[b];
+      if (y[3 * jb] - y[3 * ja] >= thr) break;
+      if (std::fabs(y[3 * jb + 1] - y[3 * ja + 1]) < thr &&
+          std::fabs(y[3 * jb + 2] - y[3 * ja + 2]) < thr)
+        out.emplace_back(ja, jb);
+    }
+  }
+  return out;
+}
+
 int build_plan(dses_plan* P, const double* x, const double* y) {
   const int64_t n = P->n, m = P->m;
   cudaStream_t st = 0;
@@ -269,8 +291,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   std::iota(px.begin(), px.end(), 0);
   std::iota(py.begin(), py.end(), 0);
   std::vector<std::pair<int, int>> tx, ty;
-  kd_tiles(x, 0, n, px, tx, kSub);   // source sub-tiles; units = kSubPerUnit consecutive ones
-  kd_tiles(y, 0, m, py, ty, kLeaf);  // reference leaves; groups = kLeafPerGroup consecutive ones
+  kd_tiles(x, 0, n, px, tx, kTile);  // source units
+  kd_tiles(y, 0, m, py, ty, kTile);  // reference groups
   std::vector<double> xs(3 * n), ys(3 * m);
   for (int64_t i = 0; i < n; ++i)
     for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
@@ -294,22 +316,13 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     }
     T.rad = F ? (int)std::ceil(rad * inv_s * (1.0 + 1e-9)) + 3 : 0;
   };
-  std::vector<XTile> xsub(tx.size()), xt;
+  std::vector<XTile> xt(tx.size());
   for (size_t t = 0; t < tx.size(); ++t) {
-    XTile& T = xsub[t];
+    XTile& T = xt[t];
     T = XTile{};
     T.start = tx[t].first;
     T.count = tx[t].second;
     sphere(T);
-  }
-  for (size_t t0 = 0; t0 < xsub.size(); t0 += kSubPerUnit) {
-    XTile U{};
-    U.sub = (int)t0;
-    U.nsub = (int)std::min<size_t>(kSubPerUnit, xsub.size() - t0);
-    U.start = xsub[t0].start;
-    U.count = xsub[t0 + U.nsub - 1].start + xsub[t0 + U.nsub - 1].count - U.start;
-    sphere(U);
-    xt.push_back(U);
   }
   // fixed-point reference: Yq = rint(fl(y*inv)*S) - lo*S + S/2 + G
   std::vector<int4> yq(m);
@@ -332,75 +345,39 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       for (int k = 0; k < 3; ++k) { T.lo[k] = std::min(T.lo[k], v[k]); T.hi[k] = std::max(T.hi[k], v[k]); }
     }
   };
-  std::vector<YTile> yleaf(ty.size()), yt;
+  std::vector<YTile> yt(ty.size());
   for (size_t t = 0; t < ty.size(); ++t) {
-    YTile& T = yleaf[t];
+    YTile& T = yt[t];
     T = YTile{};
     T.start = ty[t].first;
     T.count = ty[t].second;
     ybox(T);
-  }
-  for (size_t t0 = 0; t0 < yleaf.size(); t0 += kLeafPerGroup) {
-    YTile G{};
-    G.leaf = (int)t0;
-    G.nleaf = (int)std::min<size_t>(kLeafPerGroup, yleaf.size() - t0);
-    G.start = yleaf[t0].start;
-    G.count = yleaf[t0 + G.nleaf - 1].start + yleaf[t0 + G.nleaf - 1].count - G.start;
-    ybox(G);
-    yt.push_back(G);
   }
   if (yt.size() >= 65536 || xt.size() >= 65536)
     return fail(DSES_E_INVALID, "cloud too large for the 16-bit work-unit encoding");
   // ---- dedup near lists (tile order): j' < j with |y_j - y_j'|_inf < bin (1 + 1e-6)
   trace("dedup near lists");
   const double thr = P->bin * (1.0 + 1e-6);
-  std::vector<int> o0(m);
-  std::iota(o0.begin(), o0.end(), 0);
-  std::sort(o0.begin(), o0.end(), [&](int a, int b) {
-    return ys[3 * a] < ys[3 * b] || (ys[3 * a] == ys[3 * b] && a < b);
-  });
+  const std::vector<std::pair<int, int>> near = near_pairs(ys.data(), m, thr);
   std::vector<std::vector<int>> nl(m);
-  int64_t npairs = 0;
-  for (int64_t a = 0; a < m; ++a) {
-    const int ja = o0[a];
-    for (int64_t b = a + 1; b < m; ++b) {
-      const int jb = o0[b];
-      if (ys[3 * jb] - ys[3 * ja] >= thr) break;
-      if (std::fabs(ys[3 * jb + 1] - ys[3 * ja + 1]) < thr &&
-          std::fabs(ys[3 * jb + 2] - ys[3 * ja + 2]) < thr) {
-        if (ja < jb) nl[jb].push_back(ja); else nl[ja].push_back(jb);
-        ++npairs;
-      }
-    }
+  for (const auto& e : near) {
+    if (e.first < e.second) nl[e.second].push_back(e.first); else nl[e.first].push_back(e.second);
   }
+  const int64_t npairs = (int64_t)near.size();
   std::vector<int> noff(m + 1, 0), nidx;
   nidx.reserve((size_t)npairs);
+  std::vector<int4> part(m, make_int4(-1, -1, -1, -1));
   for (int64_t j = 0; j < m; ++j) {
     std::sort(nl[j].begin(), nl[j].end());
     noff[j] = (int)nidx.size();
     nidx.insert(nidx.end(), nl[j].begin(), nl[j].end());
+    const int np = (int)nl[j].size();
+    int* pj = &part[j].x;
+    for (int k = 0; k < std::min(np, kMaxPartners); ++k) pj[k] = nl[j][k];
+    yq[j].w = np <= kMaxPartners ? np : kMaxPartners + 1;
   }
   noff[m] = (int)nidx.size();
   P->near_pairs = npairs;
-  // dedup partners resolved inside the warp: up to two near neighbours j' < j
-  // in the same reference group (their lanes); anything else sets "far"
-  std::vector<int> group_of(m);
-  for (size_t t = 0; t < yt.size(); ++t)
-    for (int q = yt[t].start; q < yt[t].start + yt[t].count; ++q) group_of[q] = (int)t;
-  for (int64_t j = 0; j < m; ++j) {
-    int w = 0, nin = 0;
-    bool far = false;
-    for (int k = noff[j]; k < noff[j + 1]; ++k) {
-      const int jj = nidx[k];
-      if (group_of[jj] == group_of[j] && nin < 2) {
-        w |= (jj - yt[group_of[j]].start + 1) << (6 * nin);
-        ++nin;
-      } else {
-        far = true;
-      }
-    }
-    yq[j].w = w | (far ? (1 << 12) : 0);
-  }
   // ---- scoring layout: x original order, y sorted by axis 0 (stable)
   trace("scoring layout");
   std::vector<int> sy(m);
@@ -423,9 +400,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   if (nidx.empty()) nidx.push_back(0);
   CK(upload(P->near_idx, nidx, st));
   CK(upload(P->xt, xt, st));
-  CK(upload(P->xsub, xsub, st));
   CK(upload(P->yt, yt, st));
-  CK(upload(P->yleaf, yleaf, st));
+  CK(upload(P->part, part, st));
   CK(upload(P->x0, xv, st));
   CK(upload(P->ys0, c0, st));
   CK(upload(P->ys1, c1, st));
@@ -446,6 +422,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.D0 = (unsigned)(P->dims[0] * Si); v.D1 = (unsigned)(P->dims[1] * Si); v.D2 = (unsigned)(P->dims[2] * Si);
   v.W0 = v.D0 + 2 * kGuard; v.W1 = v.D1 + 2 * kGuard; v.W2 = v.D2 + 2 * kGuard;
   if (!F) { v.W0 = v.W1 = v.W2 = 0xffffffffu; }
+  else if (std::max(v.W0, std::max(v.W1, v.W2)) >= (1u << 30))
+    return fail(DSES_E_INVALID, "internal: fixed-point window overflow (F=%d)", F);
   v.inv_bin = P->inv_bin;
   v.inv_s = inv_s;
   v.flo0 = (double)P->ilo[0]; v.flo1 = (double)P->ilo[1]; v.flo2 = (double)P->ilo[2];
@@ -455,8 +433,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.xs = P->xs.as<double>(); v.ys = P->ys.as<double>(); v.yq = P->yq.as<int4>();
   v.near_off = P->near_off.as<int>(); v.near_idx = P->near_idx.as<int>();
   v.xt = P->xt.as<XTile>(); v.yt = P->yt.as<YTile>();
-  v.xsub = P->xsub.as<XTile>(); v.nxs = (int)xsub.size();
-  v.yleaf = P->yleaf.as<YTile>();
+  v.part = P->part.as<int4>();
+  v.gthr = F ? 2u * kGuard : 0xffffffffu;
   v.stats = P->stats.as<unsigned long long>();
   v.count16 = n < 65536 ? 1 : 0;
   const int64_t words = v.count16 ? (v.nbins + 1) / 2 : v.nbins;
@@ -464,8 +442,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.n_pad = (int)((n + 3) / 4 * 4);
   // shared-memory placement
   trace("shared-memory placement");
-  const size_t fixed = vote_smem_bytes(v, false, false);
-  const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)n * 16;
+  const size_t fixed = vote_smem_bytes(v, false, false, P->vote_threads);
+  const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)v.n_pad * 16;
   const size_t lim = P->smem_optin;
   P->hsmem = v.count16 && fixed + hb <= lim;
   if (!P->hsmem) {  // global-memory histograms always use 32-bit counts
@@ -481,7 +459,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     per_sm = vote_max_ctas_per_sm(v, P->hsmem, P->psmem, P->vote_threads);
   }
   if (per_sm < 1) return fail(DSES_E_CUDA, "vote kernel cannot be resident (smem %zu)",
-                              vote_smem_bytes(v, P->hsmem, P->psmem));
+                              vote_smem_bytes(v, P->hsmem, P->psmem, P->vote_threads));
   P->vote_grid = per_sm * P->sms;
   trace("plan ready");
   return DSES_OK;
@@ -622,7 +600,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
 extern "C" int dses_plan_destroy(dses_plan* P) {
   if (!P) return DSES_OK;
   cudaSetDevice(P->device);
-  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->xsub, &P->yt, &P->yleaf,
+  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->part, &P->xt, &P->yt,
                     &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->cth, &P->sth, &P->rots,
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,

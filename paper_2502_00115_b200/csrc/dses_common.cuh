@@ -20,12 +20,9 @@
 
 namespace dses {
 
-constexpr int kTile = 32;        // reference points per group (one per lane)
-constexpr int kLeaf = 8;         // reference points per leaf (an 8-lane slice of a warp)
-constexpr int kLeafPerGroup = 4; // leaves per reference group
-constexpr int kSub = 4;          // source points per sub-tile
-constexpr int kSubPerUnit = 8;   // sub-tiles per source unit (<= 32 points)
+constexpr int kTile = 32;        // points per reference group (one per lane) and per source unit
 constexpr int kGuard = 2;        // guard band in fixed-point units
+constexpr int kMaxPartners = 4;  // dedup partners resolved on the fast path (more: exact path)
 #ifndef DSES_VOTE_THREADS
 #define DSES_VOTE_THREADS 768
 #endif
@@ -36,7 +33,6 @@ enum Metric { kL2 = 0, kL1 = 1, kTruncL1 = 2, kSatL0 = 3, kTruncL2 = 4 };
 struct XTile {          // spatial tile of the (sorted) source cloud
   int start, count;
   int rad;              // bounding-sphere radius in fixed-point units (+ rounding margin)
-  int sub, nsub;        // units: first sub-tile and sub-tile count (sub-tiles: unused)
   int pad;
   double c[3];          // sphere centre (metres)
 };
@@ -44,7 +40,6 @@ struct XTile {          // spatial tile of the (sorted) source cloud
 struct YTile {          // spatial tile of the (sorted) reference cloud
   int start, count;
   int lo[3], hi[3];     // fixed-point bounding box of Yq over the tile
-  int leaf, nleaf;      // groups: first leaf and leaf count (leaves: unused)
 };
 
 struct RotSource {      // where rotation r comes from
@@ -69,16 +64,14 @@ struct VoteParams {
   int n, m, nxt, nyt;
   const double* xs;      // (n,3) f64, X tile order
   const double* ys;      // (m,3) f64, Y tile order
-  const int4* yq;        // (m) fixed-point Yq; w = dedup partners: bits 0-5 / 6-11 = lane+1
-                         // (within the group) of up to two near neighbours j' < j of the same
-                         // group, bit 12 = "has near neighbours outside the group / more than two"
-  const int* near_off;   // (m+1) CSR offsets of the dedup near lists (Y tile order)
+  const int4* yq;        // (m) fixed-point Yq; w = number of dedup partners j' < j (<= 4),
+                         // or kMaxPartners + 1 when there are more (exact path)
+  const int4* part;      // (m) the partners j' < j (tile order), -1 padded
+  const int* near_off;   // (m+1) CSR offsets of the full dedup near lists (tile order)
   const int* near_idx;   // near neighbours j' < j with |y_j - y_j'|_inf < bin (1+1e-6)
-  const XTile* xt;        // units: groups of <= kSubPerUnit consecutive sub-tiles
-  const XTile* xsub;      // sub-tiles of <= kSub source points
-  int nxs;
-  const YTile* yt;        // reference groups of <= kLeafPerGroup leaves
-  const YTile* yleaf;     // reference leaves of <= kLeaf points
+  const XTile* xt;       // source units of <= kTile points
+  const YTile* yt;       // reference groups of <= kTile points
+  unsigned gthr;         // a pair whose min fraction over the axes is < gthr is re-binned exactly
   RotSource rot;
   int64_t r_begin, r_count;
   // outputs (indexed r - r_begin)

@@ -60,6 +60,7 @@ __device__ __forceinline__ bool pair_bin(const VoteParams& p, const double* R, c
 }
 
 constexpr int kUnitCap = 2048;  // (reference group, source unit) work units per round
+constexpr int kRing = 64;       // per-warp ring of candidate (i, j) pairs (power of two)
 constexpr int kRare = 64;       // per-warp list of deferred (i, j) pairs
 
 // Rotated sphere (centre +- radius, a rotation preserves |x - c|) of a source
@@ -106,7 +107,7 @@ __device__ __forceinline__ int2 lds_v2(uint32_t a) {
 
 template <bool HSMEM>
 __device__ __forceinline__ void hist_inc(unsigned* hist, uint32_t hist_sh, int lin) {
-  if (HSMEM) reds_add(hist_sh + 2u * (unsigned)(lin & ~1), 1u << ((lin & 1) << 4));
+  if (HSMEM) reds_add(hist_sh + 2u * (unsigned)(lin & ~1), (lin & 1) ? 0x10000u : 1u);
   else atomicAdd(&hist[lin], 1u);
 }
 
@@ -147,49 +148,77 @@ __device__ __noinline__ unsigned flush_rare(const VoteParams& p, const double* R
   return acc;
 }
 
-// One source point i against the warp's reference group (lane = j, registers).
-// Branch-free fast path.  A lane's vote is decided here unless (a) its pair
-// lies within the fixed-point guard band of a bin edge, (b) j has dedup
-// neighbours outside its group, or (c) an in-group neighbour is itself
-// undecided; those pairs are appended to the warp's deferred list and
-// finished by vote_exact.  In-group dedup (_kernels.py:153-158): the
-// neighbours j' < j of j in the same group are other lanes, so their bins
-// arrive by shuffle and an equal bin drops the vote.
+// Predicated shared-memory reduction.
+__device__ __forceinline__ void reds_add_if(uint32_t a, unsigned v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}"
+               ::"r"(a), "r"(v), "r"((unsigned)pred) : "memory");
+}
+
+// Sentinel for the reference slots of a partial group: with |Pq| < 2^29 and
+// W < 2^30, u = Yq - Pq wraps to >= 2^30 > W on axis 0, so never a candidate.
+constexpr int kNoRef = -3 * (1 << 29);
+
+struct WarpQ {        // per-warp queues (warp-uniform counters)
+  uint32_t ring_sh;   // kRing (i, j) candidate pairs
+  uint32_t rare_sh;   // kRare (i, j) pairs for the exact path
+  unsigned head, tail;
+  int nrare;
+  unsigned rechecks;
+};
+
+// Finish up to 32 candidate pairs (ring entries head .. head+cnt-1), one per
+// lane: fixed-point bin, guard band, per-source dedup against the pair's
+// partners j' < j (_kernels.py:153-158), shared-memory vote.  Pairs in the
+// guard band (theirs or a partner's) and pairs of reference points with more
+// than four partners go to the exact path.
 template <bool HSMEM, bool PSMEM>
-__device__ __forceinline__ void vote_slot(const VoteParams& p, const double* R, const int4* P,
-                                          uint32_t P_sh, unsigned* hist, uint32_t hist_sh,
-                                          const int4& Y, int l0, int l1, bool far, int i, int j,
-                                          unsigned lanemask_lt, int lane, uint32_t rare_sh,
-                                          int& nrare, unsigned& votes, unsigned& rechecks) {
-  const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)i) : __ldcg(&P[i]);
-  const int u0 = Y.x - Pi.x, u1 = Y.y - Pi.y, u2 = Y.z - Pi.z;
-  const bool cand = ((unsigned)u0 < p.W0) & ((unsigned)u1 < p.W1) & ((unsigned)u2 < p.W2);
-  if (!__any_sync(0xffffffffu, cand)) return;
-  const unsigned g2 = 2u * kGuard;
-  const bool near = ((((unsigned)u0 & p.fmask) < g2) | (((unsigned)u1 & p.fmask) < g2) |
-                     (((unsigned)u2 & p.fmask) < g2));
-  const bool in = cand & ((unsigned)u0 < p.D0) & ((unsigned)u1 < p.D1) & ((unsigned)u2 < p.D2);
-  const int lin = ((u0 >> p.F) * p.d1 + (u1 >> p.F)) * p.d2 + (u2 >> p.F);
-  // key: bin when decided in window, -1 decided out, -2 undecided
-  const bool undecided = cand & near;
-  const int key = undecided ? -2 : (in ? lin : -1);
-  const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
-  const int k1 = __shfl_sync(0xffffffffu, key, l1 & 31);
-  const bool dup = ((l0 >= 0) & (k0 == key)) | ((l1 >= 0) & (k1 == key));
-  const bool defer = undecided | (in & (far | ((l0 >= 0) & (k0 == -2)) | ((l1 >= 0) & (k1 == -2))));
-  if (in & !near & !dup & !defer) {
-    ++votes;
-    hist_inc<HSMEM>(hist, hist_sh, lin);
+__device__ __forceinline__ void drain_pass(const VoteParams& p, const double* R, const int4* P,
+                                           uint32_t P_sh, unsigned* hist, uint32_t hist_sh,
+                                           WarpQ& q, int cnt, int lane, unsigned lanemask_lt) {
+  const bool active = lane < cnt;
+  int2 ij = make_int2(0, 0);
+  if (active) ij = lds_v2(q.ring_sh + 8u * ((q.head + (unsigned)lane) & (kRing - 1)));
+  const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)ij.x) : __ldcg(&P[ij.x]);
+  const int4 Yj = __ldg(&p.yq[ij.y]);
+  const unsigned u0 = (unsigned)(Yj.x - Pi.x), u1 = (unsigned)(Yj.y - Pi.y), u2 = (unsigned)(Yj.z - Pi.z);
+  const unsigned f = __vimin3_u32(u0 & p.fmask, u1 & p.fmask, u2 & p.fmask);
+  bool near = active & (f < p.gthr);
+  bool ok = active & !near;
+  const bool partners = ok & (Yj.w != 0);
+  if (__any_sync(0xffffffffu, partners)) {
+    if (partners) {
+      if (Yj.w > 4) {
+        near = true;
+        ok = false;
+      } else {
+        const int4 pt = __ldg(&p.part[ij.y]);
+        const int pj[4] = {pt.x, pt.y, pt.z, pt.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k < Yj.w) {
+            const int4 Y2 = __ldg(&p.yq[pj[k]]);
+            const unsigned v0 = (unsigned)(Y2.x - Pi.x), v1 = (unsigned)(Y2.y - Pi.y),
+                           v2 = (unsigned)(Y2.z - Pi.z);
+            if ((v0 < p.W0) & (v1 < p.W1) & (v2 < p.W2)) {
+              if (__vimin3_u32(v0 & p.fmask, v1 & p.fmask, v2 & p.fmask) < p.gthr) near = true;
+              else if ((((u0 ^ v0) | (u1 ^ v1) | (u2 ^ v2)) >> p.F) == 0u) ok = false;
+            }
+          }
+        }
+        ok &= !near;
+      }
+    }
   }
-  const unsigned dm = __ballot_sync(0xffffffffu, defer);
+  const unsigned lin = ((u0 >> p.F) * (unsigned)p.d1 + (u1 >> p.F)) * (unsigned)p.d2 + (u2 >> p.F);
+  if (HSMEM) reds_add_if(hist_sh + ((lin << 1) & ~3u), 1u + (lin & 1u) * 0xffffu, ok);
+  else if (ok) atomicAdd(&hist[lin], 1u);
+  const unsigned dm = __ballot_sync(0xffffffffu, near);
   if (dm) {
-    if (defer) sts_v2(rare_sh + 8u * (unsigned)(nrare + __popc(dm & lanemask_lt)), i, j);
-    nrare += __popc(dm);
-    if (nrare > kRare - 32) {
-      const unsigned acc = flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, rare_sh, nrare, lane);
-      votes += acc >> 16;
-      rechecks += acc & 0xffffu;
-      nrare = 0;
+    if (near) sts_v2(q.rare_sh + 8u * (unsigned)(q.nrare + __popc(dm & lanemask_lt)), ij.x, ij.y);
+    q.nrare += __popc(dm);
+    if (q.nrare > kRare - 32) {
+      q.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, q.rare_sh, q.nrare, lane) & 0xffffu;
+      q.nrare = 0;
     }
   }
 }
@@ -205,27 +234,31 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   if (HSMEM) { hist = reinterpret_cast<unsigned*>(smem); off += (size_t)p.hist_words * 4; }
   else hist = p.hist_global + (size_t)blockIdx.x * p.hist_words;
   int4* P;
-  if (PSMEM) { P = reinterpret_cast<int4*>(smem + off); off += (size_t)p.n * 16; }
+  if (PSMEM) { P = reinterpret_cast<int4*>(smem + off); off += (size_t)p.n_pad * 16; }
   else P = p.p_global + (size_t)blockIdx.x * p.n_pad;
   int4* XB = reinterpret_cast<int4*>(smem + off);  // [2*nxt] rotated unit boxes (lo, hi)
   off += (size_t)p.nxt * 32;
-  int4* XS = reinterpret_cast<int4*>(smem + off);  // [2*nxs] rotated sub-tile boxes
-  off += (size_t)p.nxs * 32;
   double* R = reinterpret_cast<double*>(smem + off);
   off += 16 * 8;
   int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + counters
   off += 4 * 32 * 4;
-  int* units = reinterpret_cast<int*>(smem + off);  // [kUnitCap] overlapping tile pairs
+  int* units = reinterpret_cast<int*>(smem + off);  // [kUnitCap] overlapping (group, unit) pairs
   off += (size_t)kUnitCap * 4;
-  int2* rare = reinterpret_cast<int2*>(smem + off) + warp * kRare;  // deferred pairs
+  int2* ring = reinterpret_cast<int2*>(smem + off) + warp * kRing;
+  off += (size_t)nwarps * kRing * 8;
+  int2* rare = reinterpret_cast<int2*>(smem + off) + warp * kRare;
 
   int* s_nunits = red + 96;
   int* s_next = red + 97;
   const unsigned lanemask_lt = (1u << lane) - 1u;
   const uint32_t P_sh = PSMEM ? (uint32_t)__cvta_generic_to_shared(P) : 0u;
   const uint32_t hist_sh = HSMEM ? (uint32_t)__cvta_generic_to_shared(hist) : 0u;
-  const uint32_t rare_sh = (uint32_t)__cvta_generic_to_shared(rare);
-
+  WarpQ q;
+  q.ring_sh = (uint32_t)__cvta_generic_to_shared(ring);
+  q.rare_sh = (uint32_t)__cvta_generic_to_shared(rare);
+  q.head = q.tail = 0;
+  q.nrare = 0;
+  q.rechecks = 0;
 
   uint4* hist4 = reinterpret_cast<uint4*>(hist);
   const int nw4 = p.hist_words >> 2;
@@ -233,10 +266,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     if (HSMEM) hist4[w] = make_uint4(0, 0, 0, 0); else __stcg(&hist4[w], make_uint4(0, 0, 0, 0));
   }
 
-  unsigned long long st_pairs = 0;
-  unsigned st_votes = 0, st_rechecks = 0;
+  unsigned long long st_pairs = 0, st_votes = 0;
   const bool exact_mode = (p.F == 0);
-  // reference tiles per round so that the round's units fit `units`
+  // reference groups per round so that the round's units fit `units`
   const int tiles_per_round = max(1, kUnitCap / max(1, p.nxt));
 
   for (int64_t rr = blockIdx.x; rr < p.r_count; rr += gridDim.x) {
@@ -244,40 +276,36 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     if (tid < 9) R[tid] = rotation_entry(p.rot, r, tid);
     __syncthreads();
 
-    // ---- A: rotated source points in fixed point (fp64, the reference's op
-    //      order) and rotated unit / sub-tile boxes
+    // ---- A: rotated source points in fixed point (binary64 in the reference's
+    //      operation order, then one rounding) and rotated unit boxes
     for (int i = tid; i < p.n; i += nthreads) {
       const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
-      int4 q = make_int4(0, 0, 0, 0);
+      int4 v = make_int4(0, 0, 0, 0);
       if (!exact_mode) {
-        q.x = __double2int_rn(dmul(rot_row(R, 0, x0, x1, x2), p.inv_s));
-        q.y = __double2int_rn(dmul(rot_row(R, 1, x0, x1, x2), p.inv_s));
-        q.z = __double2int_rn(dmul(rot_row(R, 2, x0, x1, x2), p.inv_s));
+        v.x = __double2int_rn(dmul(rot_row(R, 0, x0, x1, x2), p.inv_s));
+        v.y = __double2int_rn(dmul(rot_row(R, 1, x0, x1, x2), p.inv_s));
+        v.z = __double2int_rn(dmul(rot_row(R, 2, x0, x1, x2), p.inv_s));
       }
-      if (PSMEM) P[i] = q; else __stcg(&P[i], q);
+      if (PSMEM) P[i] = v; else __stcg(&P[i], v);
     }
-    for (int t = tid; t < p.nxt + p.nxs; t += nthreads) {
+    for (int t = tid; t < p.nxt; t += nthreads) {
       int4 lo, hi;
-      if (t < p.nxt) {
-        tile_box(p, R, p.xt[t], exact_mode, lo, hi);
-        XB[2 * t] = lo;
-        XB[2 * t + 1] = hi;
-      } else {
-        tile_box(p, R, p.xsub[t - p.nxt], exact_mode, lo, hi);
-        XS[2 * (t - p.nxt)] = lo;
-        XS[2 * (t - p.nxt) + 1] = hi;
-      }
+      tile_box(p, R, p.xt[t], exact_mode, lo, hi);
+      XB[2 * t] = lo;
+      XB[2 * t + 1] = hi;
     }
     __syncthreads();
 
-    // ---- B: votes, in rounds over reference tiles [b0, b1).
-    //  B1  warp w tests reference tiles b0+w, b0+w+nwarps, ... against all
-    //      source units (one per lane); overlapping (tile, unit) pairs are
-    //      compacted into `units` as b << 16 | a;
+    // ---- B: votes, in rounds over reference groups [b0, b1).
+    //  B1  warp w tests groups b0+w, b0+w+nwarps, ... against every source
+    //      unit (one per lane); overlapping (group, unit) pairs are compacted
+    //      into `units` as b << 16 | a;
     //  B2  warps take units dynamically: lane = reference point j (registers);
-    //      lanes 0..7 test the unit's sub-tiles, then each surviving sub-tile's
-    //      points i are broadcast from shared memory, one vote_slot per i.
-    int nrare = 0;  // warp-uniform deferred-list fill
+    //      each lane tests one source point of the unit against the group's
+    //      box, then every surviving source i is broadcast from shared memory
+    //      and the candidate lanes (u inside the guard-extended window)
+    //      append (i, j) to the warp's ring; full rings of 32 are drained by
+    //      drain_pass, one pair per lane.
     for (int b0 = 0; b0 < p.nyt; b0 += tiles_per_round) {
       const int b1 = min(p.nyt, b0 + tiles_per_round);
       if (tid == 0) { *s_nunits = 0; *s_next = 0; }
@@ -306,34 +334,47 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         const int unit = units[u];
         const YTile yt = p.yt[unit >> 16];
         const XTile& U = p.xt[unit & 0xffff];
-        const int sub0 = U.sub, nsub = U.nsub;
+        const int ustart = U.start, ucount = U.count;
         const bool valid = lane < yt.count;
         const int j = yt.start + (valid ? lane : 0);
-        int4 Y = p.yq[j];
-        if (!valid) { Y.x = INT_MIN / 2; Y.w = 0; }  // never a candidate
-        const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
-        const bool far = (Y.w >> 12) & 1;
+        int4 Y = __ldg(&p.yq[j]);
+        if (!valid) Y.x = kNoRef;
         bool sok = false;
-        if (lane < nsub) sok = exact_mode || boxes_meet(p, yt, XS[2 * (sub0 + lane)], XS[2 * (sub0 + lane) + 1]);
+        if (lane < ucount) {
+          const int4 Pl = PSMEM ? lds_v4(P_sh + 16u * (unsigned)(ustart + lane)) : __ldcg(&P[ustart + lane]);
+          sok = exact_mode || ((yt.hi[0] - Pl.x >= 0) & (yt.lo[0] - Pl.x < (int)p.W0) &
+                               (yt.hi[1] - Pl.y >= 0) & (yt.lo[1] - Pl.y < (int)p.W1) &
+                               (yt.hi[2] - Pl.z >= 0) & (yt.lo[2] - Pl.z < (int)p.W2));
+        }
         unsigned sm = __ballot_sync(0xffffffffu, sok);
+        if (lane == 0) st_pairs += (unsigned long long)__popc(sm) * (unsigned)yt.count;
         while (sm) {
-          const int s = sub0 + __ffs(sm) - 1;
+          const int i = ustart + __ffs(sm) - 1;
           sm &= sm - 1;
-          const int i0 = XS[2 * s].w, i1 = XS[2 * s + 1].w;
-          if (lane == 0) st_pairs += (unsigned long long)(i1 - i0) * yt.count;
-#pragma unroll
-          for (int k = 0; k < kSub; ++k)
-            if (i0 + k < i1)
-              vote_slot<HSMEM, PSMEM>(p, R, P, P_sh, hist, hist_sh, Y, l0, l1, far, i0 + k, j,
-                                      lanemask_lt, lane, rare_sh, nrare, st_votes, st_rechecks);
+          const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)i) : __ldcg(&P[i]);
+          const unsigned u0 = (unsigned)(Y.x - Pi.x), u1 = (unsigned)(Y.y - Pi.y),
+                         u2 = (unsigned)(Y.z - Pi.z);
+          const bool cand = valid & (u0 < p.W0) & (u1 < p.W1) & (u2 < p.W2);
+          const unsigned m = __ballot_sync(0xffffffffu, cand);
+          if (m) {
+            if (cand) sts_v2(q.ring_sh + 8u * ((q.tail + __popc(m & lanemask_lt)) & (kRing - 1)), i, j);
+            q.tail += __popc(m);
+            if (q.tail - q.head >= 32) {
+              drain_pass<HSMEM, PSMEM>(p, R, P, P_sh, hist, hist_sh, q, 32, lane, lanemask_lt);
+              q.head += 32;
+            }
+          }
         }
       }
       __syncthreads();  // units[] is rebuilt by the next round
     }
-    if (nrare > 0) {
-      const unsigned acc = flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, rare_sh, nrare, lane);
-      st_votes += acc >> 16;
-      st_rechecks += acc & 0xffffu;
+    if (q.tail != q.head) {
+      drain_pass<HSMEM, PSMEM>(p, R, P, P_sh, hist, hist_sh, q, (int)(q.tail - q.head), lane, lanemask_lt);
+    }
+    q.head = q.tail = 0;
+    if (q.nrare > 0) {
+      q.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, q.rare_sh, q.nrare, lane) & 0xffffu;
+      q.nrare = 0;
     }
     __syncthreads();
 
@@ -346,6 +387,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       if (HSMEM) hist4[w] = make_uint4(0, 0, 0, 0); else __stcg(&hist4[w], make_uint4(0, 0, 0, 0));
       const unsigned vv[4] = {v.x, v.y, v.z, v.w};
       if (p.count16) {
+        st_votes += (v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) +
+                    (v.z & 0xffffu) + (v.z >> 16) + (v.w & 0xffffu) + (v.w >> 16);
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
           const int c = (int)((vv[h >> 1] >> ((h & 1) * 16)) & 0xffffu);
@@ -353,6 +396,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
           else if (c == best && c > 0) ++bties;
         }
       } else {
+        st_votes += (unsigned long long)v.x + v.y + v.z + v.w;
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const int c = (int)vv[h];
@@ -391,6 +435,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   }
 
   // kernel statistics
+  unsigned long long st_rechecks = q.rechecks;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     st_pairs += __shfl_xor_sync(0xffffffffu, st_pairs, o);
@@ -399,23 +444,23 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   }
   if (lane == 0) {
     atomicAdd(&p.stats[0], st_pairs);
-    atomicAdd(&p.stats[1], (unsigned long long)st_votes);
-    atomicAdd(&p.stats[2], (unsigned long long)st_rechecks);
+    atomicAdd(&p.stats[1], st_votes);
+    atomicAdd(&p.stats[2], st_rechecks);
   }
 }
 
-size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem) {
+size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads) {
   size_t b = 0;
   if (hsmem) b += (size_t)p.hist_words * 4;
-  if (psmem) b += (size_t)p.n * 16;
-  b += (size_t)(p.nxt + p.nxs) * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)kUnitCap * 4;
-  b += (size_t)(kVoteThreads / 32) * kRare * 8;
+  if (psmem) b += (size_t)p.n_pad * 16;
+  b += (size_t)p.nxt * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)kUnitCap * 4;
+  b += (size_t)(threads / 32) * (kRing + kRare) * 8;
   return b;
 }
 
 cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, int threads,
                         cudaStream_t stream) {
-  const size_t smem = vote_smem_bytes(p, hsmem, psmem);
+  const size_t smem = vote_smem_bytes(p, hsmem, psmem, threads);
   cudaError_t e;
 #define DSES_LAUNCH(H, PS)                                                                    \
   e = cudaFuncSetAttribute(vote_kernel<H, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
@@ -431,22 +476,17 @@ cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, i
 }
 
 int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int threads) {
-  const size_t smem = vote_smem_bytes(p, hsmem, psmem);
+  const size_t smem = vote_smem_bytes(p, hsmem, psmem, threads);
   int n = 0;
   cudaError_t e;
-  if (hsmem && psmem) {
-    cudaFuncSetAttribute(vote_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<true, true>, threads, smem);
-  } else if (hsmem) {
-    cudaFuncSetAttribute(vote_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<true, false>, threads, smem);
-  } else if (psmem) {
-    cudaFuncSetAttribute(vote_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<false, true>, threads, smem);
-  } else {
-    cudaFuncSetAttribute(vote_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<false, false>, threads, smem);
-  }
+#define DSES_OCC(H, PS)                                                                            \
+  cudaFuncSetAttribute(vote_kernel<H, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<H, PS>, threads, smem);
+  if (hsmem && psmem) { DSES_OCC(true, true) }
+  else if (hsmem) { DSES_OCC(true, false) }
+  else if (psmem) { DSES_OCC(false, true) }
+  else { DSES_OCC(false, false) }
+#undef DSES_OCC
   return e == cudaSuccess ? n : 0;
 }
 

@@ -1,18 +1,26 @@
-import sys, time
+"""Vote-kernel / search timing of one config (best of 3 searches) for A/B work."""
+import sys
 sys.path.insert(0, '.')
 from paper_2502_00115_b200 import _native
-if len(sys.argv) > 2: _native.LIB_PATH = sys.argv[2]
+if len(sys.argv) > 2:
+    _native.LIB_PATH = sys.argv[2]
 _native.load(_native.LIB_PATH)
 import bench
 from paper_2502_00115_b200.engines import prepare
 from paper_2502_00115_b200.synth import make_pair
-c = bench.workload(sys.argv[1]); cfg = bench.search_config(c)
+c = bench.workload(sys.argv[1])
+cfg = bench.search_config(c)
 x, y, _ = make_pair(c['spec'], 0)
 p = prepare(x, y, cfg)
 plan = _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims)
 g = _native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot)
-best = 1e9
+best, tot = 1e9, 1e9
 for rep in range(3):
     r = plan.search(g, cfg.q, p.code, p.param, p.skip_refine)
     best = min(best, r['ms_vote_kernel'])
-print(_native.LIB_PATH.split('/')[-1], sys.argv[1], f"vote kernel {best:.2f} ms", plan.stats() if False else '', r['winner_row'], r['mstar'])
+    tot = min(tot, r['ms_total'])
+R = cfg.rotation_count
+print(f"{sys.argv[1]} R={R} vote {best:.3f} ms ({R / best * 1e3:.3e} rot/s) total {tot:.3f} ms "
+      f"pairs/rot {r['pairs_evaluated'] / R:.0f} votes/rot {r['votes'] / R:.0f} "
+      f"rechecks {r['rechecks']} info {plan.info()} winner {r['winner_row']} M* {r['mstar']} "
+      f"refined {r['candidates_refined']} rescored {r['rescored']}", flush=True)
