@@ -156,7 +156,7 @@ static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
 struct dses_plan {
   int device = 0, sms = 0;
   size_t smem_optin = 0;
-  int64_t n = 0, m = 0;
+  int64_t n = 0, m = 0, m_pad = 0;
   double bin = 0, inv_bin = 0;
   int64_t ilo[3] = {0, 0, 0}, dims[3] = {1, 1, 1};
   int F = 0;
@@ -166,7 +166,7 @@ struct dses_plan {
   bool hsmem = true, psmem = true;
   int vote_grid = 0, vote_threads = kVoteThreads;
   // device data
-  DevBuf xs, ys, yq, part, near_off, near_idx, xt, yt;  // vote (tile order)
+  DevBuf xs, ys, yq, near_off, near_idx, xt, yt;  // vote (tile order)
   DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
   DevBuf cth, sth, rots;                               // rotation sources
   DevBuf counts, lins, ties;                           // per-rotation outputs
@@ -235,6 +235,39 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
   kd_tiles(pts, lo + left, hi, perm, tiles, tile);
 }
 
+// Like kd_tiles for weighted items (centroids cen, weights wt): leaves hold
+// items of total weight <= cap; splits are placed so that the left part fills
+// whole leaves where the weights allow.
+void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int64_t hi,
+                 std::vector<int>& perm, std::vector<std::pair<int, int>>& tiles, int cap) {
+  int64_t W = 0;
+  for (int64_t q = lo; q < hi; ++q) W += wt[perm[q]];
+  if (W <= cap || hi - lo <= 1) {
+    if (hi > lo) tiles.emplace_back((int)lo, (int)(hi - lo));
+    return;
+  }
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t q = lo; q < hi; ++q)
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = std::min(mn[k], cen[3 * perm[q] + k]);
+      mx[k] = std::max(mx[k], cen[3 * perm[q] + k]);
+    }
+  int axis = 0;
+  for (int k = 1; k < 3; ++k)
+    if (mx[k] - mn[k] > mx[axis] - mn[axis]) axis = k;
+  std::sort(perm.begin() + lo, perm.begin() + hi, [&](int a, int b) {
+    const double va = cen[3 * a + axis], vb = cen[3 * b + axis];
+    return va < vb || (va == vb && a < b);
+  });
+  const int64_t ntile = (W + cap - 1) / cap;
+  const int64_t target = std::max<int64_t>(1, ntile / 2) * cap;
+  int64_t s = lo, acc = 0;
+  while (s < hi - 1 && acc + wt[perm[s]] <= target) acc += wt[perm[s++]];
+  if (s == lo) s = lo + 1;
+  kd_weighted(cen, wt, lo, s, perm, tiles, cap);
+  kd_weighted(cen, wt, s, hi, perm, tiles, cap);
+}
+
 // Unordered pairs (a, b), a != b, of reference points closer than thr in
 // every axis (sweep over the points sorted by axis 0).
 std::vector<std::pair<int, int>> near_pairs(const double* y, int64_t m, double thr) {
@@ -287,17 +320,13 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
 
   // ---- spatial tiles
   trace("spatial tiles");
-  std::vector<int> px(n), py(m);
+  std::vector<int> px(n);
   std::iota(px.begin(), px.end(), 0);
-  std::iota(py.begin(), py.end(), 0);
-  std::vector<std::pair<int, int>> tx, ty;
+  std::vector<std::pair<int, int>> tx;
   kd_tiles(x, 0, n, px, tx, kTile);  // source units
-  kd_tiles(y, 0, m, py, ty, kTile);  // reference groups
-  std::vector<double> xs(3 * n), ys(3 * m);
+  std::vector<double> xs(3 * n);
   for (int64_t i = 0; i < n; ++i)
     for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
-  for (int64_t j = 0; j < m; ++j)
-    for (int k = 0; k < 3; ++k) ys[3 * j + k] = y[3 * py[j] + k];
   const double inv_s = P->inv_bin * S;
   // sphere (bbox centre, max distance) of source points [start, start+count)
   auto sphere = [&](XTile& T) {
@@ -324,59 +353,133 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     T.count = tx[t].second;
     sphere(T);
   }
+  // ---- reference layout.  Dedup partners (points closer than one bin per
+  // axis: the only pairs that can share a bin for one source) form
+  // components; groups of <= 32 points (one per lane) are k-d tiles over the
+  // components, so that every partner of a point sits in the same warp and
+  // the per-source dedup is a lane shuffle.  Points of components larger
+  // than kMaxComp, and points with more than two earlier partners, are
+  // flagged "far" and take the exact path when they vote.
+  trace("dedup components");
+  const double thr = P->bin * (1.0 + 1e-6);
+  const std::vector<std::pair<int, int>> near = near_pairs(y, m, thr);
+  std::vector<std::vector<int>> adj(m);
+  for (const auto& e : near) {
+    adj[e.first].push_back(e.second);
+    adj[e.second].push_back(e.first);
+  }
+  std::vector<std::vector<int>> items;  // components (or single points of big ones)
+  std::vector<char> item_far;
+  {
+    std::vector<char> seen(m, 0);
+    for (int64_t s0 = 0; s0 < m; ++s0) {
+      if (seen[s0]) continue;
+      std::vector<int> c(1, (int)s0);
+      seen[s0] = 1;
+      for (size_t h = 0; h < c.size(); ++h)
+        for (int v : adj[c[h]])
+          if (!seen[v]) { seen[v] = 1; c.push_back(v); }
+      std::sort(c.begin(), c.end());
+      if ((int)c.size() <= kMaxComp) {
+        items.push_back(std::move(c));
+        item_far.push_back(0);
+      } else {
+        for (int v : c) { items.push_back(std::vector<int>(1, v)); item_far.push_back(1); }
+      }
+    }
+  }
+  std::vector<double> cen(3 * items.size());
+  std::vector<int> wt(items.size());
+  for (size_t q = 0; q < items.size(); ++q) {
+    wt[q] = (int)items[q].size();
+    for (int k = 0; k < 3; ++k) {
+      double acc = 0;
+      for (int v : items[q]) acc += y[3 * v + k];
+      cen[3 * q + k] = acc / (double)items[q].size();
+    }
+  }
+  std::vector<int> iperm(items.size());
+  std::iota(iperm.begin(), iperm.end(), 0);
+  std::vector<std::pair<int, int>> itiles;
+  kd_weighted(cen.data(), wt, 0, (int64_t)items.size(), iperm, itiles, kTile);
+  std::vector<int> yidx;  // tile-order entry -> original reference index
+  std::vector<char> yfar;
+  struct GroupSpan { int start, count, gm; };
+  std::vector<GroupSpan> groups;
+  for (const auto& t : itiles) {
+    const int start = (int)yidx.size();
+    for (int q = t.first; q < t.first + t.second; ++q)
+      for (int v : items[iperm[q]]) {
+        yidx.push_back(v);
+        yfar.push_back(item_far[iperm[q]]);
+      }
+    groups.push_back({start, (int)yidx.size() - start, 1});
+  }
+  const int64_t mp = (int64_t)yidx.size();  // padded reference entries
+  P->m_pad = mp;
+  std::vector<double> ys(3 * mp, 0.0);
+  for (int64_t q = 0; q < mp; ++q)
+    for (int k = 0; k < 3; ++k) ys[3 * q + k] = y[3 * yidx[q] + k];
   // fixed-point reference: Yq = rint(fl(y*inv)*S) - lo*S + S/2 + G
-  std::vector<int4> yq(m);
+  std::vector<int4> yq(mp);
   const int64_t Si = (int64_t)1 << F;
-  for (int64_t j = 0; j < m; ++j) {
+  for (int64_t q = 0; q < mp; ++q) {
     int v[3];
     for (int k = 0; k < 3; ++k) {
-      int64_t q = F ? rint64((ys[3 * j + k] * P->inv_bin) * S) - P->ilo[k] * Si + Si / 2 + kGuard : 0;
-      if (q > (1ll << 30) || q < -(1ll << 30)) {
+      int64_t w = F ? rint64((ys[3 * q + k] * P->inv_bin) * S) - P->ilo[k] * Si + Si / 2 + kGuard : 0;
+      if (w > (1ll << 30) || w < -(1ll << 30)) {
         return fail(DSES_E_INVALID, "internal: fixed-point overflow (F=%d)", F);
       }
-      v[k] = (int)q;
+      v[k] = (int)w;
     }
-    yq[j] = make_int4(v[0], v[1], v[2], 0);  // .w = has-near flag, set below
+    yq[q] = make_int4(v[0], v[1], v[2], 0);
   }
-  auto ybox = [&](YTile& T) {
-    for (int k = 0; k < 3; ++k) { T.lo[k] = INT32_MAX; T.hi[k] = INT32_MIN; }
-    for (int q = T.start; q < T.start + T.count; ++q) {
-      const int v[3] = {yq[q].x, yq[q].y, yq[q].z};
-      for (int k = 0; k < 3; ++k) { T.lo[k] = std::min(T.lo[k], v[k]); T.hi[k] = std::max(T.hi[k], v[k]); }
-    }
-  };
-  std::vector<YTile> yt(ty.size());
-  for (size_t t = 0; t < ty.size(); ++t) {
+  std::vector<int> pos(m);
+  for (int64_t q = 0; q < mp; ++q) pos[yidx[q]] = (int)q;
+  std::vector<YTile> yt(groups.size());
+  for (size_t t = 0; t < groups.size(); ++t) {
     YTile& T = yt[t];
     T = YTile{};
-    T.start = ty[t].first;
-    T.count = ty[t].second;
-    ybox(T);
+    T.start = groups[t].start;
+    T.count = groups[t].count;
+    T.gm = 0;  // max earlier partners resolved by shuffle in this group
+    for (int k = 0; k < 3; ++k) { T.lo[k] = INT32_MAX; T.hi[k] = INT32_MIN; }
+    for (int q = T.start; q < T.start + T.count; ++q) {
+      ++T.npts;
+      const int v[3] = {yq[q].x, yq[q].y, yq[q].z};
+      for (int k = 0; k < 3; ++k) { T.lo[k] = std::min(T.lo[k], v[k]); T.hi[k] = std::max(T.hi[k], v[k]); }
+      // earlier partners (tile order) of point q: lanes of the same group
+      int w = 0, ne = 0;
+      bool far = yfar[q];
+      for (int v2 : adj[yidx[q]]) {
+        const int q2 = pos[v2];
+        if (q2 >= q) continue;
+        if (q2 < T.start || ne == 2) { far = true; continue; }
+        w |= (q2 - T.start + 1) << (6 * ne);
+        ++ne;
+      }
+      if (!far) T.gm = std::max(T.gm, ne);
+      yq[q].w = far ? kFarFlag : w;
+    }
   }
   if (yt.size() >= 65536 || xt.size() >= 65536)
     return fail(DSES_E_INVALID, "cloud too large for the 16-bit work-unit encoding");
-  // ---- dedup near lists (tile order): j' < j with |y_j - y_j'|_inf < bin (1 + 1e-6)
+  // ---- full dedup near lists (tile order, j' < j) for the exact path
   trace("dedup near lists");
-  const double thr = P->bin * (1.0 + 1e-6);
-  const std::vector<std::pair<int, int>> near = near_pairs(ys.data(), m, thr);
-  std::vector<std::vector<int>> nl(m);
+  std::vector<std::vector<int>> nl(mp);
   for (const auto& e : near) {
-    if (e.first < e.second) nl[e.second].push_back(e.first); else nl[e.first].push_back(e.second);
+    const int a = pos[e.first], b = pos[e.second];
+    if (a < b) nl[b].push_back(a); else nl[a].push_back(b);
   }
   const int64_t npairs = (int64_t)near.size();
-  std::vector<int> noff(m + 1, 0), nidx;
+  std::vector<int> noff(mp + 1, 0), nidx;
   nidx.reserve((size_t)npairs);
-  std::vector<int4> part(m, make_int4(-1, -1, -1, -1));
-  for (int64_t j = 0; j < m; ++j) {
-    std::sort(nl[j].begin(), nl[j].end());
-    noff[j] = (int)nidx.size();
-    nidx.insert(nidx.end(), nl[j].begin(), nl[j].end());
-    const int np = (int)nl[j].size();
-    int* pj = &part[j].x;
-    for (int k = 0; k < std::min(np, kMaxPartners); ++k) pj[k] = nl[j][k];
-    yq[j].w = np <= kMaxPartners ? np : kMaxPartners + 1;
+  for (int64_t q = 0; q < mp; ++q) {
+    std::sort(nl[q].begin(), nl[q].end());
+    noff[q] = (int)nidx.size();
+    nidx.insert(nidx.end(), nl[q].begin(), nl[q].end());
   }
-  noff[m] = (int)nidx.size();
+  noff[mp] = (int)nidx.size();
   P->near_pairs = npairs;
   // ---- scoring layout: x original order, y sorted by axis 0 (stable)
   trace("scoring layout");
@@ -401,7 +504,6 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   CK(upload(P->near_idx, nidx, st));
   CK(upload(P->xt, xt, st));
   CK(upload(P->yt, yt, st));
-  CK(upload(P->part, part, st));
   CK(upload(P->x0, xv, st));
   CK(upload(P->ys0, c0, st));
   CK(upload(P->ys1, c1, st));
@@ -421,7 +523,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.fmask = F ? (unsigned)(Si - 1) : 0u;
   v.D0 = (unsigned)(P->dims[0] * Si); v.D1 = (unsigned)(P->dims[1] * Si); v.D2 = (unsigned)(P->dims[2] * Si);
   v.W0 = v.D0 + 2 * kGuard; v.W1 = v.D1 + 2 * kGuard; v.W2 = v.D2 + 2 * kGuard;
-  if (!F) { v.W0 = v.W1 = v.W2 = 0xffffffffu; }
+  if (!F) { v.W0 = v.W1 = v.W2 = 0x7fffffffu; }  // every pair (not the sentinels) is a candidate
   else if (std::max(v.W0, std::max(v.W1, v.W2)) >= (1u << 30))
     return fail(DSES_E_INVALID, "internal: fixed-point window overflow (F=%d)", F);
   v.inv_bin = P->inv_bin;
@@ -433,7 +535,6 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.xs = P->xs.as<double>(); v.ys = P->ys.as<double>(); v.yq = P->yq.as<int4>();
   v.near_off = P->near_off.as<int>(); v.near_idx = P->near_idx.as<int>();
   v.xt = P->xt.as<XTile>(); v.yt = P->yt.as<YTile>();
-  v.part = P->part.as<int4>();
   v.gthr = F ? 2u * kGuard : 0xffffffffu;
   v.stats = P->stats.as<unsigned long long>();
   v.count16 = n < 65536 ? 1 : 0;
@@ -600,7 +701,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
 extern "C" int dses_plan_destroy(dses_plan* P) {
   if (!P) return DSES_OK;
   cudaSetDevice(P->device);
-  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->part, &P->xt, &P->yt,
+  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->yt,
                     &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->cth, &P->sth, &P->rots,
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,

@@ -22,7 +22,11 @@ namespace dses {
 
 constexpr int kTile = 32;        // points per reference group (one per lane) and per source unit
 constexpr int kGuard = 2;        // guard band in fixed-point units
-constexpr int kMaxPartners = 4;  // dedup partners resolved on the fast path (more: exact path)
+// Sentinel Yq.x of empty reference slots: with |Pq| < 2^29 and W < 2^30 (or
+// W = 2^31 - 1 and Pq = 0 in exact mode) u = Yq - Pq wraps to >= 2^30 > W.
+constexpr int kNoRef = -3 * (1 << 29);
+constexpr int kMaxComp = 16;     // dedup components up to this size stay in one warp
+constexpr int kFarFlag = 1 << 12; // Yq.w: the point's dedup needs the exact path
 #ifndef DSES_VOTE_THREADS
 #define DSES_VOTE_THREADS 768
 #endif
@@ -40,6 +44,8 @@ struct XTile {          // spatial tile of the (sorted) source cloud
 struct YTile {          // spatial tile of the (sorted) reference cloud
   int start, count;
   int lo[3], hi[3];     // fixed-point bounding box of Yq over the tile
+  int gm;               // max earlier dedup partners (lanes) of a point in the group: 0, 1, 2
+  int npts;             // real reference points in the group
 };
 
 struct RotSource {      // where rotation r comes from
@@ -64,9 +70,8 @@ struct VoteParams {
   int n, m, nxt, nyt;
   const double* xs;      // (n,3) f64, X tile order
   const double* ys;      // (m,3) f64, Y tile order
-  const int4* yq;        // (m) fixed-point Yq; w = number of dedup partners j' < j (<= 4),
-                         // or kMaxPartners + 1 when there are more (exact path)
-  const int4* part;      // (m) the partners j' < j (tile order), -1 padded
+  const int4* yq;        // (m) fixed-point Yq in group order; w = lanes+1 of up to two earlier
+                         // dedup partners (bits 0-5, 6-11) or kFarFlag (exact path)
   const int* near_off;   // (m+1) CSR offsets of the full dedup near lists (tile order)
   const int* near_idx;   // near neighbours j' < j with |y_j - y_j'|_inf < bin (1+1e-6)
   const XTile* xt;       // source units of <= kTile points

@@ -60,7 +60,6 @@ __device__ __forceinline__ bool pair_bin(const VoteParams& p, const double* R, c
 }
 
 constexpr int kUnitCap = 2048;  // (reference group, source unit) work units per round
-constexpr int kRing = 64;       // per-warp ring of candidate (i, j) pairs (power of two)
 constexpr int kRare = 64;       // per-warp list of deferred (i, j) pairs
 
 // Rotated sphere (centre +- radius, a rotation preserves |x - c|) of a source
@@ -154,73 +153,84 @@ __device__ __forceinline__ void reds_add_if(uint32_t a, unsigned v, bool pred) {
                ::"r"(a), "r"(v), "r"((unsigned)pred) : "memory");
 }
 
-// Sentinel for the reference slots of a partial group: with |Pq| < 2^29 and
-// W < 2^30, u = Yq - Pq wraps to >= 2^30 > W on axis 0, so never a candidate.
-constexpr int kNoRef = -3 * (1 << 29);
 
-struct WarpQ {        // per-warp queues (warp-uniform counters)
-  uint32_t ring_sh;   // kRing (i, j) candidate pairs
-  uint32_t rare_sh;   // kRare (i, j) pairs for the exact path
-  unsigned head, tail;
+struct Lane {          // per-warp deferred list state (warp-uniform)
+  uint32_t rare_sh;
   int nrare;
   unsigned rechecks;
 };
 
-// Finish up to 32 candidate pairs (ring entries head .. head+cnt-1), one per
-// lane: fixed-point bin, guard band, per-source dedup against the pair's
-// partners j' < j (_kernels.py:153-158), shared-memory vote.  Pairs in the
-// guard band (theirs or a partner's) and pairs of reference points with more
-// than four partners go to the exact path.
+// Append the lanes in `dm` (pairs (i, j)) to the warp's exact-path list.
 template <bool HSMEM, bool PSMEM>
-__device__ __forceinline__ void drain_pass(const VoteParams& p, const double* R, const int4* P,
-                                           uint32_t P_sh, unsigned* hist, uint32_t hist_sh,
-                                           WarpQ& q, int cnt, int lane, unsigned lanemask_lt) {
-  const bool active = lane < cnt;
-  int2 ij = make_int2(0, 0);
-  if (active) ij = lds_v2(q.ring_sh + 8u * ((q.head + (unsigned)lane) & (kRing - 1)));
-  const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)ij.x) : __ldcg(&P[ij.x]);
-  const int4 Yj = __ldg(&p.yq[ij.y]);
-  const unsigned u0 = (unsigned)(Yj.x - Pi.x), u1 = (unsigned)(Yj.y - Pi.y), u2 = (unsigned)(Yj.z - Pi.z);
-  const unsigned f = __vimin3_u32(u0 & p.fmask, u1 & p.fmask, u2 & p.fmask);
-  bool near = active & (f < p.gthr);
-  bool ok = active & !near;
-  const bool partners = ok & (Yj.w != 0);
-  if (__any_sync(0xffffffffu, partners)) {
-    if (partners) {
-      if (Yj.w > 4) {
-        near = true;
-        ok = false;
-      } else {
-        const int4 pt = __ldg(&p.part[ij.y]);
-        const int pj[4] = {pt.x, pt.y, pt.z, pt.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (k < Yj.w) {
-            const int4 Y2 = __ldg(&p.yq[pj[k]]);
-            const unsigned v0 = (unsigned)(Y2.x - Pi.x), v1 = (unsigned)(Y2.y - Pi.y),
-                           v2 = (unsigned)(Y2.z - Pi.z);
-            if ((v0 < p.W0) & (v1 < p.W1) & (v2 < p.W2)) {
-              if (__vimin3_u32(v0 & p.fmask, v1 & p.fmask, v2 & p.fmask) < p.gthr) near = true;
-              else if ((((u0 ^ v0) | (u1 ^ v1) | (u2 ^ v2)) >> p.F) == 0u) ok = false;
-            }
-          }
-        }
-        ok &= !near;
-      }
-    }
+__device__ __forceinline__ void defer_pairs(const VoteParams& p, const double* R, const int4* P,
+                                            unsigned* hist, uint32_t hist_sh, Lane& L, unsigned dm,
+                                            bool mine, int i, int j, int lane, unsigned lanemask_lt) {
+  if (mine) sts_v2(L.rare_sh + 8u * (unsigned)(L.nrare + __popc(dm & lanemask_lt)), i, j);
+  L.nrare += __popc(dm);
+  if (L.nrare > kRare - 32) {
+    L.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L.rare_sh, L.nrare, lane) & 0xffffu;
+    L.nrare = 0;
   }
-  const unsigned lin = ((u0 >> p.F) * (unsigned)p.d1 + (u1 >> p.F)) * (unsigned)p.d2 + (u2 >> p.F);
+}
+
+// Fixed-point decision for one pair: candidate (inside the guard-extended
+// window), near (within the guard band of a bin edge: exact path) and bin.
+struct PairBin {
+  bool cand, near;
+  unsigned lin;
+};
+__device__ __forceinline__ PairBin fixed_bin(const VoteParams& p, const int4& Y, const int4& Pi) {
+  PairBin r;
+  const unsigned u0 = (unsigned)(Y.x - Pi.x), u1 = (unsigned)(Y.y - Pi.y), u2 = (unsigned)(Y.z - Pi.z);
+  r.cand = (u0 < p.W0) & (u1 < p.W1) & (u2 < p.W2);
+  // a candidate with every fraction >= 2G lies inside [0, D) (u in [D, W) has
+  // a fraction < 2G) and its fixed-point bin u >> F is the exact bin
+  r.near = r.cand & (__vimin3_u32(u0 & p.fmask, u1 & p.fmask, u2 & p.fmask) < p.gthr);
+  r.lin = ((u0 >> p.F) * (unsigned)p.d1 + (u1 >> p.F)) * (unsigned)p.d2 + (u2 >> p.F);
+  return r;
+}
+
+template <bool HSMEM>
+__device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsigned lin, bool ok) {
   if (HSMEM) reds_add_if(hist_sh + ((lin << 1) & ~3u), 1u + (lin & 1u) * 0xffffu, ok);
   else if (ok) atomicAdd(&hist[lin], 1u);
-  const unsigned dm = __ballot_sync(0xffffffffu, near);
-  if (dm) {
-    if (near) sts_v2(q.rare_sh + 8u * (unsigned)(q.nrare + __popc(dm & lanemask_lt)), ij.x, ij.y);
-    q.nrare += __popc(dm);
-    if (q.nrare > kRare - 32) {
-      q.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, q.rare_sh, q.nrare, lane) & 0xffffu;
-      q.nrare = 0;
+}
+
+// Source point i (broadcast) against the warp's reference group (lane = one
+// reference point j, registers).  A lane votes for its fixed-point bin when
+// the pair is decided (a candidate outside the guard band) and no earlier
+// dedup partner of j -- a lane of the same group, its key arrives by
+// shuffle -- is decided in the same bin (_kernels.py:153-158: a bin counts
+// each source once).  Pairs in the guard band, pairs whose partner is in the
+// guard band, and "far" points take the exact path.  GP = number of partner
+// shuffles the group needs (0, 1, 2).
+template <bool HSMEM, bool PSMEM, int GP>
+__device__ __forceinline__ void vote_slot(const VoteParams& p, const double* R, const int4* P,
+                                          uint32_t P_sh, unsigned* hist, uint32_t hist_sh,
+                                          Lane& L, const int4& Y, int l0, int l1, bool far, int i,
+                                          int j, int lane, unsigned lanemask_lt) {
+  const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)i) : __ldcg(&P[i]);
+  const PairBin b = fixed_bin(p, Y, Pi);
+  if (!__any_sync(0xffffffffu, b.cand)) return;
+  const bool decided = b.cand & !b.near;
+  bool ok = decided & !far, defer = b.near | (decided & far);
+  if (GP > 0) {
+    const int key = decided ? (int)b.lin : (b.near ? -2 : -1);
+    const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
+    bool dup = (l0 >= 0) & (k0 == key);
+    bool und = (l0 >= 0) & (k0 == -2);
+    if (GP > 1) {
+      const int k1 = __shfl_sync(0xffffffffu, key, l1 & 31);
+      dup |= (l1 >= 0) & (k1 == key);
+      und |= (l1 >= 0) & (k1 == -2);
     }
+    dup &= decided;
+    ok = decided & !far & !dup & !und;
+    defer = b.near | (decided & !dup & (far | und));
   }
+  vote_if<HSMEM>(hist, hist_sh, b.lin, ok);
+  const unsigned dm = __ballot_sync(0xffffffffu, defer);
+  if (dm) defer_pairs<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L, dm, defer, i, j, lane, lanemask_lt);
 }
 
 template <bool HSMEM, bool PSMEM>
@@ -244,8 +254,6 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   off += 4 * 32 * 4;
   int* units = reinterpret_cast<int*>(smem + off);  // [kUnitCap] overlapping (group, unit) pairs
   off += (size_t)kUnitCap * 4;
-  int2* ring = reinterpret_cast<int2*>(smem + off) + warp * kRing;
-  off += (size_t)nwarps * kRing * 8;
   int2* rare = reinterpret_cast<int2*>(smem + off) + warp * kRare;
 
   int* s_nunits = red + 96;
@@ -253,12 +261,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   const unsigned lanemask_lt = (1u << lane) - 1u;
   const uint32_t P_sh = PSMEM ? (uint32_t)__cvta_generic_to_shared(P) : 0u;
   const uint32_t hist_sh = HSMEM ? (uint32_t)__cvta_generic_to_shared(hist) : 0u;
-  WarpQ q;
-  q.ring_sh = (uint32_t)__cvta_generic_to_shared(ring);
-  q.rare_sh = (uint32_t)__cvta_generic_to_shared(rare);
-  q.head = q.tail = 0;
-  q.nrare = 0;
-  q.rechecks = 0;
+  Lane L;
+  L.rare_sh = (uint32_t)__cvta_generic_to_shared(rare);
+  L.nrare = 0;
+  L.rechecks = 0;
 
   uint4* hist4 = reinterpret_cast<uint4*>(hist);
   const int nw4 = p.hist_words >> 2;
@@ -300,12 +306,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     //  B1  warp w tests groups b0+w, b0+w+nwarps, ... against every source
     //      unit (one per lane); overlapping (group, unit) pairs are compacted
     //      into `units` as b << 16 | a;
-    //  B2  warps take units dynamically: lane = reference point j (registers);
-    //      each lane tests one source point of the unit against the group's
-    //      box, then every surviving source i is broadcast from shared memory
-    //      and the candidate lanes (u inside the guard-extended window)
-    //      append (i, j) to the warp's ring; full rings of 32 are drained by
-    //      drain_pass, one pair per lane.
+    //  B2  warps take units dynamically: lane = one reference point, or one
+    //      dedup component of up to four points, in registers; each lane
+    //      tests one source point of the unit against the group's box, then
+    //      every surviving source i is broadcast from shared memory and voted
+    //      in place (slot_single / slot_multi).
     for (int b0 = 0; b0 < p.nyt; b0 += tiles_per_round) {
       const int b1 = min(p.nyt, b0 + tiles_per_round);
       if (tid == 0) { *s_nunits = 0; *s_next = 0; }
@@ -335,10 +340,13 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         const YTile yt = p.yt[unit >> 16];
         const XTile& U = p.xt[unit & 0xffff];
         const int ustart = U.start, ucount = U.count;
+        const int gp = yt.gm;  // partner shuffles this group needs (warp-uniform)
         const bool valid = lane < yt.count;
         const int j = yt.start + (valid ? lane : 0);
         int4 Y = __ldg(&p.yq[j]);
-        if (!valid) Y.x = kNoRef;
+        if (!valid) Y = make_int4(kNoRef, 0, 0, 0);
+        const bool far = (Y.w & kFarFlag) != 0;
+        const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
         bool sok = false;
         if (lane < ucount) {
           const int4 Pl = PSMEM ? lds_v4(P_sh + 16u * (unsigned)(ustart + lane)) : __ldcg(&P[ustart + lane]);
@@ -348,33 +356,23 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         }
         unsigned sm = __ballot_sync(0xffffffffu, sok);
         if (lane == 0) st_pairs += (unsigned long long)__popc(sm) * (unsigned)yt.count;
-        while (sm) {
-          const int i = ustart + __ffs(sm) - 1;
-          sm &= sm - 1;
-          const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)i) : __ldcg(&P[i]);
-          const unsigned u0 = (unsigned)(Y.x - Pi.x), u1 = (unsigned)(Y.y - Pi.y),
-                         u2 = (unsigned)(Y.z - Pi.z);
-          const bool cand = valid & (u0 < p.W0) & (u1 < p.W1) & (u2 < p.W2);
-          const unsigned m = __ballot_sync(0xffffffffu, cand);
-          if (m) {
-            if (cand) sts_v2(q.ring_sh + 8u * ((q.tail + __popc(m & lanemask_lt)) & (kRing - 1)), i, j);
-            q.tail += __popc(m);
-            if (q.tail - q.head >= 32) {
-              drain_pass<HSMEM, PSMEM>(p, R, P, P_sh, hist, hist_sh, q, 32, lane, lanemask_lt);
-              q.head += 32;
-            }
-          }
-        }
+#define DSES_SLOTS(GP)                                                                         \
+  while (sm) {                                                                                 \
+    const int i = ustart + __ffs(sm) - 1;                                                      \
+    sm &= sm - 1;                                                                              \
+    vote_slot<HSMEM, PSMEM, GP>(p, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, i, j, lane,   \
+                                lanemask_lt);                                                  \
+  }
+        if (gp == 0) { DSES_SLOTS(0) }
+        else if (gp == 1) { DSES_SLOTS(1) }
+        else { DSES_SLOTS(2) }
+#undef DSES_SLOTS
       }
       __syncthreads();  // units[] is rebuilt by the next round
     }
-    if (q.tail != q.head) {
-      drain_pass<HSMEM, PSMEM>(p, R, P, P_sh, hist, hist_sh, q, (int)(q.tail - q.head), lane, lanemask_lt);
-    }
-    q.head = q.tail = 0;
-    if (q.nrare > 0) {
-      q.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, q.rare_sh, q.nrare, lane) & 0xffffu;
-      q.nrare = 0;
+    if (L.nrare > 0) {
+      L.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L.rare_sh, L.nrare, lane) & 0xffffu;
+      L.nrare = 0;
     }
     __syncthreads();
 
@@ -435,7 +433,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   }
 
   // kernel statistics
-  unsigned long long st_rechecks = q.rechecks;
+  unsigned long long st_rechecks = L.rechecks;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     st_pairs += __shfl_xor_sync(0xffffffffu, st_pairs, o);
@@ -454,7 +452,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n_pad * 16;
   b += (size_t)p.nxt * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)kUnitCap * 4;
-  b += (size_t)(threads / 32) * (kRing + kRare) * 8;
+  b += (size_t)(threads / 32) * kRare * 8;
   return b;
 }
 
