@@ -14,9 +14,14 @@ data-path collective); the timed region is bracketed by a
 barrier + synchronize, timed with CUDA events on the launching stream, and the
 max over ranks is reported.  Rank 0 prints ONE JSON line.
 
-`--impl reference` times the CPU oracle (oracle/, the C restatement of the
-reference's numba kernels, all host threads) on a bounded sample of the same
-workload, on rank 0 only.
+`--impl reference` times the reference's own CPU implementation on the box's
+host cores, on rank 0 only: the unmodified `gridreg` package (pure Python +
+numba, installed offline into baseline/_ref, every host thread) through its
+public `gridreg.dses` on the same synthetic pair, full registrations when they
+fit the time budget, else `gridreg.mode_search._mode_batch` (phase 1, 99.8% of
+the reference's time) over a contiguous rotation slice.  Without baseline/_ref
+it falls back to the oracle port (oracle/gridreg_oracle.c, the C restatement
+of the reference's numba kernels).
 """
 from __future__ import annotations
 
@@ -45,7 +50,7 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--metric", default=None, help="override the config's metric name")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=6.0,
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="wall-clock budget of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -129,8 +134,93 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_reference():
+    """The unmodified reference package from baseline/_ref (None when absent).
+    numba's thread pool gets every host thread; its JIT cache goes to /tmp."""
+    if not os.path.isdir(os.path.join(REF_DIR, "gridreg")):
+        return None
+    os.environ.setdefault("NUMBA_NUM_THREADS", str(os.cpu_count() or 1))
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/dses_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import gridreg  # noqa: F401
+        from gridreg import engines, metrics, mode_search
+    except Exception as e:  # pragma: no cover - depends on the box
+        print(f"[bench] reference package unusable ({e}); using the oracle port", file=sys.stderr)
+        return None
+    return engines, metrics, mode_search
+
+
+def ref_config(ref, cfg):
+    engines, metrics, _ = ref
+    m = cfg.metric
+    metric = metrics.ErrorMetric(m.kind, m.param)
+    return engines.SearchConfig(k_rot=cfg.k_rot, rot_step=cfg.rot_step, k_trans=cfg.k_trans,
+                                trans_bin=cfg.trans_bin, q=cfg.q, metric=metric)
+
+
+def ref_phase1_slice(ref, x, y, cfg, r0, count):
+    """gridreg.mode_search._mode_batch over rotations [r0, r0+count) of the
+    reference's own grid (geometry.build_rotation_grid)."""
+    engines, _, mode_search = ref
+    from gridreg import geometry
+    grid = geometry.build_rotation_grid(cfg.k_rot, cfg.rot_step)
+    rots = np.ascontiguousarray(grid.matrices[r0:r0 + count])
+    ilo = np.full(3, -cfg.k_trans, dtype=np.int64)
+    dims = np.full(3, 2 * cfg.k_trans + 1, dtype=np.int64)
+    t0 = time.perf_counter()
+    out = mode_search._mode_batch(rots, x, y, cfg.trans_bin, ilo, dims)
+    return time.perf_counter() - t0, out
+
+
+def reference_rate(ref, x, y, cfg, budget_s):
+    """Reference rotations/s on the step-0 pair: one full gridreg.dses when it
+    fits `budget_s` (after a JIT warm-up call on a tiny grid), else phase 1
+    over a rotation slice.  Returns (value, sample description, seconds)."""
+    engines, _, _ = ref
+    rcfg = ref_config(ref, cfg)
+    total = cfg.rotation_count
+    small = engines.SearchConfig(k_rot=1, rot_step=cfg.rot_step, k_trans=cfg.k_trans,
+                                 trans_bin=cfg.trans_bin, q=cfg.q, metric=rcfg.metric)
+    engines.dses(x, y, small)  # numba JIT / cache load, untimed
+    cal = min(total, 4 * (os.cpu_count() or 1) * 16)
+    dt_cal, _ = ref_phase1_slice(ref, x, y, cfg, 0, cal)
+    est_full = dt_cal / cal * total * 1.05
+    if est_full <= budget_s:
+        t0 = time.perf_counter()
+        res = engines.dses(x, y, rcfg)
+        dt = time.perf_counter() - t0
+        return total / dt, (f"one full gridreg.dses registration ({total} rotations, "
+                            f"phase1 {res.elapsed['phase1']:.2f} s of {dt:.2f} s)"), dt
+    sample = int(min(total, max(cal, budget_s * cal / max(dt_cal, 1e-9))))
+    dt, _ = ref_phase1_slice(ref, x, y, cfg, 0, sample)
+    return sample / dt, (f"gridreg.mode_search._mode_batch (phase 1, 99.8% of the reference's "
+                         f"time, SURVEY.md 3) over rotations [0, {sample}) of {total}, "
+                         f"{dt:.2f} s wall"), dt
+
+
 def cpu_baseline(x, y, cfg, c, budget_s, gpu_check=None):
-    """Oracle C port (all host threads) on a contiguous slice of the grid."""
+    """The reference (numba, all host threads) when baseline/_ref is present,
+    else the oracle C port, on a bounded sample of the step-0 pair."""
+    ref = load_reference()
+    if ref is not None:
+        value, sample, _ = reference_rate(ref, x, y, cfg, budget_s)
+        out = {"value": value, "unit": UNIT, "cores": int(os.environ["NUMBA_NUM_THREADS"]),
+               "kind": "reference", "sample": sample + "; registrations/s = value / "
+                                                      f"{cfg.rotation_count}",
+               "registrations_per_sec_extrapolated": value / cfg.rotation_count}
+        if gpu_check is not None:
+            n = min(cfg.rotation_count, 2048)
+            _, (rc, rl, rt) = ref_phase1_slice(ref, x, y, cfg, 0, n)
+            g_counts, g_lins, g_ties = gpu_check(n)
+            out["gpu_parity_on_sample"] = bool(np.array_equal(g_counts, rc)
+                                               and np.array_equal(g_lins, rl)
+                                               and np.array_equal(g_ties, rt))
+        return out
     from oracle import oracle as O
     nthreads = O.max_threads()
     ilo = np.full(3, -cfg.k_trans, dtype=np.int64)
@@ -170,6 +260,9 @@ def run_reference(args):
     c = workload(args.config, args.metric)
     cfg = search_config(c)
     x, y, _ = make_pair(c["spec"], 0)
+    ref = load_reference()
+    if ref is not None:
+        return run_reference_package(args, ref, c, cfg, x, y)
     from oracle import oracle as O
     nthreads = O.max_threads()
     ilo = np.full(3, -cfg.k_trans, dtype=np.int64)
@@ -205,6 +298,50 @@ def run_reference(args):
                          "sample": f"each step: phase 1 over {sample} consecutive rotations of "
                                    f"{total} (oracle/gridreg_oracle.c, the C restatement of the "
                                    f"reference numba kernels); registrations/s = value / {total}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_package(args, ref, c, cfg, x, y):
+    """--impl reference with the unmodified gridreg package (numba)."""
+    engines, _, _ = ref
+    rcfg = ref_config(ref, cfg)
+    total = cfg.rotation_count
+    nsteps = args.warmup + args.steps
+    value0, _, dt0 = reference_rate(ref, x, y, cfg, budget_s=150.0 / max(1, nsteps))
+    per_step = min(150.0 / max(1, nsteps), 60.0)
+    full = total / value0 <= per_step
+    sample = total if full else int(max(16, min(total, per_step * value0)))
+    times = []
+    for s in range(nsteps):
+        if full:
+            t0 = time.perf_counter()
+            engines.dses(x, y, rcfg)
+            dt = time.perf_counter() - t0
+        else:
+            r0 = (s * sample) % max(1, total - sample + 1)
+            dt, _ = ref_phase1_slice(ref, x, y, cfg, r0, sample)
+        if s >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = sample * len(times) / tot
+    cores = int(os.environ["NUMBA_NUM_THREADS"])
+    what = (f"each step: one full gridreg.dses registration of the pair ({total} rotations)"
+            if full else
+            f"each step: gridreg.mode_search._mode_batch (phase 1) over {sample} consecutive "
+            f"rotations of {total}; registrations/s = value / {total}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": describe(args.config, c, cfg, x.shape[0], y.shape[0]),
+                   "metric": cfg.metric.kind, "l2_flush": "n/a (CPU)"},
+        "registrations_per_sec": value / total,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": what + " (unmodified gridreg 0.1.0 from baseline/_ref, "
+                                          "numba parallel, NUMBA_NUM_THREADS=" + str(cores) + ")"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

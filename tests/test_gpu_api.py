@@ -1,0 +1,225 @@
+"""Public API on the B200 (-m gpu): the reference's worked answers, error
+behaviour, and edge cases of the vote kernel, each checked against the pinned
+oracle or the reference's known answers (restated from the reference's
+tests/test_mode_search.py:115-267 and tests/test_engines.py:248-318).
+
+Edge cases exercised here that the golden configs do not reach:
+* single-point and ragged clouds (partial warps / units);
+* duplicated and clustered reference points (dedup components of 3+ points,
+  "far" points, undecided partners -> the exact binary64 path);
+* a lattice too large for shared memory (global-memory histograms, 32-bit
+  counts: the reference's sparse path);
+* coordinates too large for the fixed-point range (exact mode);
+* non-cubic windows (mode_translation with t_bounds);
+* full-size properties: rotation-range sharding gives identical results,
+  repeated runs are bit-identical.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    import paper_2502_00115_b200 as api
+    from paper_2502_00115_b200 import _native
+    if _native.device_count() < 1:
+        pytest.fail("no CUDA device visible to the extension")
+    return api
+
+
+# ---- mode_translation: reference worked examples -------------------------
+
+def test_mode_single_pair(api):
+    res = api.mode_translation([[0.0, 0.0, 0.0]], [[1.0, 2.0, 3.0]], np.eye(3), 0.5)
+    assert res.index == (2, 4, 6) and res.count == 1
+    assert np.array_equal(res.t_star, [1.0, 2.0, 3.0])
+
+
+def test_mode_cube_corners(api):
+    c = np.array([[i, j, k] for i in (0.0, 1.0) for j in (0.0, 1.0) for k in (0.0, 1.0)])
+    res = api.mode_translation(c, c, np.eye(3), 0.1)
+    assert res.count == 8 and res.num_tied_bins == 1
+    assert np.array_equal(res.t_star, [0.0, 0.0, 0.0])
+
+
+def test_mode_lex_tiebreak(api):
+    res = api.mode_translation([[0.0, 0.0, 0.0]], [[1.0, 0.0, 0.0], [0.0, 1.0, 0.0]],
+                               np.eye(3), 0.5)
+    assert res.num_tied_bins == 2 and res.index == (0, 2, 0)
+
+
+def test_mode_rotation_applied(api):
+    rot = api.rotation_from_euler((0.0, 0.0, math.pi / 2))
+    res = api.mode_translation([[1.0, 0.0, 0.0]], [[0.0, 1.0, 0.5]], rot, 0.25)
+    assert np.allclose(res.t_star, [0.0, 0.0, 0.5], atol=1e-12)
+
+
+def test_mode_dedup_counts_source_once(api):
+    res = api.mode_translation([[0.0, 0.0, 0.0]], [[1.0, 0.0, 0.0], [1.01, 0.0, 0.0]],
+                               np.eye(3), 0.1)
+    assert res.count == 1
+
+
+def test_mode_bounds(api):
+    res = api.mode_translation([[0.0, 0.0, 0.0]], [[0.5, 0.0, 0.0]], np.eye(3), 0.25,
+                               t_bounds=[[0.5, 0.0, 0.0], [0.5, 0.0, 0.0]])
+    assert res.index == (2, 0, 0)
+    with pytest.raises(api.NoCandidateError):
+        api.mode_translation([[0.0, 0.0, 0.0]], [[0.0, 0.0, 0.0]], np.eye(3), 0.1,
+                             t_bounds=[[5.0, 5.0, 5.0], [6.0, 6.0, 6.0]])
+    with pytest.raises(api.NoCandidateError):
+        api.mode_translation([[0.0, 0.0, 0.0]], [[0.0, 0.0, 0.0]], np.eye(3), 1.0,
+                             t_bounds=[[0.2, 0.2, 0.2], [0.4, 0.4, 0.4]])
+    with pytest.raises(api.InvalidInputError):
+        api.mode_translation([[0.0, 0.0, 0.0]], [[0.0, 0.0, 0.0]], np.eye(3), 0.1,
+                             t_bounds=[[1.0, 0.0, 0.0], [0.0, 1.0, 1.0]])
+
+
+# ---- dses: reference known answers ----------------------------------------
+
+def test_dses_self_registration(api):
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, (60, 3))
+    cfg = api.SearchConfig(k_rot=2, rot_step=math.radians(5), k_trans=4, trans_bin=0.05)
+    res = api.dses(x, x, cfg)
+    assert tuple(res.best.grid_coords) == (0, 0, 0)
+    assert np.array_equal(res.best.translation, [0.0, 0.0, 0.0])
+    assert res.best_error == 0.0 and res.best_inliers == 60
+
+
+def test_dses_planted_on_grid_pose(api):
+    rng = np.random.default_rng(12)
+    x = rng.uniform(-1, 1, (80, 3))
+    step = math.radians(4)
+    k = 3
+    from paper_2502_00115_b200.geometry import grid_rotation, grid_tables
+    c, s = grid_tables(k, step)
+    n = 2 * k + 1
+    r = (4 * n + 2) * n + 5
+    R = grid_rotation(c, s, k, r)
+    t = np.array([3, -2, 1]) * 0.05
+    y = x @ R.T + t
+    res = api.dses(x, y, api.SearchConfig(k_rot=k, rot_step=step, k_trans=6, trans_bin=0.05))
+    assert tuple(res.best.grid_coords) == (4 - k, 2 - k, 5 - k)
+    assert np.allclose(res.best.translation, t, atol=1e-12)
+
+
+def test_dses_no_candidate(api):
+    x = np.zeros((3, 3))
+    y = np.full((3, 3), 10.0)
+    cfg = api.SearchConfig(k_rot=1, rot_step=0.1, k_trans=2, trans_bin=0.1)
+    with pytest.raises(api.NoCandidateError):
+        api.dses(x, y, cfg)
+
+
+def test_dses_sat_l0_shortcut_refines_nothing(api):
+    rng = np.random.default_rng(13)
+    x = rng.uniform(-1, 1, (40, 3))
+    cfg = api.SearchConfig(k_rot=1, rot_step=0.05, k_trans=3, trans_bin=0.05,
+                           metric=api.ErrorMetric.saturated_l0(0.05))
+    res = api.dses(x, x, cfg)
+    assert res.candidates_refined == 0 and res.best_inliers == 40
+
+
+# ---- edge cases against the oracle -------------------------------------------
+
+def _votes(x, y, b, ilo, dims, rots):
+    from paper_2502_00115_b200 import _native
+    with _native.Plan(x, y, b, ilo, dims) as plan:
+        return plan.mode_batch(rots), plan.info(), plan.stats()
+
+
+def _check(x, y, b, ilo, dims, rots):
+    from oracle import oracle as O
+    (c, l, t), info, stats = _votes(x, y, b, ilo, dims, rots)
+    oc, ol, ot = O.mode_batch(x, y, b, ilo, dims, rots=rots)
+    assert np.array_equal(c, oc) and np.array_equal(l, ol) and np.array_equal(t, ot)
+    return info, stats
+
+
+def _rots(n, seed, scale=1.0):
+    from oracle import oracle as O
+    rng = np.random.default_rng(seed)
+    k = 6
+    return O.rotation_grid(k, scale * math.radians(15) / k)[rng.choice((2 * k + 1) ** 3, n)]
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (1, 40), (33, 1), (31, 65), (97, 130), (257, 33)])
+def test_ragged_sizes(n, m):
+    rng = np.random.default_rng(n * 1000 + m)
+    x = rng.normal(size=(n, 3)) * 0.5
+    y = rng.normal(size=(m, 3)) * 0.5
+    _check(x, y, 0.05, np.full(3, -20), np.full(3, 41), _rots(24, n + m))
+
+
+def test_clustered_reference_exercises_exact_dedup():
+    rng = np.random.default_rng(5)
+    centres = rng.normal(size=(40, 3)) * 0.6
+    # clusters of 1-7 points within a fraction of a bin: dedup components of
+    # every size, "far" points, partners in the guard band
+    y = np.concatenate([c + rng.normal(size=(rng.integers(1, 8), 3)) * 0.01 for c in centres])
+    y = np.concatenate([y, y[:10]])  # exact duplicates too
+    x = rng.normal(size=(150, 3)) * 0.6
+    info, stats = _check(x, y, 0.05, np.full(3, -20), np.full(3, 41), _rots(64, 7))
+    assert info["near_pairs"] > 100
+
+
+def test_guard_band_points_on_bin_edges():
+    # translations exactly on bin edges (k + 1/2) * bin: every pair near an edge
+    b = 0.125
+    x = np.zeros((8, 3))
+    y = (np.arange(24).reshape(8, 3) + 0.5) * b
+    info, stats = _check(x, y, b, np.full(3, -30), np.full(3, 61), np.eye(3)[None])
+    assert stats["rechecks"] > 0
+
+
+def test_lattice_larger_than_shared_memory():
+    rng = np.random.default_rng(9)
+    x = rng.normal(size=(120, 3))
+    y = rng.normal(size=(200, 3))
+    _check(x, y, 0.02, np.full(3, -100), np.full(3, 201), _rots(6, 9))
+
+
+def test_exact_mode_for_huge_coordinates():
+    rng = np.random.default_rng(10)
+    x = rng.normal(size=(50, 3)) * 1e9
+    y = x + np.array([0.3, -0.1, 0.2])
+    (c, l, t), info, _ = _votes(x, y, 0.1, np.full(3, -8), np.full(3, 17), np.eye(3)[None])
+    assert info["frac_bits"] == 0 and c[0] == 50
+    _check(x, y, 0.1, np.full(3, -8), np.full(3, 17),
+           np.concatenate([np.eye(3)[None], _rots(4, 10, 1e-9)]))
+
+
+def test_non_cubic_window():
+    rng = np.random.default_rng(14)
+    x = rng.normal(size=(90, 3)) * 0.4
+    y = rng.normal(size=(110, 3)) * 0.4
+    _check(x, y, 0.04, np.array([-25, -5, -12]), np.array([51, 9, 30]), _rots(16, 14))
+
+
+# ---- full-size properties ----------------------------------------------------
+
+def test_sharded_slices_equal_whole_grid_and_runs_repeat():
+    from paper_2502_00115_b200 import _native
+    from paper_2502_00115_b200.engines import prepare
+    import bench
+    c = bench.workload("c3")
+    cfg = bench.search_config(c)
+    from paper_2502_00115_b200.synth import make_pair
+    x, y, _ = make_pair(c["spec"], 0)
+    prep = prepare(x, y, cfg)
+    grid = _native.make_grid(cfg.k_rot, prep.cos_tab, prep.sin_tab, None)
+    R = 200_000
+    with _native.Plan(prep.x, prep.y, cfg.trans_bin, prep.ilo, prep.dims) as plan:
+        whole = plan.mode_grid(grid, 0, R)
+        again = plan.mode_grid(grid, 0, R)
+        parts = [plan.mode_grid(grid, a, b - a) for a, b in ((0, 70_001), (70_001, 150_000),
+                                                            (150_000, R))]
+    for k in range(3):
+        assert np.array_equal(whole[k], again[k])
+        assert np.array_equal(whole[k], np.concatenate([p[k] for p in parts]))
+    assert whole[0].max() > 0
