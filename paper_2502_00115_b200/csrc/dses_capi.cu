@@ -688,7 +688,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
   P->n = n;
   P->m = m;
   P->bin = bin_size;
-  P->inv_bin = 1.0 / bin_size;  // mode_search.py:158 (inv_bin = 1.0 / bin_size)
+  P->inv_bin = 1.0 / bin_size;  // mode_search.py:157 (inv_bin = 1.0 / bin_size)
   for (int k = 0; k < 3; ++k) { P->ilo[k] = ilo[k]; P->dims[k] = dims[k]; }
   for (auto& e : P->ev) cudaEventCreate(&e);
   TrafficScope ts_(P);
