@@ -545,7 +545,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   trace("shared-memory placement");
   const size_t fixed = vote_smem_bytes(v, false, false, P->vote_threads);
   const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)v.n_pad * 16;
-  const size_t lim = P->smem_optin;
+  const size_t lim = P->smem_optin - 256;  // static shared memory of the vote kernel
   P->hsmem = v.count16 && fixed + hb <= lim;
   if (!P->hsmem) {  // global-memory histograms always use 32-bit counts
     v.count16 = 0;

@@ -173,20 +173,26 @@ __device__ __forceinline__ void defer_pairs(const VoteParams& p, const double* R
   }
 }
 
+// Fast-path constants in per-lane registers.
+struct FastK {
+  unsigned W0, W1, W2, fmask, gthr, d1, d2;
+  int F;
+};
+
 // Fixed-point decision for one pair: candidate (inside the guard-extended
 // window), near (within the guard band of a bin edge: exact path) and bin.
 struct PairBin {
   bool cand, near;
   unsigned lin;
 };
-__device__ __forceinline__ PairBin fixed_bin(const VoteParams& p, const int4& Y, const int4& Pi) {
+__device__ __forceinline__ PairBin fixed_bin(const FastK& k, const int4& Y, const int4& Pi) {
   PairBin r;
   const unsigned u0 = (unsigned)(Y.x - Pi.x), u1 = (unsigned)(Y.y - Pi.y), u2 = (unsigned)(Y.z - Pi.z);
-  r.cand = (u0 < p.W0) & (u1 < p.W1) & (u2 < p.W2);
+  r.cand = (u0 < k.W0) & (u1 < k.W1) & (u2 < k.W2);
   // a candidate with every fraction >= 2G lies inside [0, D) (u in [D, W) has
   // a fraction < 2G) and its fixed-point bin u >> F is the exact bin
-  r.near = r.cand & (__vimin3_u32(u0 & p.fmask, u1 & p.fmask, u2 & p.fmask) < p.gthr);
-  r.lin = ((u0 >> p.F) * (unsigned)p.d1 + (u1 >> p.F)) * (unsigned)p.d2 + (u2 >> p.F);
+  r.near = r.cand & (__vimin3_u32(u0 & k.fmask, u1 & k.fmask, u2 & k.fmask) < k.gthr);
+  r.lin = ((u0 >> k.F) * k.d1 + (u1 >> k.F)) * k.d2 + (u2 >> k.F);
   return r;
 }
 
@@ -204,33 +210,54 @@ __device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsign
 // each source once).  Pairs in the guard band, pairs whose partner is in the
 // guard band, and "far" points take the exact path.  GP = number of partner
 // shuffles the group needs (0, 1, 2).
-template <bool HSMEM, bool PSMEM, int GP>
-__device__ __forceinline__ void vote_slot(const VoteParams& p, const double* R, const int4* P,
-                                          uint32_t P_sh, unsigned* hist, uint32_t hist_sh,
-                                          Lane& L, const int4& Y, int l0, int l1, bool far, int i,
-                                          int j, int lane, unsigned lanemask_lt) {
-  const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)i) : __ldcg(&P[i]);
-  const PairBin b = fixed_bin(p, Y, Pi);
-  if (!__any_sync(0xffffffffu, b.cand)) return;
-  const bool decided = b.cand & !b.near;
-  bool ok = decided & !far, defer = b.near | (decided & far);
-  if (GP > 0) {
-    const int key = decided ? (int)b.lin : (b.near ? -2 : -1);
-    const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
-    bool dup = (l0 >= 0) & (k0 == key);
-    bool und = (l0 >= 0) & (k0 == -2);
-    if (GP > 1) {
-      const int k1 = __shfl_sync(0xffffffffu, key, l1 & 31);
-      dup |= (l1 >= 0) & (k1 == key);
-      und |= (l1 >= 0) & (k1 == -2);
-    }
-    dup &= decided;
-    ok = decided & !far & !dup & !und;
-    defer = b.near | (decided & !dup & (far | und));
+template <bool HSMEM, bool PSMEM, int GP, int NS>
+__device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, const double* R,
+                                          const int4* P, uint32_t P_sh, unsigned* hist,
+                                          uint32_t hist_sh, Lane& L, const int4& Y, int l0, int l1,
+                                          bool far, const int (&is)[NS], int j, int lane,
+                                          unsigned lanemask_lt) {
+  // NS source points per call: their independent work interleaves and the
+  // warp votes / loop overhead are shared.
+  PairBin b[NS];
+  bool any = false;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)is[s]) : __ldcg(&P[is[s]]);
+    b[s] = fixed_bin(fk, Y, Pi);
+    any |= b[s].cand;
   }
-  vote_if<HSMEM>(hist, hist_sh, b.lin, ok);
-  const unsigned dm = __ballot_sync(0xffffffffu, defer);
-  if (dm) defer_pairs<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L, dm, defer, i, j, lane, lanemask_lt);
+  if (!__any_sync(0xffffffffu, any)) return;
+  bool defer[NS], anydef = false;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const bool decided = b[s].cand & !b[s].near;
+    bool ok = decided & !far;
+    defer[s] = b[s].near | (decided & far);
+    if (GP > 0) {
+      const int key = decided ? (int)b[s].lin : (b[s].near ? -2 : -1);
+      const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
+      bool dup = (l0 >= 0) & (k0 == key);
+      bool und = (l0 >= 0) & (k0 == -2);
+      if (GP > 1) {
+        const int k1 = __shfl_sync(0xffffffffu, key, l1 & 31);
+        dup |= (l1 >= 0) & (k1 == key);
+        und |= (l1 >= 0) & (k1 == -2);
+      }
+      dup &= decided;
+      ok = decided & !far & !dup & !und;
+      defer[s] = b[s].near | (decided & !dup & (far | und));
+    }
+    vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok);
+    anydef |= defer[s];
+  }
+  if (__any_sync(0xffffffffu, anydef)) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const unsigned dm = __ballot_sync(0xffffffffu, defer[s]);
+      if (dm) defer_pairs<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L, dm, defer[s], is[s], j, lane,
+                                        lanemask_lt);
+    }
+  }
 }
 
 template <bool HSMEM, bool PSMEM>
@@ -260,7 +287,19 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   int* s_next = red + 97;
   const unsigned lanemask_lt = (1u << lane) - 1u;
   const uint32_t P_sh = PSMEM ? (uint32_t)__cvta_generic_to_shared(P) : 0u;
-  const uint32_t hist_sh = HSMEM ? (uint32_t)__cvta_generic_to_shared(hist) : 0u;
+  // fast-path constants through shared memory: loaded into regular registers
+  // once, instead of being re-loaded into uniform registers in the hot loop
+  __shared__ unsigned kc[9];
+  if (tid == 0) {
+    kc[0] = p.W0; kc[1] = p.W1; kc[2] = p.W2; kc[3] = p.fmask; kc[4] = p.gthr;
+    kc[5] = (unsigned)p.d1; kc[6] = (unsigned)p.d2; kc[7] = (unsigned)p.F;
+    kc[8] = HSMEM ? (uint32_t)__cvta_generic_to_shared(hist) : 0u;
+  }
+  __syncthreads();
+  FastK fk;
+  fk.W0 = kc[0]; fk.W1 = kc[1]; fk.W2 = kc[2]; fk.fmask = kc[3]; fk.gthr = kc[4];
+  fk.d1 = kc[5]; fk.d2 = kc[6]; fk.F = (int)kc[7];
+  const uint32_t hist_sh = kc[8];
   Lane L;
   L.rare_sh = (uint32_t)__cvta_generic_to_shared(rare);
   L.nrare = 0;
@@ -358,10 +397,18 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         if (lane == 0) st_pairs += (unsigned long long)__popc(sm) * (unsigned)yt.count;
 #define DSES_SLOTS(GP)                                                                         \
   while (sm) {                                                                                 \
-    const int i = ustart + __ffs(sm) - 1;                                                      \
+    const int i0 = ustart + __ffs(sm) - 1;                                                     \
     sm &= sm - 1;                                                                              \
-    vote_slot<HSMEM, PSMEM, GP>(p, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, i, j, lane,   \
-                                lanemask_lt);                                                  \
+    if (sm) {                                                                                  \
+      const int is[2] = {i0, ustart + __ffs(sm) - 1};                                          \
+      sm &= sm - 1;                                                                            \
+      vote_slot<HSMEM, PSMEM, GP, 2>(p, fk, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
+                                     j, lane, lanemask_lt);                                    \
+    } else {                                                                                   \
+      const int is[1] = {i0};                                                                  \
+      vote_slot<HSMEM, PSMEM, GP, 1>(p, fk, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
+                                     j, lane, lanemask_lt);                                    \
+    }                                                                                          \
   }
         if (gp == 0) { DSES_SLOTS(0) }
         else if (gp == 1) { DSES_SLOTS(1) }
