@@ -432,8 +432,13 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       if (HSMEM) hist4[w] = make_uint4(0, 0, 0, 0); else __stcg(&hist4[w], make_uint4(0, 0, 0, 0));
       const unsigned vv[4] = {v.x, v.y, v.z, v.w};
       if (p.count16) {
-        st_votes += (v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) +
-                    (v.z & 0xffffu) + (v.z >> 16) + (v.w & 0xffffu) + (v.w >> 16);
+        // sum of the two 16-bit halves of a word: ((v * 0x10001) mod 2^32) >> 16
+        st_votes += ((v.x * 0x10001u) >> 16) + ((v.y * 0x10001u) >> 16) +
+                    ((v.z * 0x10001u) >> 16) + ((v.w * 0x10001u) >> 16);
+        // packed 16-bit max first: most words hold no count >= the running best
+        const unsigned m2 = __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w));
+        const int hm = (int)max(m2 & 0xffffu, m2 >> 16);
+        if (hm < best) continue;
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
           const int c = (int)((vv[h >> 1] >> ((h & 1) * 16)) & 0xffffu);

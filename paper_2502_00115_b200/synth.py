@@ -126,3 +126,10 @@ CONFIGS = {
                              shape="bracket"),
                k_rot=10, rot_step_deg=0.5, k_trans=4, trans_bin=0.004, metric="trunc-l1"),
 }
+
+# local-regime variant (k_rot=7 around identity, L1 -- a flat
+# histogram where ~97% of the rotations pass the q*M* cutoff: scoring-heavy)
+CONFIGS["c2local"] = dict(spec=PairSpec(), k_rot=7, rot_step_deg=3.0, k_trans=20, trans_bin=0.025,
+                          metric="l1")
+CONFIGS["c2l2"] = dict(spec=PairSpec(), k_rot=7, rot_step_deg=3.0, k_trans=20, trans_bin=0.025,
+                       metric="l2")
