@@ -442,13 +442,14 @@ def main():
         flops = 2.0 * (3.0 * pairs_eval + 9.0 * R * n_src * args.steps)
         achieved = flops / (vote_ms * 1e-3) / 1e12
         peak = 2.0 * ffma_s / 1e12
-        traffic = None
+        traffic, ncu_info = None, None
         prof = os.path.join(ROOT, "profiles", f"ncu_vote_{args.config}.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+                ncu_info = json.load(open(prof))
+                traffic = ncu_info.get("dram_bytes_per_launch")
             except (OSError, ValueError):
-                traffic = None
+                traffic, ncu_info = None, None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -473,7 +474,14 @@ def main():
                          "peak_source": "live FFMA probe on this GPU (MEASURED_PEAKS.json has no FP32)",
                          "pairs_evaluated_per_step": pairs_eval / args.steps,
                          "nominal_pairs_per_step": R * n_src * preps[0].y.shape[0],
-                         "vote_kernel_ms_per_step": vote_ms / args.steps},
+                         "vote_kernel_ms_per_step": vote_ms / args.steps,
+                         "traffic_source": (f"profiles/ncu_vote_{args.config}.json: dram read+write "
+                                            f"bytes of one ncu --set full capture ({ncu_info['launch']})"
+                                            if ncu_info else None),
+                         "ncu_issue_active_pct": ncu_info.get("issue_active_pct") if ncu_info else None,
+                         "ncu_alu_pipe_pct": ncu_info.get("alu_pipe_pct") if ncu_info else None,
+                         "note": "integer/ALU-issue bound (no tensor-core or HBM bound applies: "
+                                 "inputs are shared-memory resident, contraction dim 3)"},
             "stages_ms_per_step": {
                 "vote": sum(r["ms_vote"] for r in results) / args.steps,
                 "select": sum(r["ms_select"] for r in results) / args.steps,

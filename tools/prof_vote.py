@@ -1,4 +1,5 @@
-"""One vote-kernel launch on a synthetic config (for ncu)."""
+"""One vote-kernel launch on a synthetic config (for ncu): the search's phase 1
+over the first `nrot` rotations of the seed-0 pair (second launch profiled)."""
 import sys
 sys.path.insert(0, '.')
 import bench
