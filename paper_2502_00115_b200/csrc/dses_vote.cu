@@ -423,57 +423,70 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     }
     __syncthreads();
 
-    // ---- mode: scan (and re-zero) the histogram
-    int best = 0, blin = INT_MAX, bties = 0;
+    // ---- mode, pass 1: block maximum M of the histogram (packed 16-bit max
+    //      per word) and the vote total
+    unsigned mx = 0;
     for (int w = tid; w < nw4; w += nthreads) {
       // global slabs are only touched by atomics (L2) and these L1-bypassing accesses
       const uint4 v = HSMEM ? hist4[w] : __ldcg(&hist4[w]);
-      if ((v.x | v.y | v.z | v.w) == 0u) continue;
-      if (HSMEM) hist4[w] = make_uint4(0, 0, 0, 0); else __stcg(&hist4[w], make_uint4(0, 0, 0, 0));
-      const unsigned vv[4] = {v.x, v.y, v.z, v.w};
       if (p.count16) {
         // sum of the two 16-bit halves of a word: ((v * 0x10001) mod 2^32) >> 16
         st_votes += ((v.x * 0x10001u) >> 16) + ((v.y * 0x10001u) >> 16) +
                     ((v.z * 0x10001u) >> 16) + ((v.w * 0x10001u) >> 16);
-        // packed 16-bit max first: most words hold no count >= the running best
-        const unsigned m2 = __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w));
-        const int hm = (int)max(m2 & 0xffffu, m2 >> 16);
-        if (hm < best) continue;
+        mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w)));
+      } else {
+        st_votes += (unsigned long long)v.x + v.y + v.z + v.w;
+        mx = max(mx, max(max(v.x, v.y), max(v.z, v.w)));
+      }
+    }
+    if (p.count16) mx = max(mx & 0xffffu, mx >> 16);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[warp] = (int)mx;
+    __syncthreads();
+    int M = 0;
+    for (int w = 0; w < nwarps; ++w) M = max(M, red[w]);
+    __syncthreads();  // red[] is reused below
+    // ---- pass 2: re-zero, and locate the smallest flat bin at M and the
+    //      number of bins at M (_kernels.py:159-170); words without M are skipped
+    int best = M, blin = INT_MAX, bties = 0;
+    const unsigned MM = (unsigned)M * 0x10001u;
+    for (int w = tid; w < nw4; w += nthreads) {
+      const uint4 v = HSMEM ? hist4[w] : __ldcg(&hist4[w]);
+      if ((v.x | v.y | v.z | v.w) == 0u) continue;
+      if (HSMEM) hist4[w] = make_uint4(0, 0, 0, 0); else __stcg(&hist4[w], make_uint4(0, 0, 0, 0));
+      if (M == 0) continue;
+      const unsigned vv[4] = {v.x, v.y, v.z, v.w};
+      if (p.count16) {
+        // a half equals M iff the packed max of (v, MM) has a half == M and
+        // v has that half; test cheaply via min(v ^ MM) over halves == 0
+        const unsigned z = __vminu2(__vminu2(v.x ^ MM, v.y ^ MM), __vminu2(v.z ^ MM, v.w ^ MM));
+        if ((z & 0xffffu) != 0u && (z >> 16) != 0u) continue;
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
           const int c = (int)((vv[h >> 1] >> ((h & 1) * 16)) & 0xffffu);
-          if (c > best) { best = c; blin = 8 * w + h; bties = 1; }
-          else if (c == best && c > 0) ++bties;
+          if (c == M) { blin = min(blin, 8 * w + h); ++bties; }
         }
       } else {
-        st_votes += (unsigned long long)v.x + v.y + v.z + v.w;
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int c = (int)vv[h];
-          if (c > best) { best = c; blin = 4 * w + h; bties = 1; }
-          else if (c == best && c > 0) ++bties;
-        }
+        for (int h = 0; h < 4; ++h)
+          if ((int)vv[h] == M) { blin = min(blin, 4 * w + h); ++bties; }
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const int ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, blin, o);
-      const int ot = __shfl_xor_sync(0xffffffffu, bties, o);
-      mode_combine(best, blin, bties, ob, ol, ot);
+      blin = min(blin, __shfl_xor_sync(0xffffffffu, blin, o));
+      bties += __shfl_xor_sync(0xffffffffu, bties, o);
     }
-    if (lane == 0) { red[warp] = best; red[32 + warp] = blin; red[64 + warp] = bties; }
+    if (lane == 0) { red[32 + warp] = blin; red[64 + warp] = bties; }
     __syncthreads();
     if (warp == 0) {
-      best = lane < nwarps ? red[lane] : 0;
       blin = lane < nwarps ? red[32 + lane] : INT_MAX;
       bties = lane < nwarps ? red[64 + lane] : 0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const int ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, blin, o);
-        const int ot = __shfl_xor_sync(0xffffffffu, bties, o);
-        mode_combine(best, blin, bties, ob, ol, ot);
+        blin = min(blin, __shfl_xor_sync(0xffffffffu, blin, o));
+        bties += __shfl_xor_sync(0xffffffffu, bties, o);
       }
       if (lane == 0) {
         p.counts[rr] = best;
