@@ -41,12 +41,27 @@ struct XTile {          // spatial tile of the (sorted) source cloud
   double c[3];          // sphere centre (metres)
 };
 
-struct YTile {          // spatial tile of the (sorted) reference cloud
-  int start, count;
-  int lo[3], hi[3];     // fixed-point bounding box of Yq over the tile
+struct __align__(16) YTile {  // spatial tile of the (sorted) reference cloud; 3 x 16 bytes
+  int lo[3];            // fixed-point bounding box of Yq over the tile
+  int start;
+  int hi[3];
+  int count;
   int gm;               // max earlier dedup partners (lanes) of a point in the group: 0, 1, 2
   int npts;             // real reference points in the group
+  int pad[2];
 };
+static_assert(sizeof(YTile) == 48, "YTile is loaded as three int4");
+
+// YTile through three 16-byte read-only loads
+__device__ __forceinline__ YTile load_ytile(const YTile* yt, int b) {
+  const int4* q = reinterpret_cast<const int4*>(yt + b);
+  const int4 a = __ldg(q), h = __ldg(q + 1), m = __ldg(q + 2);
+  YTile t;
+  t.lo[0] = a.x; t.lo[1] = a.y; t.lo[2] = a.z; t.start = a.w;
+  t.hi[0] = h.x; t.hi[1] = h.y; t.hi[2] = h.z; t.count = h.w;
+  t.gm = m.x; t.npts = m.y; t.pad[0] = t.pad[1] = 0;
+  return t;
+}
 
 struct RotSource {      // where rotation r comes from
   const double* cth;    // grid tables (device), 2k+1 values; NULL -> explicit

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       if (tid == 0) { *s_nunits = 0; *s_next = 0; }
       __syncthreads();
       for (int b = b0 + warp; b < b1; b += nwarps) {
-        const YTile yt = p.yt[b];
+        const YTile yt = load_ytile(p.yt, b);
         for (int a0 = 0; a0 < p.nxt; a0 += 32) {
           const int a = a0 + lane;
           const bool ov = a < p.nxt && (exact_mode || boxes_meet(p, yt, XB[2 * a], XB[2 * a + 1]));
@@ -376,9 +376,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= nunits) break;
         const int unit = units[u];
-        const YTile yt = p.yt[unit >> 16];
-        const XTile& U = p.xt[unit & 0xffff];
-        const int ustart = U.start, ucount = U.count;
+        const YTile yt = load_ytile(p.yt, unit >> 16);
+        const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + (unit & 0xffff)));
+        const int ustart = U.x, ucount = U.y;
         const int gp = yt.gm;  // partner shuffles this group needs (warp-uniform)
         const bool valid = lane < yt.count;
         const int j = yt.start + (valid ? lane : 0);
