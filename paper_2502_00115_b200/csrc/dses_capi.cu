@@ -543,6 +543,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.n_pad = (int)((n + 3) / 4 * 4);
   // shared-memory placement
   trace("shared-memory placement");
+  v.unit_cap = 2048;
   const size_t fixed = vote_smem_bytes(v, false, false, P->vote_threads);
   const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)v.n_pad * 16;
   const size_t lim = P->smem_optin - 256;  // static shared memory of the vote kernel
@@ -553,6 +554,12 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   }
   P->psmem = fixed + pb + (P->hsmem ? hb : 0) <= lim;
   if (!P->hsmem && !P->psmem && fixed + pb <= lim) P->psmem = true;
+  {  // spend the remaining shared memory on the (group, unit) list: fewer rounds
+    const size_t used = fixed + (P->hsmem ? hb : 0) + (P->psmem ? pb : 0);
+    const int64_t all = (int64_t)v.nxt * v.nyt;
+    const int64_t extra = used < lim ? (int64_t)((lim - used) / 4) : 0;
+    v.unit_cap = (int)std::max<int64_t>(2048, std::min<int64_t>(2048 + extra, std::max<int64_t>(all, 2048)));
+  }
   trace("occupancy");
   int per_sm = vote_max_ctas_per_sm(v, P->hsmem, P->psmem, P->vote_threads);
   if (per_sm < 1) {

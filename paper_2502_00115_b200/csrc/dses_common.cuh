@@ -83,6 +83,7 @@ struct VoteParams {
   double flo0, flo1, flo2, fd0, fd1, fd2;
   // clouds (tile-sorted)
   int n, m, nxt, nyt;
+  int unit_cap;          // capacity of the per-round (group, unit) list in shared memory
   const double* xs;      // (n,3) f64, X tile order
   const double* ys;      // (m,3) f64, Y tile order
   const int4* yq;        // (m) fixed-point Yq in group order; w = lanes+1 of up to two earlier

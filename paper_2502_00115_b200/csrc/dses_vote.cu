@@ -59,7 +59,7 @@ __device__ __forceinline__ bool pair_bin(const VoteParams& p, const double* R, c
   return exact_bin(p, p0, p1, p2, p.ys + 3 * j, lin);
 }
 
-constexpr int kUnitCap = 2048;  // (reference group, source unit) work units per round
+constexpr int kUnitCap = 2048;  // minimum (reference group, source unit) list capacity per round
 constexpr int kRare = 64;       // per-warp list of deferred (i, j) pairs
 
 // Rotated sphere (centre +- radius, a rotation preserves |x - c|) of a source
@@ -279,8 +279,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   off += 16 * 8;
   int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + counters
   off += 4 * 32 * 4;
-  int* units = reinterpret_cast<int*>(smem + off);  // [kUnitCap] overlapping (group, unit) pairs
-  off += (size_t)kUnitCap * 4;
+  int* units = reinterpret_cast<int*>(smem + off);  // [unit_cap] overlapping (group, unit) pairs
+  off += (size_t)p.unit_cap * 4;
   int2* rare = reinterpret_cast<int2*>(smem + off) + warp * kRare;
 
   int* s_nunits = red + 96;
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   unsigned long long st_pairs = 0, st_votes = 0;
   const bool exact_mode = (p.F == 0);
   // reference groups per round so that the round's units fit `units`
-  const int tiles_per_round = max(1, kUnitCap / max(1, p.nxt));
+  const int tiles_per_round = max(1, p.unit_cap / max(1, p.nxt));
 
   for (int64_t rr = blockIdx.x; rr < p.r_count; rr += gridDim.x) {
     const int64_t r = p.r_begin + rr;
@@ -516,7 +516,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
   size_t b = 0;
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n_pad * 16;
-  b += (size_t)p.nxt * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)kUnitCap * 4;
+  b += (size_t)p.nxt * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)p.unit_cap * 4;
   b += (size_t)(threads / 32) * kRare * 8;
   return b;
 }
