@@ -168,6 +168,9 @@ struct dses_plan {
   // device data
   DevBuf xs, ys, yq, near_off, near_idx, xt, yt;  // vote (tile order)
   DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
+  DevBuf gcell, gpts;                                  // scoring: uniform grid over y
+  float gorg[3] = {0, 0, 0}, gh = 1.f;
+  int gdim[3] = {1, 1, 1};
   DevBuf cth, sth, rots;                               // rotation sources
   DevBuf counts, lins, ties;                           // per-rotation outputs
   DevBuf hist_g, p_g;                                  // global fallbacks
@@ -509,6 +512,48 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   CK(upload(P->ys1, c1, st));
   CK(upload(P->ys2, c2, st));
   CK(upload(P->ysf, yf, st));
+  {  // uniform grid over y for the screen's nearest-neighbour search: cells of
+     // 4 translation bins (grown until the grid has <= 2^20 cells)
+    trace("score grid");
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t j = 0; j < m; ++j)
+      for (int k = 0; k < 3; ++k) {
+        const float v = (&yf[j].x)[k];
+        mn[k] = std::min(mn[k], v);
+        mx[k] = std::max(mx[k], v);
+      }
+    double h = 4.0 * P->bin;
+    int dim[3];
+    for (;;) {
+      int64_t cells = 1;
+      for (int k = 0; k < 3; ++k) {
+        dim[k] = (int)std::min<double>(std::floor((mx[k] - mn[k]) / h) + 1.0, 1 << 20);
+        cells *= dim[k];
+      }
+      if (cells <= (1 << 20)) break;
+      h *= 1.25;
+    }
+    const float hf = (float)h, inv = (float)(1.0 / h);
+    auto cell_of = [&](const float4& q) {
+      int c[3];
+      for (int k = 0; k < 3; ++k)
+        c[k] = std::min(dim[k] - 1, std::max(0, (int)std::floor(((&q.x)[k] - mn[k]) * inv)));
+      return (c[0] * dim[1] + c[1]) * dim[2] + c[2];
+    };
+    const int ncell = dim[0] * dim[1] * dim[2];
+    std::vector<int> cnt(ncell + 1, 0), cid(m);
+    for (int64_t j = 0; j < m; ++j) { cid[j] = cell_of(yf[j]); ++cnt[cid[j] + 1]; }
+    for (int c = 0; c < ncell; ++c) cnt[c + 1] += cnt[c];
+    std::vector<int2> range(ncell);
+    for (int c = 0; c < ncell; ++c) range[c] = make_int2(cnt[c], cnt[c + 1]);
+    std::vector<float4> gp(m);
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t j = 0; j < m; ++j) gp[fill[cid[j]]++] = yf[j];
+    CK(upload(P->gcell, range, st));
+    CK(upload(P->gpts, gp, st));
+    for (int k = 0; k < 3; ++k) { P->gorg[k] = mn[k]; P->gdim[k] = dim[k]; }
+    P->gh = hf;
+  }
   CK(P->stats.ensure(4 * sizeof(unsigned long long)));
   CK(cudaMemsetAsync(P->stats.p, 0, 4 * sizeof(unsigned long long), st));
   CK(P->scal.ensure(64));
@@ -543,7 +588,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.n_pad = (int)((n + 3) / 4 * 4);
   // shared-memory placement
   trace("shared-memory placement");
-  v.unit_cap = 2048;
+  v.unit_cap = kUnitCapMin;
   const size_t fixed = vote_smem_bytes(v, false, false, P->vote_threads);
   const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)v.n_pad * 16;
   const size_t lim = P->smem_optin - 256;  // static shared memory of the vote kernel
@@ -558,7 +603,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     const size_t used = fixed + (P->hsmem ? hb : 0) + (P->psmem ? pb : 0);
     const int64_t all = (int64_t)v.nxt * v.nyt;
     const int64_t extra = used < lim ? (int64_t)((lim - used) / 4) : 0;
-    v.unit_cap = (int)std::max<int64_t>(2048, std::min<int64_t>(2048 + extra, std::max<int64_t>(all, 2048)));
+    v.unit_cap = (int)std::max<int64_t>(kUnitCapMin, std::min<int64_t>(kUnitCapMin + extra,
+                                                                    std::max<int64_t>(all, kUnitCapMin)));
   }
   trace("occupancy");
   int per_sm = vote_max_ctas_per_sm(v, P->hsmem, P->psmem, P->vote_threads);
@@ -647,6 +693,11 @@ ScoreParams score_params(const dses_plan* P, const RotSource& rs, int code, doub
   // per-axis |d32 - d64| <= 2^-24 (|y| + |p| + |d|) <= 2^-23 (bx + by); margin x2
   s.amb = (float)(2.0 * std::ldexp(P->bx + P->by, -23));
   s.tvec = nullptr;
+  s.gcell = P->gcell.as<int2>();
+  s.gpts = P->gpts.as<float4>();
+  for (int k = 0; k < 3; ++k) { s.gorg[k] = P->gorg[k]; s.gdim[k] = P->gdim[k]; }
+  s.gh = P->gh;
+  s.ginv = 1.0f / P->gh;
   return s;
 }
 
@@ -709,7 +760,7 @@ extern "C" int dses_plan_destroy(dses_plan* P) {
   if (!P) return DSES_OK;
   cudaSetDevice(P->device);
   DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->yt,
-                    &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->cth, &P->sth, &P->rots,
+                    &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->gcell, &P->gpts, &P->cth, &P->sth, &P->rots,
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,
                     &P->err64, &P->win_err, &P->win_row, &P->win_c, &P->tmp_rows, &P->tmp_lins,

@@ -22,6 +22,7 @@ namespace dses {
 
 constexpr int kTile = 32;        // points per reference group (one per lane) and per source unit
 constexpr int kGuard = 2;        // guard band in fixed-point units
+constexpr int kUnitCapMin = 2048; // minimum (reference group, source unit) list capacity per round
 // Sentinel Yq.x of empty reference slots: with |Pq| < 2^29 and W < 2^30 (or
 // W = 2^31 - 1 and Pq = 0 in exact mode) u = Yq - Pq wraps to >= 2^30 > W.
 constexpr int kNoRef = -3 * (1 << 29);
@@ -124,6 +125,12 @@ struct ScoreParams {     // scoring kernels (dses_score.cu)
   float paramf, halff;    // fp32 metric parameter and sat_l0 half width
   float amb;              // sat_l0 fp32 ambiguity margin (absolute)
   const double* tvec;     // explicit translations (row-indexed) instead of decoding bins
+  // uniform grid over the reference cloud (screen nearest-neighbour search)
+  const int2* gcell;      // per cell: [begin, end) into gpts
+  const float4* gpts;     // reference points sorted by cell (fp32)
+  float gorg[3];          // grid origin
+  float gh, ginv;         // cell size and 1/cell size
+  int gdim[3];            // cells per axis
 };
 
 // ---------------------------------------------------------------------------

@@ -266,6 +266,101 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(ScoreParams s, c
   }
 }
 
+// ---------------------------------------------------------------------------
+// phase 3a (grid): fp32 screen with uniform-grid nearest-neighbour lookups
+// into the full reference cloud (used for truncated L1 / L2; the kernel also
+// handles L1 / L2).  Per source
+// point, shells of cells at Chebyshev radius r = 0, 1, 2, ... around the
+// point's (clamped) cell are visited until the best distance is provably
+// below every unvisited point: a point outside the shells 0..r-1 differs
+// from the query by >= (r-1) h along some axis, so the search stops once
+// best <= (r-1) h (scaled down by 1e-6 against fp32 rounding).  Truncated
+// metrics start from best = tau, so they visit only shells within tau.
+// Beyond radius kGridShells the point falls back to a full scan.
+// ---------------------------------------------------------------------------
+constexpr int kGridShells = 4;
+
+template <bool L2>
+__device__ __forceinline__ float cell_scan(const ScoreParams& s, int cell, float p0, float p1, float p2,
+                                           float best) {
+  const int2 rg = __ldg(&s.gcell[cell]);
+  for (int q = rg.x; q < rg.y; ++q) {
+    const float4 y = __ldg(&s.gpts[q]);
+    const float a = y.x - p0, b = y.y - p1, d = y.z - p2;
+    best = fminf(best, L2 ? fmaf(d, d, fmaf(b, b, a * a)) : fabsf(a) + fabsf(b) + fabsf(d));
+  }
+  return best;
+}
+
+template <bool L2>
+__device__ float grid_nn(const ScoreParams& s, float p0, float p1, float p2, float best) {
+  const float pc[3] = {p0, p1, p2};
+  int c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    c[k] = min(s.gdim[k] - 1, max(0, __float2int_rd((pc[k] - s.gorg[k]) * s.ginv)));
+  const int rmax = max(s.gdim[0], max(s.gdim[1], s.gdim[2]));
+  for (int r = 0; r <= rmax; ++r) {
+    if (r > 0) {
+      const float lb = (float)(r - 1) * s.gh * (1.0f - 1e-6f);
+      if ((L2 ? lb * lb : lb) >= best) break;
+    }
+    if (r > kGridShells) {  // far from the cloud: full scan
+      for (int q = 0; q < s.m; ++q) {
+        const float4 y = __ldg(&s.gpts[q]);
+        const float a = y.x - p0, b = y.y - p1, d = y.z - p2;
+        best = fminf(best, L2 ? fmaf(d, d, fmaf(b, b, a * a)) : fabsf(a) + fabsf(b) + fabsf(d));
+      }
+      break;
+    }
+    for (int dx = -r; dx <= r; ++dx) {
+      const int x = c[0] + dx;
+      if (x < 0 || x >= s.gdim[0]) continue;
+      for (int dy = -r; dy <= r; ++dy) {
+        const int yy = c[1] + dy;
+        if (yy < 0 || yy >= s.gdim[1]) continue;
+        const bool edge = (dx == -r) | (dx == r) | (dy == -r) | (dy == r);
+        const int step = edge ? 1 : max(1, 2 * r);
+        for (int dz = -r; dz <= r; dz += step) {
+          const int z = c[2] + dz;
+          if (z < 0 || z >= s.gdim[2]) continue;
+          best = cell_scan<L2>(s, (x * s.gdim[1] + yy) * s.gdim[2] + z, p0, p1, p2, best);
+        }
+      }
+    }
+  }
+  return best;
+}
+
+__global__ void __launch_bounds__(kScreenThreads) screen_grid_kernel(ScoreParams s, const int64_t* rows,
+                                                                     const int* lins, double* partial) {
+  __shared__ double R[9], t[3];
+  __shared__ double sred[kScreenThreads / 32];
+  const int c = blockIdx.y;
+  load_pose(s, rows[c], lins[c], R, t);
+  const int i = blockIdx.x * kScreenThreads + threadIdx.x;
+  double v = 0.0;
+  if (i < s.n) {
+    double pp[3];
+    pose_point(R, t, s.x + 3 * i, pp);
+    const float p0 = (float)pp[0], p1 = (float)pp[1], p2 = (float)pp[2];
+    if (s.code == kL1) v = grid_nn<false>(s, p0, p1, p2, FLT_MAX);
+    else if (s.code == kTruncL1) v = grid_nn<false>(s, p0, p1, p2, s.paramf);
+    else if (s.code == kL2) v = sqrtf(grid_nn<true>(s, p0, p1, p2, FLT_MAX));
+    else v = fminf(sqrtf(grid_nn<true>(s, p0, p1, p2, s.paramf * s.paramf)), s.paramf);
+  }
+  // deterministic block sum in binary64
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < kScreenThreads / 32; ++w) tot += sred[w];
+    partial[(size_t)c * gridDim.x + blockIdx.x] = tot;
+  }
+}
+
 // err32[c] = sum of the block partials in block order; atomicMin of the
 // (non-negative) binary64 bits gives the minimum.
 __global__ void screen_reduce_kernel(const double* partial, int nblk, int64_t ncand, double* err,
@@ -388,8 +483,15 @@ cudaError_t launch_screen(const ScoreParams& s, const int64_t* rows, const int* 
   const int nblk = (s.n + kScreenThreads - 1) / kScreenThreads;
   for (int64_t c0 = 0; c0 < ncand; c0 += 65535) {
     const int64_t cn = std::min<int64_t>(65535, ncand - c0);
-    screen_kernel<<<dim3(nblk, (unsigned)cn), kScreenThreads, 0, st>>>(s, rows + c0, lins + c0,
-                                                                     partial + c0 * nblk);
+    // truncated metrics: grid lookups bounded by tau; L1 / L2 (unbounded
+    // nearest neighbour, far points in poorly aligned candidates) and sat_l0
+    // keep the streamed full / windowed scan, measured faster for them
+    if (s.code != kTruncL1 && s.code != kTruncL2)
+      screen_kernel<<<dim3(nblk, (unsigned)cn), kScreenThreads, 0, st>>>(s, rows + c0, lins + c0,
+                                                                       partial + c0 * nblk);
+    else
+      screen_grid_kernel<<<dim3(nblk, (unsigned)cn), kScreenThreads, 0, st>>>(
+          s, rows + c0, lins + c0, partial + c0 * nblk);
   }
   screen_reduce_kernel<<<(int)((ncand + 255) / 256), 256, 0, st>>>(partial, nblk, ncand, err,
                                                                    minbits);

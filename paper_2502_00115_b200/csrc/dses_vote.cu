@@ -59,7 +59,6 @@ __device__ __forceinline__ bool pair_bin(const VoteParams& p, const double* R, c
   return exact_bin(p, p0, p1, p2, p.ys + 3 * j, lin);
 }
 
-constexpr int kUnitCap = 2048;  // minimum (reference group, source unit) list capacity per round
 constexpr int kRare = 64;       // per-warp list of deferred (i, j) pairs
 
 // Rotated sphere (centre +- radius, a rotation preserves |x - c|) of a source

@@ -129,7 +129,7 @@ CONFIGS = {
 
 # local-regime variant (k_rot=7 around identity, L1 -- a flat
 # histogram where ~97% of the rotations pass the q*M* cutoff: scoring-heavy)
-CONFIGS["c2local"] = dict(spec=PairSpec(), k_rot=7, rot_step_deg=3.0, k_trans=20, trans_bin=0.025,
-                          metric="l1")
-CONFIGS["c2l2"] = dict(spec=PairSpec(), k_rot=7, rot_step_deg=3.0, k_trans=20, trans_bin=0.025,
-                       metric="l2")
+CONFIGS["c2local"] = dict(spec=PairSpec(rot_range_deg=120.0), k_rot=7, rot_step_deg=3.0, k_trans=20,
+                          trans_bin=0.025, metric="l1")
+CONFIGS["c2l2"] = dict(spec=PairSpec(rot_range_deg=120.0), k_rot=7, rot_step_deg=3.0, k_trans=20,
+                       trans_bin=0.025, metric="l2")
