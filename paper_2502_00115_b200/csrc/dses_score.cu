@@ -361,6 +361,70 @@ __global__ void __launch_bounds__(kScreenThreads) screen_grid_kernel(ScoreParams
   }
 }
 
+// ---------------------------------------------------------------------------
+// phase 3a (full scan, L1 / L2): kScanCands candidates per block share every
+// reference point read from shared memory (register blocking: one broadcast
+// LDS feeds kScanCands distance evaluations).
+// ---------------------------------------------------------------------------
+constexpr int kScanCands = 4;
+
+template <bool L2>
+__global__ void __launch_bounds__(kScreenThreads) screen_scan_kernel(ScoreParams s, const int64_t* rows,
+                                                                     const int* lins, int64_t ncand,
+                                                                     double* partial) {
+  __shared__ double R[kScanCands][9], t[kScanCands][3];
+  __shared__ float4 ych[kScreenChunk];
+  __shared__ double sred[kScanCands][kScreenThreads / 32];
+  const int64_t c0 = (int64_t)blockIdx.y * kScanCands;
+  for (int q = 0; q < kScanCands; ++q) {
+    const int64_t c = min(c0 + q, ncand - 1);
+    if (threadIdx.x < 9) R[q][threadIdx.x] = rotation_entry(s.rot, rows[c], threadIdx.x);
+    if (threadIdx.x == 0) {
+      if (s.tvec) { t[q][0] = s.tvec[3 * rows[c]]; t[q][1] = s.tvec[3 * rows[c] + 1]; t[q][2] = s.tvec[3 * rows[c] + 2]; }
+      else decode_translation(s, lins[c], t[q]);
+    }
+  }
+  __syncthreads();
+  const int i = blockIdx.x * kScreenThreads + threadIdx.x;
+  const bool active = i < s.n;
+  float px[kScanCands], py[kScanCands], pz[kScanCands], best[kScanCands];
+#pragma unroll
+  for (int q = 0; q < kScanCands; ++q) {
+    double pp[3] = {0.0, 0.0, 0.0};
+    if (active) pose_point(R[q], t[q], s.x + 3 * i, pp);
+    px[q] = (float)pp[0]; py[q] = (float)pp[1]; pz[q] = (float)pp[2];
+    best[q] = FLT_MAX;
+  }
+  for (int base = 0; base < s.m; base += kScreenChunk) {
+    const int cnt = min(kScreenChunk, s.m - base);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cnt; k += kScreenThreads) ych[k] = s.ysf[base + k];
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < cnt; ++k) {
+      const float4 y = ych[k];
+#pragma unroll
+      for (int q = 0; q < kScanCands; ++q) {
+        const float a = y.x - px[q], b = y.y - py[q], d = y.z - pz[q];
+        best[q] = fminf(best[q], L2 ? fmaf(d, d, fmaf(b, b, a * a)) : fabsf(a) + fabsf(b) + fabsf(d));
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kScanCands; ++q) {
+    double v = active ? (L2 ? sqrtf(best[q]) : best[q]) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sred[q][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kScanCands && c0 + threadIdx.x < ncand) {
+    double tot = 0.0;
+    for (int w = 0; w < kScreenThreads / 32; ++w) tot += sred[threadIdx.x][w];
+    partial[(size_t)(c0 + threadIdx.x) * gridDim.x + blockIdx.x] = tot;
+  }
+}
+
 // err32[c] = sum of the block partials in block order; atomicMin of the
 // (non-negative) binary64 bits gives the minimum.
 __global__ void screen_reduce_kernel(const double* partial, int nblk, int64_t ncand, double* err,
@@ -481,6 +545,22 @@ cudaError_t launch_screen(const ScoreParams& s, const int64_t* rows, const int* 
                           unsigned long long* minbits, cudaStream_t st) {
   if (ncand <= 0) return cudaSuccess;
   const int nblk = (s.n + kScreenThreads - 1) / kScreenThreads;
+  if (s.code == kL1 || s.code == kL2) {
+    const int64_t ng = (ncand + kScanCands - 1) / kScanCands;
+    for (int64_t g0 = 0; g0 < ng; g0 += 65535) {
+      const int64_t gn = std::min<int64_t>(65535, ng - g0);
+      const int64_t c0 = g0 * kScanCands;
+      if (s.code == kL1)
+        screen_scan_kernel<false><<<dim3(nblk, (unsigned)gn), kScreenThreads, 0, st>>>(
+            s, rows + c0, lins + c0, ncand - c0, partial + c0 * nblk);
+      else
+        screen_scan_kernel<true><<<dim3(nblk, (unsigned)gn), kScreenThreads, 0, st>>>(
+            s, rows + c0, lins + c0, ncand - c0, partial + c0 * nblk);
+    }
+    screen_reduce_kernel<<<(int)((ncand + 255) / 256), 256, 0, st>>>(partial, nblk, ncand, err,
+                                                                     minbits);
+    return cudaGetLastError();
+  }
   for (int64_t c0 = 0; c0 < ncand; c0 += 65535) {
     const int64_t cn = std::min<int64_t>(65535, ncand - c0);
     // truncated metrics: grid lookups bounded by tau; L1 / L2 (unbounded

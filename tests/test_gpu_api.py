@@ -223,3 +223,24 @@ def test_sharded_slices_equal_whole_grid_and_runs_repeat():
         assert np.array_equal(whole[k], again[k])
         assert np.array_equal(whole[k], np.concatenate([p[k] for p in parts]))
     assert whole[0].max() > 0
+
+
+@pytest.mark.parametrize("kind,param", [("trunc_l2", 0.1), ("l2", None), ("l1", None),
+                                        ("trunc_l1", 0.06)])
+def test_dses_every_metric_matches_oracle(api, kind, param):
+    """Each scoring path (grid screen for truncated metrics, streamed screen
+    for L1/L2; exact binary64 re-score) against the oracle dses, including the
+    trunc_l2 extension (parity pinned to the oracle only)."""
+    from oracle import oracle as O
+    from paper_2502_00115_b200.synth import CONFIGS, make_pair
+    x, y, _ = make_pair(CONFIGS["c2"]["spec"], 21)
+    cfg = api.SearchConfig(k_rot=3, rot_step=math.radians(6), k_trans=20, trans_bin=0.025,
+                           metric=api.ErrorMetric(kind, param))
+    res = api.dses(x, y, cfg)
+    ref = O.dses(x, y, k_rot=cfg.k_rot, rot_step=cfg.rot_step, k_trans=cfg.k_trans,
+                 trans_bin=cfg.trans_bin, q=cfg.q, metric=(kind, param))
+    assert tuple(res.best.grid_coords) == tuple(ref["grid_coords"])
+    assert np.array_equal(res.best.translation, ref["translation"])
+    assert math.isclose(res.best_error, ref["best_error"], rel_tol=1e-9)
+    assert res.candidates_refined == ref["candidates_refined"]
+    assert res.best_inliers == ref["best_inliers"]
