@@ -31,6 +31,10 @@
 #include <cstdio>
 #include "dses_common.cuh"
 
+#ifndef DSES_NS4
+#define DSES_NS4 0  // four source points per slot (measured slower at 768 threads)
+#endif
+
 namespace dses {
 
 // Fast fixed-point bin of pair (Yq, Pq); returns 0 = out of window, 1 = in
@@ -398,7 +402,13 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   while (sm) {                                                                                 \
     const int i0 = ustart + __ffs(sm) - 1;                                                     \
     sm &= sm - 1;                                                                              \
-    if (sm) {                                                                                  \
+    if (DSES_NS4 && __popc(sm) >= 3) {                                                         \
+      int is[4];                                                                               \
+      is[0] = i0;                                                                              \
+      for (int q = 1; q < 4; ++q) { is[q] = ustart + __ffs(sm) - 1; sm &= sm - 1; }            \
+      vote_slot<HSMEM, PSMEM, GP, 4>(p, fk, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
+                                     j, lane, lanemask_lt);                                    \
+    } else if (sm) {                                                                           \
       const int is[2] = {i0, ustart + __ffs(sm) - 1};                                          \
       sm &= sm - 1;                                                                            \
       vote_slot<HSMEM, PSMEM, GP, 2>(p, fk, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
