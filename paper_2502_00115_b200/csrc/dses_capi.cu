@@ -110,18 +110,23 @@ static void keep_pool(int device) {
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  bool borrowed = false;  // points into another buffer (an upload arena): never freed here
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap && p) return cudaSuccess;
-    if (p) cudaFreeAsync(p, 0);
-    p = nullptr;
-    cap = 0;
+    release();
     size_t want = std::max<size_t>(bytes + bytes / 2, 256);
     cudaError_t e = cudaMallocAsync(&p, want, 0);
     if (e == cudaSuccess) cap = want;
     return e;
   }
+  void borrow(void* q, size_t bytes) { release(); p = q; cap = bytes; borrowed = true; }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
-  void release() { if (p) cudaFreeAsync(p, 0); p = nullptr; cap = 0; }
+  void release() {
+    if (p && !borrowed) cudaFreeAsync(p, 0);
+    p = nullptr;
+    cap = 0;
+    borrowed = false;
+  }
 };
 
 // host<->device traffic is counted per plan (bench.py reports it as e2e bytes)
@@ -143,12 +148,45 @@ static inline cudaError_t launched(cudaError_t e, int n = 1) {
   return e;
 }
 
-template <class T>
-static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
-  cudaError_t e = b.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
-  if (e != cudaSuccess || v.empty()) return e;
-  return h2d(b.p, v.data(), sizeof(T) * v.size(), st);
-}
+
+// All of a plan's read-only inputs go to the device in ONE copy: packed into
+// a per-thread pinned staging buffer, copied into one arena, and the plan's
+// buffers borrow sub-ranges of the arena (16 pageable copies cost ~0.2 ms).
+struct UploadPack {
+  struct Item { DevBuf* buf; const void* src; size_t off, bytes; };
+  std::vector<Item> items;
+  size_t total = 0;
+  template <class T> void add(DevBuf& b, const std::vector<T>& v) {
+    const size_t bytes = sizeof(T) * std::max<size_t>(v.size(), 1);
+    const size_t off = (total + 255) & ~size_t(255);
+    items.push_back({&b, v.empty() ? nullptr : v.data(), off, sizeof(T) * v.size()});
+    (void)bytes;
+    total = off + bytes;
+  }
+  // the caller synchronises `st` before the staging buffer is reused
+  cudaError_t commit(DevBuf& arena, cudaStream_t st) {
+    static thread_local void* staging = nullptr;
+    static thread_local size_t staging_cap = 0;
+    if (total > staging_cap) {
+      if (staging) cudaFreeHost(staging);
+      staging = nullptr;
+      staging_cap = 0;
+      const size_t want = std::max<size_t>(total + total / 2, 1 << 16);
+      cudaError_t e = cudaHostAlloc(&staging, want, cudaHostAllocDefault);
+      if (e != cudaSuccess) return e;
+      staging_cap = want;
+    }
+    for (const Item& it : items)
+      if (it.bytes) std::memcpy(static_cast<unsigned char*>(staging) + it.off, it.src, it.bytes);
+    cudaError_t e = arena.ensure(total);
+    if (e != cudaSuccess) return e;
+    e = h2d(arena.p, staging, total, st);
+    if (e != cudaSuccess) return e;
+    for (const Item& it : items)
+      it.buf->borrow(static_cast<unsigned char*>(arena.p) + it.off, it.bytes);
+    return cudaSuccess;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // the plan
@@ -169,6 +207,7 @@ struct dses_plan {
   DevBuf xs, ys, yq, near_off, near_idx, xt, yt;  // vote (tile order)
   DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
   DevBuf gcell, gpts;                                  // scoring: uniform grid over y
+  DevBuf arena;                                        // the inputs above live here (UploadPack)
   float gorg[3] = {0, 0, 0}, gh = 1.f;
   int gdim[3] = {1, 1, 1};
   DevBuf cth, sth, rots;                               // rotation sources
@@ -366,45 +405,53 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   trace("dedup components");
   const double thr = P->bin * (1.0 + 1e-6);
   const std::vector<std::pair<int, int>> near = near_pairs(y, m, thr);
-  std::vector<std::vector<int>> adj(m);
-  for (const auto& e : near) {
-    adj[e.first].push_back(e.second);
-    adj[e.second].push_back(e.first);
+  // adjacency in CSR form
+  std::vector<int> aoff(m + 1, 0), aidx(2 * near.size());
+  for (const auto& e : near) { ++aoff[e.first + 1]; ++aoff[e.second + 1]; }
+  for (int64_t j = 0; j < m; ++j) aoff[j + 1] += aoff[j];
+  {
+    std::vector<int> fill(aoff.begin(), aoff.end() - 1);
+    for (const auto& e : near) { aidx[fill[e.first]++] = e.second; aidx[fill[e.second]++] = e.first; }
   }
-  std::vector<std::vector<int>> items;  // components (or single points of big ones)
+  // components (flat): item q = points ipts[ioff[q] .. ioff[q+1]), sorted
+  std::vector<int> ioff(1, 0), ipts;
   std::vector<char> item_far;
+  ipts.reserve(m);
   {
     std::vector<char> seen(m, 0);
+    std::vector<int> c;
     for (int64_t s0 = 0; s0 < m; ++s0) {
       if (seen[s0]) continue;
-      std::vector<int> c(1, (int)s0);
+      c.assign(1, (int)s0);
       seen[s0] = 1;
       for (size_t h = 0; h < c.size(); ++h)
-        for (int v : adj[c[h]])
-          if (!seen[v]) { seen[v] = 1; c.push_back(v); }
-      std::sort(c.begin(), c.end());
+        for (int a = aoff[c[h]]; a < aoff[c[h] + 1]; ++a)
+          if (!seen[aidx[a]]) { seen[aidx[a]] = 1; c.push_back(aidx[a]); }
+      if (c.size() > 1) std::sort(c.begin(), c.end());
       if ((int)c.size() <= kMaxComp) {
-        items.push_back(std::move(c));
+        ipts.insert(ipts.end(), c.begin(), c.end());
+        ioff.push_back((int)ipts.size());
         item_far.push_back(0);
       } else {
-        for (int v : c) { items.push_back(std::vector<int>(1, v)); item_far.push_back(1); }
+        for (int v : c) { ipts.push_back(v); ioff.push_back((int)ipts.size()); item_far.push_back(1); }
       }
     }
   }
-  std::vector<double> cen(3 * items.size());
-  std::vector<int> wt(items.size());
-  for (size_t q = 0; q < items.size(); ++q) {
-    wt[q] = (int)items[q].size();
+  const size_t nitems = item_far.size();
+  std::vector<double> cen(3 * nitems);
+  std::vector<int> wt(nitems);
+  for (size_t q = 0; q < nitems; ++q) {
+    wt[q] = ioff[q + 1] - ioff[q];
     for (int k = 0; k < 3; ++k) {
       double acc = 0;
-      for (int v : items[q]) acc += y[3 * v + k];
-      cen[3 * q + k] = acc / (double)items[q].size();
+      for (int a = ioff[q]; a < ioff[q + 1]; ++a) acc += y[3 * ipts[a] + k];
+      cen[3 * q + k] = acc / (double)wt[q];
     }
   }
-  std::vector<int> iperm(items.size());
+  std::vector<int> iperm(nitems);
   std::iota(iperm.begin(), iperm.end(), 0);
   std::vector<std::pair<int, int>> itiles;
-  kd_weighted(cen.data(), wt, 0, (int64_t)items.size(), iperm, itiles, kTile);
+  kd_weighted(cen.data(), wt, 0, (int64_t)nitems, iperm, itiles, kTile);
   std::vector<int> yidx;  // tile-order entry -> original reference index
   std::vector<char> yfar;
   struct GroupSpan { int start, count, gm; };
@@ -412,8 +459,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   for (const auto& t : itiles) {
     const int start = (int)yidx.size();
     for (int q = t.first; q < t.first + t.second; ++q)
-      for (int v : items[iperm[q]]) {
-        yidx.push_back(v);
+      for (int a = ioff[iperm[q]]; a < ioff[iperm[q] + 1]; ++a) {
+        yidx.push_back(ipts[a]);
         yfar.push_back(item_far[iperm[q]]);
       }
     groups.push_back({start, (int)yidx.size() - start, 1});
@@ -454,8 +501,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       // earlier partners (tile order) of point q: lanes of the same group
       int w = 0, ne = 0;
       bool far = yfar[q];
-      for (int v2 : adj[yidx[q]]) {
-        const int q2 = pos[v2];
+      for (int a = aoff[yidx[q]]; a < aoff[yidx[q] + 1]; ++a) {
+        const int q2 = pos[aidx[a]];
         if (q2 >= q) continue;
         if (q2 < T.start || ne == 2) { far = true; continue; }
         w |= (q2 - T.start + 1) << (6 * ne);
@@ -469,20 +516,20 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     return fail(DSES_E_INVALID, "cloud too large for the 16-bit work-unit encoding");
   // ---- full dedup near lists (tile order, j' < j) for the exact path
   trace("dedup near lists");
-  std::vector<std::vector<int>> nl(mp);
-  for (const auto& e : near) {
-    const int a = pos[e.first], b = pos[e.second];
-    if (a < b) nl[b].push_back(a); else nl[a].push_back(b);
-  }
+  // CSR near lists in tile order: j' < j, sorted (the exact path's partners)
   const int64_t npairs = (int64_t)near.size();
-  std::vector<int> noff(mp + 1, 0), nidx;
-  nidx.reserve((size_t)npairs);
-  for (int64_t q = 0; q < mp; ++q) {
-    std::sort(nl[q].begin(), nl[q].end());
-    noff[q] = (int)nidx.size();
-    nidx.insert(nidx.end(), nl[q].begin(), nl[q].end());
+  std::vector<int> noff(mp + 1, 0), nidx((size_t)npairs);
+  for (const auto& e : near) ++noff[std::max(pos[e.first], pos[e.second]) + 1];
+  for (int64_t q = 0; q < mp; ++q) noff[q + 1] += noff[q];
+  {
+    std::vector<int> fill(noff.begin(), noff.end() - 1);
+    for (const auto& e : near) {
+      const int a = pos[e.first], b = pos[e.second];
+      nidx[fill[std::max(a, b)]++] = std::min(a, b);
+    }
+    for (int64_t q = 0; q < mp; ++q)
+      if (noff[q + 1] - noff[q] > 1) std::sort(nidx.begin() + noff[q], nidx.begin() + noff[q + 1]);
   }
-  noff[mp] = (int)nidx.size();
   P->near_pairs = npairs;
   // ---- scoring layout: x original order, y sorted by axis 0 (stable)
   trace("scoring layout");
@@ -499,19 +546,22 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   }
   std::vector<double> xv(x, x + 3 * n);
   // ---- uploads
-  CK(upload(P->xs, xs, st));
-  CK(upload(P->ys, ys, st));
-  CK(upload(P->yq, yq, st));
-  CK(upload(P->near_off, noff, st));
+  UploadPack pack;
+  std::vector<int2> range;  // score grid (filled below)
+  std::vector<float4> gp;
+  pack.add(P->xs, xs);
+  pack.add(P->ys, ys);
+  pack.add(P->yq, yq);
+  pack.add(P->near_off, noff);
   if (nidx.empty()) nidx.push_back(0);
-  CK(upload(P->near_idx, nidx, st));
-  CK(upload(P->xt, xt, st));
-  CK(upload(P->yt, yt, st));
-  CK(upload(P->x0, xv, st));
-  CK(upload(P->ys0, c0, st));
-  CK(upload(P->ys1, c1, st));
-  CK(upload(P->ys2, c2, st));
-  CK(upload(P->ysf, yf, st));
+  pack.add(P->near_idx, nidx);
+  pack.add(P->xt, xt);
+  pack.add(P->yt, yt);
+  pack.add(P->x0, xv);
+  pack.add(P->ys0, c0);
+  pack.add(P->ys1, c1);
+  pack.add(P->ys2, c2);
+  pack.add(P->ysf, yf);
   {  // uniform grid over y for the screen's nearest-neighbour search: cells of
      // 4 translation bins (grown until the grid has <= 2^20 cells)
     trace("score grid");
@@ -544,16 +594,17 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     std::vector<int> cnt(ncell + 1, 0), cid(m);
     for (int64_t j = 0; j < m; ++j) { cid[j] = cell_of(yf[j]); ++cnt[cid[j] + 1]; }
     for (int c = 0; c < ncell; ++c) cnt[c + 1] += cnt[c];
-    std::vector<int2> range(ncell);
+    range.resize(ncell);
     for (int c = 0; c < ncell; ++c) range[c] = make_int2(cnt[c], cnt[c + 1]);
-    std::vector<float4> gp(m);
+    gp.resize(m);
     std::vector<int> fill(cnt.begin(), cnt.end() - 1);
     for (int64_t j = 0; j < m; ++j) gp[fill[cid[j]]++] = yf[j];
-    CK(upload(P->gcell, range, st));
-    CK(upload(P->gpts, gp, st));
+    pack.add(P->gcell, range);
+    pack.add(P->gpts, gp);
     for (int k = 0; k < 3; ++k) { P->gorg[k] = mn[k]; P->gdim[k] = dim[k]; }
     P->gh = hf;
   }
+  CK(pack.commit(P->arena, st));
   CK(P->stats.ensure(4 * sizeof(unsigned long long)));
   CK(cudaMemsetAsync(P->stats.p, 0, 4 * sizeof(unsigned long long), st));
   CK(P->scal.ensure(64));
@@ -760,7 +811,7 @@ extern "C" int dses_plan_destroy(dses_plan* P) {
   if (!P) return DSES_OK;
   cudaSetDevice(P->device);
   DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->yt,
-                    &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->gcell, &P->gpts, &P->cth, &P->sth, &P->rots,
+                    &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->gcell, &P->gpts, &P->arena, &P->cth, &P->sth, &P->rots,
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,
                     &P->err64, &P->win_err, &P->win_row, &P->win_c, &P->tmp_rows, &P->tmp_lins,
