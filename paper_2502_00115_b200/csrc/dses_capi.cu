@@ -30,6 +30,11 @@ cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, i
                         cudaStream_t stream);
 int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int threads);
 size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads);
+// dses_sparse.cu
+size_t sparse_scratch_bytes(int64_t n, int64_t m);
+cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t r_count,
+                                void* scratch, size_t scratch_bytes, unsigned long long* counters,
+                                int* counts, long long* lins, int* ties, int sms, cudaStream_t st);
 // dses_score.cu
 cudaError_t launch_select_stats(const int* counts, int64_t nrot, unsigned long long* mstar,
                                 unsigned long long* nvalid, int sms, cudaStream_t st);
@@ -208,6 +213,9 @@ struct dses_plan {
   DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
   DevBuf gcell, gpts;                                  // scoring: uniform grid over y
   DevBuf arena;                                        // the inputs above live here (UploadPack)
+  DevBuf yorig;                                        // (m, 3) reference, original order (sparse path)
+  bool sparse = false;                                 // lattice beyond kDenseMaxBins: sort-based mode
+  DevBuf lins64, sparse_scratch;
   float gorg[3] = {0, 0, 0}, gh = 1.f;
   int gdim[3] = {1, 1, 1};
   DevBuf cth, sth, rots;                               // rotation sources
@@ -547,6 +555,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   std::vector<double> xv(x, x + 3 * n);
   // ---- uploads
   UploadPack pack;
+  const std::vector<double> yv(y, y + 3 * m);
+  pack.add(P->yorig, yv);
   std::vector<int2> range;  // score grid (filled below)
   std::vector<float4> gp;
   pack.add(P->xs, xs);
@@ -614,6 +624,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   trace("vote kernel parameters");
   VoteParams& v = P->vp;
   v.d0 = (int)P->dims[0]; v.d1 = (int)P->dims[1]; v.d2 = (int)P->dims[2];
+  if (P->sparse) return DSES_OK;  // mode queries use the sort-based path only
   v.nbins = v.d0 * v.d1 * v.d2;
   v.F = F;
   v.fmask = F ? (unsigned)(Si - 1) : 0u;
@@ -687,7 +698,37 @@ int set_grid(dses_plan* P, const dses_grid* g, RotSource* rs, cudaStream_t st) {
   return DSES_OK;
 }
 
+int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
+  CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  CK(P->lins64.ensure(sizeof(long long) * std::max<int64_t>(r_count, 1)));
+  CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  P->cur_r_begin = r_begin;
+  P->cur_r_count = r_count;
+  P->cur_rot = rs;
+  if (r_count <= 0) return DSES_OK;
+  SparseParams sp{};
+  sp.n = (int)P->n;
+  sp.m = (int)P->m;
+  sp.x = P->x0.as<double>();
+  sp.y = P->yorig.as<double>();
+  sp.inv_bin = P->inv_bin;
+  sp.flo0 = (double)P->ilo[0]; sp.flo1 = (double)P->ilo[1]; sp.flo2 = (double)P->ilo[2];
+  sp.fd0 = (double)P->dims[0]; sp.fd1 = (double)P->dims[1]; sp.fd2 = (double)P->dims[2];
+  sp.d1 = P->dims[1];
+  sp.d2 = P->dims[2];
+  sp.rot = rs;
+  const size_t sb = sparse_scratch_bytes(P->n, P->m);
+  CK(P->sparse_scratch.ensure(sb));
+  CK(P->scal.ensure(64));
+  CK(launched(launch_sparse_modes(sp, r_begin, r_count, P->sparse_scratch.p, P->sparse_scratch.cap,
+                                  P->scal.as<unsigned long long>() + 6, P->counts.as<int>(),
+                                  P->lins64.as<long long>(), P->ties.as<int>(), P->sms, st),
+              (int)(5 * r_count)));
+  return DSES_OK;
+}
+
 int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
+  if (P->sparse) return run_sparse(P, rs, r_begin, r_count, st);
   CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
   CK(P->lins.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
   CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
@@ -775,7 +816,8 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
   for (int k = 0; k < 3; ++k)
     if (dims[k] < 1) return fail(DSES_E_INVALID, "dims must be positive");
   const double nbins = (double)dims[0] * (double)dims[1] * (double)dims[2];
-  if (nbins > 2147483647.0) return fail(DSES_E_INVALID, "translation lattice too large");
+  if (nbins * (double)n >= 4.611686018427388e18)  // the reference's key-space guard (mode_search.py:149-152)
+    return fail(DSES_E_INVALID, "translation lattice too large");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(DSES_E_NODEVICE, "no CUDA device");
@@ -799,6 +841,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
   P->bin = bin_size;
   P->inv_bin = 1.0 / bin_size;  // mode_search.py:157 (inv_bin = 1.0 / bin_size)
   for (int k = 0; k < 3; ++k) { P->ilo[k] = ilo[k]; P->dims[k] = dims[k]; }
+  P->sparse = nbins > (double)kDenseMaxBins;
   for (auto& e : P->ev) cudaEventCreate(&e);
   TrafficScope ts_(P);
   const int rc = build_plan(P, x, y);
@@ -811,7 +854,7 @@ extern "C" int dses_plan_destroy(dses_plan* P) {
   if (!P) return DSES_OK;
   cudaSetDevice(P->device);
   DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->yt,
-                    &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->gcell, &P->gpts, &P->arena, &P->cth, &P->sth, &P->rots,
+                    &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->gcell, &P->gpts, &P->arena, &P->yorig, &P->lins64, &P->sparse_scratch, &P->cth, &P->sth, &P->rots,
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,
                     &P->err64, &P->win_err, &P->win_row, &P->win_c, &P->tmp_rows, &P->tmp_lins,
@@ -835,15 +878,17 @@ extern "C" int dses_plan_info(const dses_plan* P, int64_t* frac_bits, int64_t* x
 static int fetch_modes(dses_plan* P, int64_t nrot, int64_t* counts, int64_t* lins, int64_t* ties,
                        cudaStream_t st) {
   std::vector<int> c(nrot), l(nrot), t(nrot);
+  std::vector<long long> l64(P->sparse ? nrot : 0);
   if (nrot > 0) {
     CK(d2h(c.data(), P->counts.p, 4 * nrot, st));
-    CK(d2h(l.data(), P->lins.p, 4 * nrot, st));
+    if (P->sparse) CK(d2h(l64.data(), P->lins64.p, 8 * nrot, st));
+    else CK(d2h(l.data(), P->lins.p, 4 * nrot, st));
     CK(d2h(t.data(), P->ties.p, 4 * nrot, st));
   }
   CK(cudaStreamSynchronize(st));
   for (int64_t r = 0; r < nrot; ++r) {
     if (counts) counts[r] = c[r];
-    if (lins) lins[r] = l[r];
+    if (lins) lins[r] = P->sparse ? (int64_t)l64[r] : (int64_t)l[r];
     if (ties) ties[r] = t[r];
   }
   return DSES_OK;
@@ -930,6 +975,10 @@ extern "C" int dses_stage_vote(dses_plan* P, const dses_grid* g, int64_t r_begin
                                int64_t* mstar_local, int64_t* valid_local, void* stream) {
   TrafficScope ts_(P);
   if (!P || !g) return fail(DSES_E_INVALID, "bad arguments");
+  if (P->sparse)
+    return fail(DSES_E_INVALID, "translation window of %.3g bins is beyond the search's dense "
+                "limit (%d bins); mode queries (dses_mode_*) support it",
+                (double)P->dims[0] * P->dims[1] * P->dims[2], kDenseMaxBins);
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t total = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);

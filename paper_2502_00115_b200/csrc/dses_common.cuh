@@ -22,7 +22,8 @@ namespace dses {
 
 constexpr int kTile = 32;        // points per reference group (one per lane) and per source unit
 constexpr int kGuard = 2;        // guard band in fixed-point units
-constexpr int kUnitCapMin = 2048; // minimum (reference group, source unit) list capacity per round
+constexpr int kUnitCapMin = 2048;
+constexpr int kDenseMaxBins = 1 << 26;  // beyond: sort-based (sparse) mode queries // minimum (reference group, source unit) list capacity per round
 // Sentinel Yq.x of empty reference slots: with |Pq| < 2^29 and W < 2^30 (or
 // W = 2^31 - 1 and Pq = 0 in exact mode) u = Yq - Pq wraps to >= 2^30 > W.
 constexpr int kNoRef = -3 * (1 << 29);
@@ -131,6 +132,16 @@ struct ScoreParams {     // scoring kernels (dses_score.cu)
   float gorg[3];          // grid origin
   float gh, ginv;         // cell size and 1/cell size
   int gdim[3];            // cells per axis
+};
+
+struct SparseParams {    // sort-based mode queries (dses_sparse.cu)
+  int n, m;
+  const double* x;        // (n, 3) source (any order: keys carry i)
+  const double* y;        // (m, 3) reference
+  double inv_bin;
+  double flo0, flo1, flo2, fd0, fd1, fd2;
+  int64_t d1, d2;
+  RotSource rot;
 };
 
 // ---------------------------------------------------------------------------

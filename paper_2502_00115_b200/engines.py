@@ -32,6 +32,7 @@ from .mode_search import bin_center, bin_index, check_key_space, decode_flat
 
 DEFAULT_POSE_CAP = 100_000_000  # engines.py:45
 CUTOFF_EPS = 1e-9               # engines.py:49
+DENSE_MAX_BINS = 1 << 26        # csrc/dses_common.cuh kDenseMaxBins
 
 
 @dataclass(frozen=True)
@@ -128,8 +129,11 @@ def prepare(source, reference, cfg: SearchConfig) -> Prepared:
     dims = np.full(3, 2 * cfg.k_trans + 1, dtype=np.int64)
     nbins = int(dims[0]) ** 3
     check_key_space(nbins, x.shape[0])
-    if nbins > 2**31 - 1:
-        raise InvalidInputError("translation window exceeds 2^31 bins")
+    if nbins > DENSE_MAX_BINS:
+        # the search needs the dense vote (mode queries, mode_translation, take
+        # larger lattices through the sort-based path)
+        raise InvalidInputError(
+            f"translation window of {nbins} bins exceeds the GPU search limit of {DENSE_MAX_BINS}")
     code, param = cfg.metric._code_param()
     skip = cfg.metric.kind == "sat_l0" and cfg.metric.param == cfg.trans_bin  # engines.py:265
     return Prepared(x, y, cos_tab, sin_tab, center_rot, ilo, dims, code, param, skip)

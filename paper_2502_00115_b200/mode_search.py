@@ -105,8 +105,6 @@ def mode_translation(source, reference, rotation, bin_size: float, t_bounds=None
         ilo, ihi = bounds_to_index_range(t_bounds, bin_size)
     dims = ihi - ilo + 1
     check_key_space(int(np.prod(dims.astype(object))), x.shape[0])
-    if int(np.prod(dims.astype(object))) > 2**31 - 1:
-        raise InvalidInputError("translation lattice exceeds 2^31 bins")
     with _native.Plan(x, y, bin_size, ilo, dims, device) as plan:
         counts, lins, ties = plan.mode_batch(rot.reshape(1, 9))
     if counts[0] <= 0:

@@ -244,3 +244,48 @@ def test_dses_every_metric_matches_oracle(api, kind, param):
     assert math.isclose(res.best_error, ref["best_error"], rel_tol=1e-9)
     assert res.candidates_refined == ref["candidates_refined"]
     assert res.best_inliers == ref["best_inliers"]
+
+
+def _dict_mode(hist):
+    """Mode of a translation-histogram dict (oracle.translation_histogram):
+    max count, lexicographically smallest bin at the max, tied bins."""
+    best = max(hist.values())
+    tied = sorted(k for k, v in hist.items() if v == best)
+    return best, tied[0], len(tied)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_mode_translation_sparse_lattice(api, seed):
+    """No t_bounds at a fine bin: the data-derived lattice has ~10^10 bins,
+    far beyond any dense histogram -> the sort-based path (_kernels.py:196-294)."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (150, 3))
+    t = np.array([0.2031, -0.4112, 0.0555])
+    y = np.concatenate([x[:100] + t + rng.normal(0, 0.0002, (100, 3)), rng.uniform(-1, 1, (80, 3))])
+    b = 0.001
+    rot = np.eye(3)
+    res = api.mode_translation(x, y, rot, b)
+    hist = O.translation_histogram(x, y, rot, b)
+    count, idx, ties = _dict_mode(hist)
+    assert res.count == count and res.index == idx and res.num_tied_bins == ties
+
+
+def test_sparse_window_matches_dict_histogram():
+    """A bounded window just above the dense limit (410^3 bins), several rotations."""
+    from oracle import oracle as O
+    from paper_2502_00115_b200 import _native
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-0.5, 0.5, (120, 3))
+    y = rng.uniform(-0.5, 0.5, (140, 3))
+    b = 0.004
+    ilo = np.full(3, -205, dtype=np.int64)
+    dims = np.full(3, 410, dtype=np.int64)
+    rots = _rots(5, 3)
+    with _native.Plan(x, y, b, ilo, dims) as plan:
+        counts, lins, ties = plan.mode_batch(rots)
+    for r in range(rots.shape[0]):
+        hist = O.translation_histogram(x, y, rots[r], b, ilo=ilo, ihi=ilo + dims - 1)
+        count, idx, nt = _dict_mode(hist)
+        assert counts[r] == count and ties[r] == nt
+        assert O.decode_flat(lins[r], ilo, dims) == idx
