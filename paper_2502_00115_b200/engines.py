@@ -147,15 +147,7 @@ def winner_transform(prep: Prepared, cfg: SearchConfig, row: int, lin: int) -> R
     return RigidTransform(rot, t, grid_coords=tuple(grid_index(cfg.k_rot, row)))
 
 
-def dses(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationResult:
-    """Direct semi-exhaustive search on one B200 (engines.py:229-301)."""
-    from . import _native
-
-    t0 = time.perf_counter()
-    prep = prepare(source, reference, cfg)
-    grid = _native.make_grid(cfg.k_rot, prep.cos_tab, prep.sin_tab, prep.center_rot)
-    with _native.Plan(prep.x, prep.y, cfg.trans_bin, prep.ilo, prep.dims, device) as plan:
-        res = plan.search(grid, cfg.q, prep.code, prep.param, prep.skip_refine)
+def _result(prep: Prepared, cfg: SearchConfig, res: dict, t0: float) -> RegistrationResult:
     if res["candidates_evaluated"] == 0:
         raise NoCandidateError(
             "no rotation produced an in-bounds translation vote; widen k_trans "
@@ -180,3 +172,46 @@ def dses(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationR
                                           "ms_vote_kernel")},
         },
     )
+
+
+def _build(source, reference, cfg: SearchConfig, device: int):
+    """Host preparation + native plan (clouds resident on the GPU)."""
+    from . import _native
+
+    t0 = time.perf_counter()
+    prep = prepare(source, reference, cfg)
+    grid = _native.make_grid(cfg.k_rot, prep.cos_tab, prep.sin_tab, prep.center_rot)
+    plan = _native.Plan(prep.x, prep.y, cfg.trans_bin, prep.ilo, prep.dims, device)
+    return t0, prep, grid, plan
+
+
+def dses(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationResult:
+    """Direct semi-exhaustive search on one B200 (engines.py:229-301)."""
+    t0, prep, grid, plan = _build(source, reference, cfg, device)
+    with plan:
+        res = plan.search(grid, cfg.q, prep.code, prep.param, prep.skip_refine)
+    return _result(prep, cfg, res, t0)
+
+
+def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
+    """dses over a batch of (source, reference) pairs (the registration loop of
+    harness.run_batch, harness.py:145-162): the host preparation and plan
+    construction of pair k+1 (a worker thread; the C ABI releases the GIL)
+    overlap the GPU search of pair k.  Results are identical to calling
+    dses() on each pair; errors are raised for the first failing pair."""
+    import concurrent.futures as cf
+
+    pairs = list(zip(sources, references))
+    out = []
+    if not pairs:
+        return out
+    with cf.ThreadPoolExecutor(max_workers=1) as ex:
+        fut = ex.submit(_build, pairs[0][0], pairs[0][1], cfg, device)
+        for k in range(len(pairs)):
+            t0, prep, grid, plan = fut.result()
+            if k + 1 < len(pairs):
+                fut = ex.submit(_build, pairs[k + 1][0], pairs[k + 1][1], cfg, device)
+            with plan:
+                res = plan.search(grid, cfg.q, prep.code, prep.param, prep.skip_refine)
+            out.append(_result(prep, cfg, res, t0))
+    return out

@@ -289,3 +289,16 @@ def test_sparse_window_matches_dict_histogram():
         count, idx, nt = _dict_mode(hist)
         assert counts[r] == count and ties[r] == nt
         assert O.decode_flat(lins[r], ilo, dims) == idx
+
+
+def test_dses_batch_equals_single_calls(api):
+    from paper_2502_00115_b200.synth import CONFIGS, make_pair
+    pairs = [make_pair(CONFIGS["c1"]["spec"], s) for s in range(4)]
+    cfg = api.SearchConfig(k_rot=2, rot_step=math.radians(9), k_trans=20, trans_bin=0.025)
+    batch = api.dses_batch([p[0] for p in pairs], [p[1] for p in pairs], cfg)
+    for (x, y, _), b in zip(pairs, batch):
+        single = api.dses(x, y, cfg)
+        assert tuple(single.best.grid_coords) == tuple(b.best.grid_coords)
+        assert np.array_equal(single.best.translation, b.best.translation)
+        assert single.best_error == b.best_error and single.best_inliers == b.best_inliers
+    assert api.dses_batch([], [], cfg) == []
