@@ -14,6 +14,7 @@
  *   dses_refine_batch      <- _kernels.refine_batch       (_kernels.py:297-324); with one
  *                             pose it is alignment_error_kernel (_kernels.py:83-89)
  *                             after RigidTransform.apply (metrics.py:133-140)
+ *   dses_exhaustive        <- engines.exhaustive_search   (engines.py:156-193)
  *   dses_plan_* + dses_search / dses_stage_*
  *                          <- engines.dses                (engines.py:229-301),
  *                             split into the stages a multi-GPU caller needs
@@ -121,6 +122,16 @@ int dses_mode_dense_batch(int device, const double* rots, int64_t nrot, const do
 int dses_search(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t r_count, double q,
                 int metric_code, double metric_param, int skip_refine, dses_result* out,
                 void* stream);
+
+/* engines.exhaustive_search (engines.py:156-193, _kernels.exhaustive_batch
+ * _kernels.py:327-381): the metric at every pose of the 6-D grid, rotations
+ * of `grid` x translations t_center + (-k..k) * trans_bin per axis; winner =
+ * minimum error, ties to the smallest (rotation, translation) enumeration
+ * index.  winner_row / winner_lin = rotation / translation flat index,
+ * best_error = its binary64 error (refine_batch operation order). */
+int dses_exhaustive(dses_plan* plan, const dses_grid* grid, int64_t k_trans,
+                    const double t_center[3], int metric_code, double metric_param,
+                    dses_result* out, void* stream);
 
 /* ---- stages for a sharded (multi-GPU) search ----------------------------- */
 /* Stage 1: vote over this rank's rotation slice; returns local M* and the

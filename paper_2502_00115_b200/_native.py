@@ -75,6 +75,8 @@ _SIGS = [
     ("dses_search", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, ctypes.c_double,
                                    ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                    ctypes.POINTER(Result), _vp]),
+    ("dses_exhaustive", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _dp, ctypes.c_int,
+                                       ctypes.c_double, ctypes.POINTER(Result), _vp]),
     ("dses_stage_vote", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, _ip, _ip, _vp]),
     ("dses_stage_argmax", ctypes.c_int, [_vp, _i64, _ip, _vp]),
     ("dses_stage_screen", ctypes.c_int, [_vp, ctypes.c_double, _i64, ctypes.c_int, ctypes.c_double,
@@ -241,6 +243,13 @@ class Plan:
         check(self._L.dses_search(self._h, ctypes.byref(grid), int(r_begin), int(r_count), float(q),
                                   int(code), float(param), int(bool(skip_refine)),
                                   ctypes.byref(res), stream), "dses_search")
+        return res.as_dict()
+
+    def exhaustive(self, grid: Grid, k_trans, t_center, code, param, stream=None):
+        res = Result()
+        tc = np.ascontiguousarray(t_center, dtype=np.float64).reshape(3)
+        check(self._L.dses_exhaustive(self._h, ctypes.byref(grid), int(k_trans), dptr(tc), int(code),
+                                      float(param), ctypes.byref(res), stream), "dses_exhaustive")
         return res.as_dict()
 
     # ---- stages (multi-GPU) ----

@@ -50,7 +50,10 @@ cudaError_t launch_rescore_compact(const double* err, int64_t ncand, double thr,
 cudaError_t launch_exact(const ScoreParams& s, const int64_t* rows, const int* lins, const int* sel,
                          int64_t nsel, double* vals, double* out, cudaStream_t st);
 cudaError_t launch_winner(const double* err64, const int* sel, const int64_t* rows, int64_t nsel,
-                          double* best_err, int64_t* best_row, int* best_c, cudaStream_t st);
+                          double* best_err, int64_t* best_row, int* best_c, cudaStream_t st,
+                          const int* lins = nullptr);
+cudaError_t launch_enumerate_poses(int64_t p0, int64_t np, int64_t ntrans, int64_t* rows, int* lins,
+                                   cudaStream_t st);
 int screen_threads();
 int exact_threads();
 }  // namespace dses
@@ -785,6 +788,7 @@ ScoreParams score_params(const dses_plan* P, const RotSource& rs, int code, doub
   // per-axis |d32 - d64| <= 2^-24 (|y| + |p| + |d|) <= 2^-23 (bx + by); margin x2
   s.amb = (float)(2.0 * std::ldexp(P->bx + P->by, -23));
   s.tvec = nullptr;
+  s.exh_k = -1;
   s.gcell = P->gcell.as<int2>();
   s.gpts = P->gpts.as<float4>();
   for (int k = 0; k < 3; ++k) { s.gorg[k] = P->gorg[k]; s.gdim[k] = P->gdim[k]; }
@@ -1218,6 +1222,98 @@ extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, in
   out->h2d_bytes = P->traffic.h2d;
   out->d2h_bytes = P->traffic.d2h;
   return dses_stage_stats(P, &out->pairs_evaluated, &out->votes, &out->rechecks);
+}
+
+extern "C" int dses_exhaustive(dses_plan* P, const dses_grid* g, int64_t k_trans,
+                               const double t_center[3], int code, double param, dses_result* out,
+                               void* stream) {
+  TrafficScope ts_(P);
+  if (!P || !g || !t_center || !out || k_trans < 0 || code < 0 || code > 4)
+    return fail(DSES_E_INVALID, "bad arguments");
+  std::memset(out, 0, sizeof(*out));
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  RotSource rs;
+  int rc = set_grid(P, g, &rs, st);
+  if (rc) return rc;
+  const int64_t nside = 2 * k_trans + 1;
+  const int64_t ntrans = nside * nside * nside;
+  const int64_t nrot = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);
+  if (ntrans >= (1ll << 31)) return fail(DSES_E_INVALID, "translation grid too large");
+  const int64_t npose = nrot * ntrans;
+  CK(cudaEventRecord(P->ev[0], st));
+  // every pose (rotation-major, translation lexicographic: _kernels.py:327-381)
+  CK(P->cand_rows.ensure(sizeof(int64_t) * npose));
+  CK(P->cand_lins.ensure(sizeof(int) * npose));
+  CK(launched(launch_enumerate_poses(0, npose, ntrans, P->cand_rows.as<int64_t>(),
+                                     P->cand_lins.as<int>(), st)));
+  ScoreParams s = score_params(P, rs, code, param);
+  s.d1 = (int)nside;
+  s.d2 = (int)nside;
+  s.exh_k = (int)k_trans;
+  for (int k = 0; k < 3; ++k) s.tcen[k] = t_center[k];
+  // fp32 screen of every pose (chunks), then exact binary64 re-score of the
+  // poses within the rigorous screen tolerance of the minimum
+  const int64_t chunk = 1 << 20;
+  const int nblk = (int)((P->n + screen_threads() - 1) / screen_threads());
+  CK(P->partial.ensure(sizeof(double) * nblk * std::min<int64_t>(chunk, npose)));
+  CK(P->err32.ensure(sizeof(double) * npose));
+  unsigned long long* mb = P->scal.as<unsigned long long>() + 4;
+  CK(cudaMemsetAsync(mb, 0x7f, sizeof(unsigned long long), st));
+  for (int64_t p0 = 0; p0 < npose; p0 += chunk) {
+    const int64_t np = std::min<int64_t>(chunk, npose - p0);
+    CK(launched(launch_screen(s, P->cand_rows.as<int64_t>() + p0, P->cand_lins.as<int>() + p0, np,
+                              P->partial.as<double>(), P->err32.as<double>() + p0, mb, st),
+                (int)((np + 65534) / 65535) + 1));
+  }
+  double mn;
+  CK(d2h(&mn, mb, sizeof mn, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaEventRecord(P->ev[2], st));
+  const double thr = mn + screen_tolerance(P, code);
+  CK(P->sel.ensure(sizeof(int) * npose));
+  unsigned long long* ns = P->scal.as<unsigned long long>() + 5;
+  CK(cudaMemsetAsync(ns, 0, sizeof(unsigned long long), st));
+  CK(launched(launch_rescore_compact(P->err32.as<double>(), npose, thr, P->sel.as<int>(), ns, st)));
+  unsigned long long nsel;
+  CK(d2h(&nsel, ns, sizeof nsel, st));
+  CK(cudaStreamSynchronize(st));
+  if (nsel == 0) return fail(DSES_E_CUDA, "internal: exhaustive screen selected no pose");
+  CK(P->vals.ensure(sizeof(double) * P->n * nsel));
+  CK(P->err64.ensure(sizeof(double) * nsel));
+  CK(P->win_err.ensure(sizeof(double)));
+  CK(P->win_row.ensure(sizeof(int64_t)));
+  CK(P->win_c.ensure(sizeof(int)));
+  CK(launched(launch_exact(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->sel.as<int>(),
+                           (int64_t)nsel, P->vals.as<double>(), P->err64.as<double>(), st),
+              (int)((nsel + 65534) / 65535) + 1));
+  CK(launched(launch_winner(P->err64.as<double>(), P->sel.as<int>(), P->cand_rows.as<int64_t>(),
+                            (int64_t)nsel, P->win_err.as<double>(), P->win_row.as<int64_t>(),
+                            P->win_c.as<int>(), st, P->cand_lins.as<int>())));
+  double e;
+  int64_t r;
+  int c;
+  CK(d2h(&e, P->win_err.p, sizeof e, st));
+  CK(d2h(&r, P->win_row.p, sizeof r, st));
+  CK(d2h(&c, P->win_c.p, sizeof c, st));
+  CK(cudaStreamSynchronize(st));
+  int lin = 0;
+  CK(d2h(&lin, P->cand_lins.as<int>() + c, sizeof lin, st));
+  CK(cudaEventRecord(P->ev[4], st));
+  CK(cudaEventSynchronize(P->ev[4]));
+  out->candidates_evaluated = npose;
+  out->candidates_refined = 0;
+  out->winner_row = r;
+  out->winner_lin = lin;
+  out->best_error = e;
+  out->rescored = (int64_t)nsel;
+  float ms;
+  cudaEventElapsedTime(&ms, P->ev[0], P->ev[2]); out->ms_score = ms;
+  cudaEventElapsedTime(&ms, P->ev[0], P->ev[4]); out->ms_total = ms;
+  out->launches = P->traffic.launches;
+  out->h2d_bytes = P->traffic.h2d;
+  out->d2h_bytes = P->traffic.d2h;
+  return DSES_OK;
 }
 
 extern "C" int dses_plan_traffic(dses_plan* P, int64_t* h2d_bytes, int64_t* d2h_bytes,

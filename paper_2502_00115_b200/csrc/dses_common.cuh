@@ -126,6 +126,8 @@ struct ScoreParams {     // scoring kernels (dses_score.cu)
   float paramf, halff;    // fp32 metric parameter and sat_l0 half width
   float amb;              // sat_l0 fp32 ambiguity margin (absolute)
   const double* tvec;     // explicit translations (row-indexed) instead of decoding bins
+  int exh_k;              // >= 0: exhaustive-search translations t = tcen + (f - exh_k) * bin
+  double tcen[3];         //       (engines.py:168-169), f = the lattice index of lin
   // uniform grid over the reference cloud (screen nearest-neighbour search)
   const int2* gcell;      // per cell: [begin, end) into gpts
   const float4* gpts;     // reference points sorted by cell (fp32)

@@ -86,6 +86,12 @@ __global__ void compact_kernel(const int* counts, const int* lins, int64_t nrot,
 // t = bin_center(_decode_flat(lin)) = (f + ilo) * bin  (mode_search.py:51-54,167-171)
 __device__ __forceinline__ void decode_translation(const ScoreParams& s, int lin, double* t) {
   const int a = lin / (s.d1 * s.d2), rem = lin % (s.d1 * s.d2), b = rem / s.d2, c = rem % s.d2;
+  if (s.exh_k >= 0) {  // t_center + side * trans_bin, side = -k..k (engines.py:168-169)
+    t[0] = dadd(s.tcen[0], dmul((double)(a - s.exh_k), s.bin_size));
+    t[1] = dadd(s.tcen[1], dmul((double)(b - s.exh_k), s.bin_size));
+    t[2] = dadd(s.tcen[2], dmul((double)(c - s.exh_k), s.bin_size));
+    return;
+  }
   t[0] = dmul((double)(a + s.ilo0), s.bin_size);
   t[1] = dmul((double)(b + s.ilo1), s.bin_size);
   t[2] = dmul((double)(c + s.ilo2), s.bin_size);
@@ -478,7 +484,8 @@ __global__ void exact_sum_kernel(const double* vals, int n, int64_t nsel, double
 
 // lexicographic (error, row) minimum over the re-scored set; single block.
 __global__ void winner_kernel(const double* err64, const int* sel, const int64_t* rows,
-                              int64_t nsel, double* best_err, int64_t* best_row, int* best_c) {
+                              int64_t nsel, double* best_err, int64_t* best_row, int* best_c,
+                              const int* lins) {
   __shared__ double se[32];
   __shared__ int64_t sr[32];
   __shared__ int sc[32];
@@ -488,7 +495,10 @@ __global__ void winner_kernel(const double* err64, const int* sel, const int64_t
   for (int64_t k = threadIdx.x; k < nsel; k += blockDim.x) {
     const int c = sel ? sel[k] : (int)k;
     const double ek = err64[k];
-    const int64_t rk = rows[c];
+    // tie-break key: the flat rotation index (lexicographic grid order,
+    // engines.py:276-280); with `lins` (exhaustive search) rotation-major then
+    // translation index, i.e. the pose enumeration order (_kernels.py:327-381)
+    const int64_t rk = lins ? rows[c] * ((int64_t)1 << 31) + lins[c] : rows[c];
     if (ek < e || (ek == e && rk < r)) { e = ek; r = rk; cc = c; }
   }
 #pragma unroll
@@ -506,7 +516,7 @@ __global__ void winner_kernel(const double* err64, const int* sel, const int64_t
     for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
       if (se[k] < e || (se[k] == e && sr[k] < r)) { e = se[k]; r = sr[k]; cc = sc[k]; }
     *best_err = e;
-    *best_row = r;
+    *best_row = lins ? (cc >= 0 ? rows[cc] : INT64_MAX) : r;
     *best_c = cc;
   }
 }
@@ -578,6 +588,23 @@ cudaError_t launch_screen(const ScoreParams& s, const int64_t* rows, const int* 
   return cudaGetLastError();
 }
 
+__global__ void enumerate_poses_kernel(int64_t p0, int64_t np, int64_t ntrans, int64_t* rows,
+                                       int* lins) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    rows[k] = (p0 + k) / ntrans;
+    lins[k] = (int)((p0 + k) % ntrans);
+  }
+}
+
+cudaError_t launch_enumerate_poses(int64_t p0, int64_t np, int64_t ntrans, int64_t* rows, int* lins,
+                                   cudaStream_t st) {
+  if (np <= 0) return cudaSuccess;
+  enumerate_poses_kernel<<<(int)std::min<int64_t>(4096, (np + 255) / 256), 256, 0, st>>>(
+      p0, np, ntrans, rows, lins);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rescore_compact(const double* err, int64_t ncand, double thr, int* sel,
                                    unsigned long long* nsel, cudaStream_t st) {
   if (ncand <= 0) return cudaSuccess;
@@ -599,8 +626,9 @@ cudaError_t launch_exact(const ScoreParams& s, const int64_t* rows, const int* l
 }
 
 cudaError_t launch_winner(const double* err64, const int* sel, const int64_t* rows, int64_t nsel,
-                          double* best_err, int64_t* best_row, int* best_c, cudaStream_t st) {
-  winner_kernel<<<1, 1024, 0, st>>>(err64, sel, rows, nsel, best_err, best_row, best_c);
+                          double* best_err, int64_t* best_row, int* best_c, cudaStream_t st,
+                          const int* lins) {
+  winner_kernel<<<1, 1024, 0, st>>>(err64, sel, rows, nsel, best_err, best_row, best_c, lins);
   return cudaGetLastError();
 }
 

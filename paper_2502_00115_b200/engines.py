@@ -215,3 +215,53 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
                 res = plan.search(grid, cfg.q, prep.code, prep.param, prep.skip_refine)
             out.append(_result(prep, cfg, res, t0))
     return out
+
+
+def exhaustive_search(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationResult:
+    """Algorithm 1 on the GPU: the metric at every pose of the 6-D grid
+    (engines.py:156-193).  Translations are t_center + (-k..k) * trans_bin per
+    axis (engines.py:168-169, not lattice-bin centres); the winner is the
+    minimum error, ties to the first pose in rotation-major, translation-
+    lexicographic order (_kernels.py:327-381).  best_error / best_inliers of
+    the winner are recomputed like the reference (engines.py:181-182)."""
+    from . import _native
+    from .metrics import alignment_error, count_inliers
+
+    t0 = time.perf_counter()
+    x = as_point_cloud(source)
+    y = as_point_cloud(reference)
+    total_poses = cfg.rotation_count * cfg.translation_count
+    if total_poses > cfg.pose_cap:
+        raise SearchSpaceTooLargeError(
+            f"{total_poses} poses exceed the cap of {cfg.pose_cap}; exhaustive "
+            f"search cost grows as O(K_rot^3 * K_trans^3 * M * N)")
+    check_grid_args(cfg.k_rot, cfg.rot_step)
+    cos_tab, sin_tab = grid_tables(cfg.k_rot, cfg.rot_step)
+    if cfg.center is not None:
+        center_rot = np.ascontiguousarray(cfg.center.rotation, dtype=np.float64)
+        t_center = np.asarray(cfg.center.translation, dtype=np.float64)
+    else:
+        center_rot, t_center = None, np.zeros(3)
+    code, param = cfg.metric._code_param()
+    grid = _native.make_grid(cfg.k_rot, cos_tab, sin_tab, center_rot)
+    dims = np.full(3, 2 * cfg.k_trans + 1, dtype=np.int64)
+    ilo = bin_index(t_center, cfg.trans_bin) - cfg.k_trans
+    with _native.Plan(x, y, cfg.trans_bin, ilo, dims, device) as plan:
+        res = plan.exhaustive(grid, cfg.k_trans, t_center, code, param)
+    side = np.arange(-cfg.k_trans, cfg.k_trans + 1, dtype=np.int64).astype(np.float64)
+    tvals = [t_center[a] + side * cfg.trans_bin for a in range(3)]
+    nt = 2 * cfg.k_trans + 1
+    a, rem = divmod(int(res["winner_lin"]), nt * nt)
+    b, c = divmod(rem, nt)
+    t_best = np.array([tvals[0][a], tvals[1][b], tvals[2][c]])
+    row = int(res["winner_row"])
+    rot = grid_rotation(cos_tab, sin_tab, cfg.k_rot, row, center_rot)
+    best = RigidTransform(rot, t_best, grid_coords=tuple(grid_index(cfg.k_rot, row)))
+    err = alignment_error(x, y, best, cfg.metric, device)
+    inl = count_inliers(x, y, best, cfg.trans_bin, device)
+    total = time.perf_counter() - t0
+    return RegistrationResult(best=best, best_error=err, best_inliers=inl,
+                              candidates_evaluated=total_poses, candidates_refined=0,
+                              elapsed={"search": total, "total": total,
+                                       "device_total": res["ms_total"] * 1e-3,
+                                       "rescored": res["rescored"]})

@@ -239,8 +239,50 @@ def make_small():
     save("small", rec)
 
 
+def make_exh():
+    """engines.exhaustive_search (Algorithm 1, the optimality oracle) on small
+    instances: every metric, with and without a centre pose, plus the
+    DSES-vs-exhaustive inlier equality of the acceptance suite (C2)."""
+    rec = {}
+    cases = [
+        ("inliers", None, None, 2, 4),
+        ("trunc-l1", None, None, 1, 4),
+        ("l1", None, None, 1, 3),
+        ("l2", None, None, 1, 3),
+        ("trunc-l1", 0.3, (np.radians([2.0, -3.0, 4.0]), [0.03, -0.02, 0.05]), 1, 3),
+    ]
+    for c, (name, thr, centre, k_rot, k_trans) in enumerate(cases):
+        rng = np.random.default_rng(np.random.SeedSequence([0xE7, c]))
+        y = rng.uniform(-1.0, 1.0, (70, 3))
+        rot = geometry.rotation_from_euler(rng.uniform(-0.1, 0.1, 3))
+        x = (y[:45] - rng.uniform(-0.1, 0.1, 3)) @ rot + rng.normal(0, 0.01, (45, 3))
+        metric = ErrorMetric.from_name(name, 0.05, thr)
+        kw = dict(k_rot=k_rot, rot_step=math.radians(4.0), k_trans=k_trans, trans_bin=0.05,
+                  metric=metric)
+        if centre is not None:
+            kw["center"] = geometry.RigidTransform(geometry.rotation_from_euler(centre[0]),
+                                                   np.asarray(centre[1]))
+        cfg = SearchConfig(**kw)
+        p = f"e{c}"
+        res = engines.exhaustive_search(x, y, cfg)
+        rec[f"{p}_x"], rec[f"{p}_y"] = x, y
+        cfg_fields(rec, p, cfg)
+        rec[f"{p}_R"] = np.asarray(res.best.rotation)
+        rec[f"{p}_t"] = np.asarray(res.best.translation)
+        rec[f"{p}_grid"] = np.asarray(res.best.grid_coords, dtype=np.int64)
+        rec[f"{p}_best_error"] = np.float64(res.best_error)
+        rec[f"{p}_best_inliers"] = np.int64(res.best_inliers)
+        rec[f"{p}_evaluated"] = np.int64(res.candidates_evaluated)
+        if name == "inliers":
+            rec[f"{p}_dses_inliers"] = np.int64(engines.dses(x, y, cfg).best_inliers)
+        print(f"  {p}: {name} grid {res.best.grid_coords} err {res.best_error:.6g} "
+              f"inl {res.best_inliers}")
+    rec["n_exh_cases"] = np.int64(len(cases))
+    save("exh", rec)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4"]
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "exh"]
     for w in which:
         print(w)
         globals()[f"make_{w}"]()

@@ -112,3 +112,24 @@ def test_config_votes_and_dses(native, golden, name, prefix):
         assert np.array_equal(ties, rec[f"{prefix}_ties"])
     res = dses(rec["x"], rec["y"], cfg)
     check_result(res, rec, prefix)
+
+
+def test_exhaustive_search_matches_reference(native, golden):
+    """Algorithm 1 (engines.exhaustive_search) on the GPU against the
+    unmodified reference's results (tests/golden/exh.npz): winner pose
+    identical, errors within 1e-9 relative, inliers and pose count exact;
+    DSES reaches the exhaustive inlier count (reference acceptance C2)."""
+    from paper_2502_00115_b200 import dses, exhaustive_search
+    g = golden("exh")
+    for c in range(int(g["n_exh_cases"])):
+        p = f"e{c}"
+        cfg = api_cfg(g, p)
+        res = exhaustive_search(g[f"{p}_x"], g[f"{p}_y"], cfg)
+        assert tuple(res.best.grid_coords) == tuple(int(v) for v in g[f"{p}_grid"]), p
+        assert np.array_equal(res.best.translation, g[f"{p}_t"]), p
+        assert np.array_equal(res.best.rotation, g[f"{p}_R"]), p
+        assert math.isclose(res.best_error, float(g[f"{p}_best_error"]), rel_tol=1e-9, abs_tol=1e-12)
+        assert res.best_inliers == int(g[f"{p}_best_inliers"])
+        assert res.candidates_evaluated == int(g[f"{p}_evaluated"])
+        if f"{p}_dses_inliers" in g:
+            assert dses(g[f"{p}_x"], g[f"{p}_y"], cfg).best_inliers == int(g[f"{p}_dses_inliers"])
