@@ -281,8 +281,39 @@ def make_exh():
     save("exh", rec)
 
 
+def make_harness():
+    """harness._run_one (dses + apply_transform + chamfer + evaluate_pose) on
+    four benchgen instances with a small grid; ground truth from benchgen."""
+    from gridreg import harness, metrics
+    rec = {}
+    search = SearchConfig(k_rot=4, rot_step=math.radians(6.0), k_trans=20, trans_bin=0.025)
+    n = 4
+    for k in range(n):
+        inst = benchgen.make_instance(benchgen.ScenarioConfig(rng_seed=100 + k, rot_range_deg=15.0))
+        r = harness._run_one(inst, search, k, 100 + k, 1.0, 0.1)
+        p = f"h{k}"
+        rec[f"{p}_x"], rec[f"{p}_y"] = inst.source, inst.reference
+        rec[f"{p}_gt_R"] = np.asarray(inst.gt_aligner.rotation)
+        rec[f"{p}_gt_t"] = np.asarray(inst.gt_aligner.translation)
+        rec[f"{p}_status"] = np.array(r.status)
+        if r.status == "ok":
+            e = r.eval
+            rec[f"{p}_eval"] = np.array([e.mie_r, e.mie_t, e.mae_r, e.mae_t, e.chamfer])
+            rec[f"{p}_hit"] = np.int64(e.is_recall_hit)
+            rec[f"{p}_inliers"] = np.int64(r.inliers)
+            rec[f"{p}_refined"] = np.int64(r.candidates_refined)
+            res = engines.dses(inst.source, inst.reference, search)
+            rec[f"{p}_grid"] = np.asarray(res.best.grid_coords, dtype=np.int64)
+            moved = res.best.apply(inst.source)
+            rec[f"{p}_chamfer_one_way"] = np.float64(metrics._kernels.chamfer_one_way(moved, inst.reference))
+        print(f"  {p}: {r.status} {r.eval}")
+    cfg_fields(rec, "h", search)
+    rec["n_harness_cases"] = np.int64(n)
+    save("harness", rec)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "exh"]
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "exh", "harness"]
     for w in which:
         print(w)
         globals()[f"make_{w}"]()
