@@ -201,7 +201,7 @@ __device__ __forceinline__ PairBin fixed_bin(const FastK& k, const int4& Y, cons
 
 template <bool HSMEM>
 __device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsigned lin, bool ok) {
-  if (HSMEM) reds_add_if(hist_sh + ((lin << 1) & ~3u), 1u + (lin & 1u) * 0xffffu, ok);
+  if (HSMEM) reds_add_if(hist_sh + ((lin >> 1) << 2), 1u << ((lin & 1u) << 4), ok);
   else if (ok) atomicAdd(&hist[lin], 1u);
 }
 
