@@ -302,3 +302,21 @@ def test_dses_batch_equals_single_calls(api):
         assert np.array_equal(single.best.translation, b.best.translation)
         assert single.best_error == b.best_error and single.best_inliers == b.best_inliers
     assert api.dses_batch([], [], cfg) == []
+
+
+def test_source_cloud_beyond_shared_memory():
+    """41^3 histogram in shared memory + 6,000 rotated source points in global
+    memory (the vote kernel's <HSMEM, !PSMEM> instantiation)."""
+    rng = np.random.default_rng(31)
+    x = rng.normal(size=(6000, 3)) * 0.5
+    y = rng.normal(size=(2500, 3)) * 0.5
+    _check(x, y, 0.025, np.full(3, -20), np.full(3, 41), _rots(3, 31))
+
+
+def test_more_than_65535_sources_uses_32bit_counts():
+    """n >= 65536: 16-bit counters could overflow, so the histogram is 32-bit
+    (global memory) -- the <!HSMEM> instantiations."""
+    rng = np.random.default_rng(32)
+    x = rng.normal(size=(70000, 3)) * 0.5
+    y = rng.normal(size=(120, 3)) * 0.5
+    _check(x, y, 0.05, np.full(3, -10), np.full(3, 21), _rots(2, 32))
