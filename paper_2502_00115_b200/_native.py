@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libdses_b200.so")
+LIB_PATH = os.environ.get("DSES_LIB") or os.path.join(_HERE, "_lib", "libdses_b200.so")
 
 DSES_OK = 0
 DSES_E_INVALID = -1

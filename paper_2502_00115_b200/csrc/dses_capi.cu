@@ -640,7 +640,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.inv_s = inv_s;
   v.flo0 = (double)P->ilo[0]; v.flo1 = (double)P->ilo[1]; v.flo2 = (double)P->ilo[2];
   v.fd0 = (double)P->dims[0]; v.fd1 = (double)P->dims[1]; v.fd2 = (double)P->dims[2];
-  v.n = (int)n; v.m = (int)m;
+  v.n = (int)n; v.m = (int)m; v.m_pad = (int)P->m_pad;
   v.nxt = (int)xt.size(); v.nyt = (int)yt.size();
   v.xs = P->xs.as<double>(); v.ys = P->ys.as<double>(); v.yq = P->yq.as<int4>();
   v.near_off = P->near_off.as<int>(); v.near_idx = P->near_idx.as<int>();

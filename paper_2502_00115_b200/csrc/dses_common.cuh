@@ -18,6 +18,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// DSES_DEBUG_BOUNDS: device-side bounds checks on every histogram update and
+// point index (a debug build; compute-sanitizer is unavailable on the pool).
+#ifdef DSES_DEBUG_BOUNDS
+#include <cassert>
+#define DSES_ASSERT(c) assert(c)
+#else
+#define DSES_ASSERT(c) ((void)0)
+#endif
+
 namespace dses {
 
 constexpr int kTile = 32;        // points per reference group (one per lane) and per source unit
@@ -85,6 +94,7 @@ struct VoteParams {
   double flo0, flo1, flo2, fd0, fd1, fd2;
   // clouds (tile-sorted)
   int n, m, nxt, nyt;
+  int m_pad;             // reference slots (yq / ys / near lists are m_pad long)
   int unit_cap;          // capacity of the per-round (group, unit) list in shared memory
   const double* xs;      // (n,3) f64, X tile order
   const double* ys;      // (m,3) f64, Y tile order

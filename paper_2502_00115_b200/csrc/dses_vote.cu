@@ -131,6 +131,7 @@ __device__ __noinline__ unsigned vote_exact(const VoteParams& p, const double* R
     int lin2;
     if (pair_bin(p, R, Pi, i, p.yq[jj], jj, &lin2, rechecks) && lin2 == lin) return rechecks;
   }
+  DSES_ASSERT(lin >= 0 && lin < p.nbins && i >= 0 && i < p.n && j >= 0 && j < p.m_pad);
   hist_inc<HSMEM>(hist, hist_sh, lin);
   return (1u << 16) | rechecks;
 }
@@ -200,7 +201,9 @@ __device__ __forceinline__ PairBin fixed_bin(const FastK& k, const int4& Y, cons
 }
 
 template <bool HSMEM>
-__device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsigned lin, bool ok) {
+__device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsigned lin, bool ok,
+                                        unsigned nbins = 0xffffffffu) {
+  DSES_ASSERT(!ok || lin < nbins);
   if (HSMEM) reds_add_if(hist_sh + ((lin >> 1) << 2), 1u << ((lin & 1u) << 4), ok);
   else if (ok) atomicAdd(&hist[lin], 1u);
 }
@@ -250,7 +253,8 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
       ok = decided & !far & !dup & !und;
       defer[s] = b[s].near | (decided & !dup & (far | und));
     }
-    vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok);
+    vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins);
+    DSES_ASSERT(is[s] >= 0 && is[s] < p.n && j >= 0 && j < p.m_pad);
     anydef |= defer[s];
   }
   if (__any_sync(0xffffffffu, anydef)) {
