@@ -288,9 +288,11 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
   kd_tiles(pts, lo + left, hi, perm, tiles, tile);
 }
 
-// Like kd_tiles for weighted items (centroids cen, weights wt): leaves hold
-// items of total weight <= cap; splits are placed so that the left part fills
-// whole leaves where the weights allow.
+// Like kd_tiles for weighted items (centroids cen, weights wt >= 1): leaves
+// hold items of total weight <= cap.  Median splits by item count
+// (nth_element, O(n) per level) placed so that the left part holds about
+// floor(leaves / 2) * cap weight; a leaf that ends up over capacity is simply
+// split again.
 void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int64_t hi,
                  std::vector<int>& perm, std::vector<std::pair<int, int>>& tiles, int cap) {
   int64_t W = 0;
@@ -308,37 +310,79 @@ void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int6
   int axis = 0;
   for (int k = 1; k < 3; ++k)
     if (mx[k] - mn[k] > mx[axis] - mn[axis]) axis = k;
-  std::sort(perm.begin() + lo, perm.begin() + hi, [&](int a, int b) {
-    const double va = cen[3 * a + axis], vb = cen[3 * b + axis];
-    return va < vb || (va == vb && a < b);
-  });
   const int64_t ntile = (W + cap - 1) / cap;
   const int64_t target = std::max<int64_t>(1, ntile / 2) * cap;
-  int64_t s = lo, acc = 0;
-  while (s < hi - 1 && acc + wt[perm[s]] <= target) acc += wt[perm[s++]];
-  if (s == lo) s = lo + 1;
+  // split index s: the left part (the s - lo smallest along `axis`) carries as
+  // close to `target` weight as the item weights allow without exceeding it.
+  // nth_element partitions in O(n); a few corrections settle s.
+  auto less = [&](int a, int b) {
+    const double va = cen[3 * a + axis], vb = cen[3 * b + axis];
+    return va < vb || (va == vb && a < b);
+  };
+  int64_t s = lo + (int64_t)((double)target * (double)(hi - lo) / (double)W);
+  s = std::min(hi - 1, std::max(lo + 1, s));
+  std::nth_element(perm.begin() + lo, perm.begin() + s, perm.begin() + hi, less);
+  int64_t wl = 0;
+  for (int64_t q = lo; q < s; ++q) wl += wt[perm[q]];
+  if (wl > target) {  // hand the largest left items to the right part
+    const int64_t k = std::min<int64_t>(s - lo - 1, wl - target);
+    std::nth_element(perm.begin() + lo, perm.begin() + (s - k), perm.begin() + s, less);
+    std::sort(perm.begin() + (s - k), perm.begin() + s, less);
+    while (wl > target && s > lo + 1) wl -= wt[perm[--s]];
+  } else if (wl < target) {  // take the smallest right items while they fit
+    const int64_t k = std::min<int64_t>(hi - s - 1, target - wl);
+    if (k > 0) {
+      std::nth_element(perm.begin() + s, perm.begin() + (s + k), perm.begin() + hi, less);
+      std::sort(perm.begin() + s, perm.begin() + (s + k), less);
+      while (s < hi - 1 && s < s + k && wl + wt[perm[s]] <= target) wl += wt[perm[s++]];
+    }
+  }
   kd_weighted(cen, wt, lo, s, perm, tiles, cap);
   kd_weighted(cen, wt, s, hi, perm, tiles, cap);
 }
 
 // Unordered pairs (a, b), a != b, of reference points closer than thr in
-// every axis (sweep over the points sorted by axis 0).
+// every axis.  Points are bucketed into strips of width thr along axis 0 and
+// sorted by axis 1 inside each strip; a point's partners lie in its own strip
+// (later in axis-1 order) or in the next strip (an axis-1 window found by
+// binary search), so each pair is found once.
 std::vector<std::pair<int, int>> near_pairs(const double* y, int64_t m, double thr) {
-  std::vector<int> o0(m);
-  std::iota(o0.begin(), o0.end(), 0);
-  std::sort(o0.begin(), o0.end(), [&](int a, int b) {
-    return y[3 * a] < y[3 * b] || (y[3 * a] == y[3 * b] && a < b);
+  double mn0 = INFINITY;
+  for (int64_t j = 0; j < m; ++j) mn0 = std::min(mn0, y[3 * j]);
+  const double width = thr * (1.0 + 1e-9);  // partners are never two strips apart
+  struct Key { int64_t strip; double y1; int idx; };
+  std::vector<Key> keys(m);
+  for (int64_t j = 0; j < m; ++j)
+    keys[j] = {(int64_t)std::floor((y[3 * j] - mn0) / width), y[3 * j + 1], (int)j};
+  std::sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
+    if (a.strip != b.strip) return a.strip < b.strip;
+    return a.y1 < b.y1 || (a.y1 == b.y1 && a.idx < b.idx);
   });
+  auto close = [&](int a, int b) {
+    return std::fabs(y[3 * a] - y[3 * b]) < thr && std::fabs(y[3 * a + 1] - y[3 * b + 1]) < thr &&
+           std::fabs(y[3 * a + 2] - y[3 * b + 2]) < thr;
+  };
   std::vector<std::pair<int, int>> out;
-  for (int64_t a = 0; a < m; ++a) {
-    const int ja = o0[a];
-    for (int64_t b = a + 1; b < m; ++b) {
-      const int jb = o0[b];
-      if (y[3 * jb] - y[3 * ja] >= thr) break;
-      if (std::fabs(y[3 * jb + 1] - y[3 * ja + 1]) < thr &&
-          std::fabs(y[3 * jb + 2] - y[3 * ja + 2]) < thr)
-        out.emplace_back(ja, jb);
+  for (int64_t p = 0; p < m;) {
+    const int64_t sp = keys[p].strip;
+    int64_t e = p;
+    while (e < m && keys[e].strip == sp) ++e;  // current strip [p, e)
+    int64_t ne = e;
+    while (ne < m && keys[ne].strip == sp + 1) ++ne;  // next strip [e, ne)
+    for (int64_t q = p; q < e; ++q) {
+      const int a = keys[q].idx;
+      const double y1 = keys[q].y1;
+      for (int64_t r = q + 1; r < e && keys[r].y1 - y1 < thr; ++r)
+        if (close(a, keys[r].idx)) out.emplace_back(a, keys[r].idx);
+      int64_t lo = e, hi2 = ne;  // next strip: axis-1 window (y1 - thr, y1 + thr)
+      while (lo < hi2) {
+        const int64_t mid = (lo + hi2) / 2;
+        if (keys[mid].y1 <= y1 - thr) lo = mid + 1; else hi2 = mid;
+      }
+      for (int64_t r = lo; r < ne && keys[r].y1 - y1 < thr; ++r)
+        if (close(a, keys[r].idx)) out.emplace_back(a, keys[r].idx);
     }
+    p = e;
   }
   return out;
 }
@@ -416,6 +460,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   trace("dedup components");
   const double thr = P->bin * (1.0 + 1e-6);
   const std::vector<std::pair<int, int>> near = near_pairs(y, m, thr);
+  trace("  near pairs");
   // adjacency in CSR form
   std::vector<int> aoff(m + 1, 0), aidx(2 * near.size());
   for (const auto& e : near) { ++aoff[e.first + 1]; ++aoff[e.second + 1]; }
@@ -449,6 +494,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     }
   }
   const size_t nitems = item_far.size();
+  trace("  components");
   std::vector<double> cen(3 * nitems);
   std::vector<int> wt(nitems);
   for (size_t q = 0; q < nitems; ++q) {
@@ -463,6 +509,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   std::iota(iperm.begin(), iperm.end(), 0);
   std::vector<std::pair<int, int>> itiles;
   kd_weighted(cen.data(), wt, 0, (int64_t)nitems, iperm, itiles, kTile);
+  trace("  component k-d tiles");
   std::vector<int> yidx;  // tile-order entry -> original reference index
   std::vector<char> yfar;
   struct GroupSpan { int start, count, gm; };
@@ -545,8 +592,12 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   // ---- scoring layout: x original order, y sorted by axis 0 (stable)
   trace("scoring layout");
   std::vector<int> sy(m);
-  std::iota(sy.begin(), sy.end(), 0);
-  std::stable_sort(sy.begin(), sy.end(), [&](int a, int b) { return y[3 * a] < y[3 * b]; });
+  {  // stable sort by axis 0 == sort by (y0, index)
+    std::vector<std::pair<double, int>> k0(m);
+    for (int64_t j = 0; j < m; ++j) k0[j] = {y[3 * j], (int)j};
+    std::sort(k0.begin(), k0.end());
+    for (int64_t j = 0; j < m; ++j) sy[j] = k0[j].second;
+  }
   std::vector<double> c0(m), c1(m), c2(m);
   std::vector<float4> yf(m);
   for (int64_t j = 0; j < m; ++j) {
