@@ -39,19 +39,25 @@ cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t 
 cudaError_t launch_select_stats(const int* counts, int64_t nrot, unsigned long long* mstar,
                                 unsigned long long* nvalid, int sms, cudaStream_t st);
 cudaError_t launch_argmax(const int* counts, int64_t nrot, int64_t r_begin, int mstar,
-                          unsigned long long* row, int sms, cudaStream_t st);
+                          unsigned long long* row, int sms, cudaStream_t st,
+                          const unsigned long long* dmstar = nullptr);
 cudaError_t launch_compact(const int* counts, const int* lins, int64_t nrot, int64_t r_begin,
                            double cutoff, int64_t* rows, int* cl, unsigned long long* ncand, int sms,
-                           cudaStream_t st);
+                           cudaStream_t st, const unsigned long long* dmstar = nullptr,
+                           double q = 0.0);
 cudaError_t launch_screen(const ScoreParams& s, const int64_t* rows, const int* lins, int64_t ncand,
-                          double* partial, double* err, unsigned long long* minbits, cudaStream_t st);
+                          double* partial, double* err, unsigned long long* minbits, cudaStream_t st,
+                          const unsigned long long* dcount = nullptr);
 cudaError_t launch_rescore_compact(const double* err, int64_t ncand, double thr, int* sel,
-                                   unsigned long long* nsel, cudaStream_t st);
+                                   unsigned long long* nsel, cudaStream_t st,
+                                   const unsigned long long* dcount = nullptr,
+                                   const unsigned long long* dmin = nullptr, double tol = 0.0);
 cudaError_t launch_exact(const ScoreParams& s, const int64_t* rows, const int* lins, const int* sel,
-                         int64_t nsel, double* vals, double* out, cudaStream_t st);
+                         int64_t nsel, double* vals, double* out, cudaStream_t st,
+                         const unsigned long long* dcount = nullptr);
 cudaError_t launch_winner(const double* err64, const int* sel, const int64_t* rows, int64_t nsel,
                           double* best_err, int64_t* best_row, int* best_c, cudaStream_t st,
-                          const int* lins = nullptr);
+                          const int* lins = nullptr, const unsigned long long* dcount = nullptr);
 cudaError_t launch_enumerate_poses(int64_t p0, int64_t np, int64_t ntrans, int64_t* rows, int* lins,
                                    cudaStream_t st);
 int screen_threads();

@@ -21,6 +21,14 @@
 
 namespace dses {
 
+// Candidate counts are either host values or device counters (`dcount`,
+// written by the previous kernel of the same stream): kernels loop over
+// candidates with a grid stride, so a fixed grid serves either without a
+// host round trip.
+__device__ __forceinline__ int64_t eff_count(const unsigned long long* dcount, int64_t cap) {
+  return dcount ? min((int64_t)*dcount, cap) : cap;
+}
+
 
 // ---------------------------------------------------------------------------
 // phase 2
@@ -47,7 +55,8 @@ __global__ void select_stats_kernel(const int* counts, int64_t nrot, unsigned lo
 
 // smallest row whose count equals mstar (the first entry of the stable order)
 __global__ void argmax_kernel(const int* counts, int64_t nrot, int64_t r_begin, int mstar,
-                              unsigned long long* row) {
+                              unsigned long long* row, const unsigned long long* dmstar) {
+  if (dmstar) mstar = (int)*dmstar;
   unsigned long long best = ULLONG_MAX;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrot;
        r += (int64_t)gridDim.x * blockDim.x)
@@ -59,7 +68,11 @@ __global__ void argmax_kernel(const int* counts, int64_t nrot, int64_t r_begin, 
 
 __global__ void compact_kernel(const int* counts, const int* lins, int64_t nrot, int64_t r_begin,
                                double cutoff, int64_t* rows, int* cand_lins,
-                               unsigned long long* ncand) {
+                               unsigned long long* ncand, const unsigned long long* dmstar,
+                               double q) {
+  // engines.py:196-201 in binary64: cutoff = q * M* - 1e-9 (M* on the device
+  // when dmstar is given)
+  if (dmstar) cutoff = q * (double)*dmstar - 1e-9;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrot;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int c = counts[r];
@@ -185,13 +198,16 @@ constexpr int kScreenThreads = 256;
 constexpr int kScreenChunk = 2048;  // reference points per shared-memory chunk (32 KB)
 
 __global__ void __launch_bounds__(kScreenThreads) screen_kernel(ScoreParams s, const int64_t* rows,
-                                                                const int* lins, double* partial) {
+                                                                const int* lins, double* partial,
+                                                                const unsigned long long* dcount,
+                                                                int64_t ncand) {
   __shared__ double R[9], t[3];
   __shared__ float4 ych[kScreenChunk];
   __shared__ float wred[2][kScreenThreads / 32];
   __shared__ int jrange[2];
   __shared__ double sred[kScreenThreads / 32];
-  const int c = blockIdx.y;
+  const int64_t nc = eff_count(dcount, ncand);
+  for (int64_t c = blockIdx.y; c < nc; c += gridDim.y) {
   load_pose(s, rows[c], lins[c], R, t);
   const int i = blockIdx.x * kScreenThreads + threadIdx.x;
   const bool active = i < s.n;
@@ -270,6 +286,8 @@ __global__ void __launch_bounds__(kScreenThreads) screen_kernel(ScoreParams s, c
     for (int w = 0; w < kScreenThreads / 32; ++w) tot += sred[w];
     partial[(size_t)c * gridDim.x + blockIdx.x] = tot;
   }
+  __syncthreads();  // shared pose / chunk / reduction reused by the next candidate
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -339,10 +357,13 @@ __device__ float grid_nn(const ScoreParams& s, float p0, float p1, float p2, flo
 }
 
 __global__ void __launch_bounds__(kScreenThreads) screen_grid_kernel(ScoreParams s, const int64_t* rows,
-                                                                     const int* lins, double* partial) {
+                                                                     const int* lins, double* partial,
+                                                                     const unsigned long long* dcount,
+                                                                     int64_t ncand) {
   __shared__ double R[9], t[3];
   __shared__ double sred[kScreenThreads / 32];
-  const int c = blockIdx.y;
+  const int64_t nc = eff_count(dcount, ncand);
+  for (int64_t c = blockIdx.y; c < nc; c += gridDim.y) {
   load_pose(s, rows[c], lins[c], R, t);
   const int i = blockIdx.x * kScreenThreads + threadIdx.x;
   double v = 0.0;
@@ -365,6 +386,8 @@ __global__ void __launch_bounds__(kScreenThreads) screen_grid_kernel(ScoreParams
     for (int w = 0; w < kScreenThreads / 32; ++w) tot += sred[w];
     partial[(size_t)c * gridDim.x + blockIdx.x] = tot;
   }
+  __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -376,12 +399,16 @@ constexpr int kScanCands = 4;
 
 template <bool L2>
 __global__ void __launch_bounds__(kScreenThreads) screen_scan_kernel(ScoreParams s, const int64_t* rows,
-                                                                     const int* lins, int64_t ncand,
-                                                                     double* partial) {
+                                                                     const int* lins, int64_t ncand_cap,
+                                                                     double* partial,
+                                                                     const unsigned long long* dcount) {
   __shared__ double R[kScanCands][9], t[kScanCands][3];
   __shared__ float4 ych[kScreenChunk];
   __shared__ double sred[kScanCands][kScreenThreads / 32];
-  const int64_t c0 = (int64_t)blockIdx.y * kScanCands;
+  const int64_t ncand = eff_count(dcount, ncand_cap);
+  const int64_t ngroups = (ncand + kScanCands - 1) / kScanCands;
+  for (int64_t g = blockIdx.y; g < ngroups; g += gridDim.y) {
+  const int64_t c0 = g * kScanCands;
   for (int q = 0; q < kScanCands; ++q) {
     const int64_t c = min(c0 + q, ncand - 1);
     if (threadIdx.x < 9) R[q][threadIdx.x] = rotation_entry(s.rot, rows[c], threadIdx.x);
@@ -429,25 +456,35 @@ __global__ void __launch_bounds__(kScreenThreads) screen_scan_kernel(ScoreParams
     for (int w = 0; w < kScreenThreads / 32; ++w) tot += sred[threadIdx.x][w];
     partial[(size_t)(c0 + threadIdx.x) * gridDim.x + blockIdx.x] = tot;
   }
+  __syncthreads();
+  }
 }
 
 // err32[c] = sum of the block partials in block order; atomicMin of the
 // (non-negative) binary64 bits gives the minimum.
 __global__ void screen_reduce_kernel(const double* partial, int nblk, int64_t ncand, double* err,
-                                     unsigned long long* minbits) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= ncand) return;
-  double tot = 0.0;
-  for (int b = 0; b < nblk; ++b) tot += partial[c * nblk + b];
-  err[c] = tot;
-  atomicMin(minbits, (unsigned long long)__double_as_longlong(tot));
+                                     unsigned long long* minbits, const unsigned long long* dcount) {
+  const int64_t nc = eff_count(dcount, ncand);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double tot = 0.0;
+    for (int b = 0; b < nblk; ++b) tot += partial[c * nblk + b];
+    err[c] = tot;
+    atomicMin(minbits, (unsigned long long)__double_as_longlong(tot));
+  }
 }
 
+// keep candidates with screened error <= threshold; with `dmin` the
+// threshold is (device minimum) + tol
 __global__ void rescore_compact_kernel(const double* err, int64_t ncand, double threshold,
-                                       int* sel, unsigned long long* nsel) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= ncand) return;
-  if (err[c] <= threshold) sel[atomicAdd(nsel, 1ull)] = (int)c;
+                                       int* sel, unsigned long long* nsel,
+                                       const unsigned long long* dcount,
+                                       const unsigned long long* dmin, double tol) {
+  const int64_t nc = eff_count(dcount, ncand);
+  const double thr = dmin ? __longlong_as_double((long long)*dmin) + tol : threshold;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc;
+       c += (int64_t)gridDim.x * blockDim.x)
+    if (err[c] <= thr) sel[atomicAdd(nsel, 1ull)] = (int)c;
 }
 
 // ---------------------------------------------------------------------------
@@ -460,32 +497,41 @@ constexpr int kExactThreads = 128;
 __global__ void __launch_bounds__(kExactThreads) exact_points_kernel(ScoreParams s,
                                                                      const int64_t* rows,
                                                                      const int* lins,
-                                                                     const int* sel, int64_t c_off,
-                                                                     double* vals) {
+                                                                     const int* sel, int64_t nsel_cap,
+                                                                     double* vals,
+                                                                     const unsigned long long* dcount) {
   __shared__ double R[9], t[3];
-  const int64_t k = c_off + blockIdx.y;
-  const int64_t c = sel ? sel[k] : k;
-  load_pose(s, rows[c], lins[c], R, t);
-  const int i = blockIdx.x * kExactThreads + threadIdx.x;
-  if (i >= s.n) return;
-  double pp[3];
-  pose_point(R, t, s.x + 3 * i, pp);
-  vals[(size_t)k * s.n + i] = exact_point_best(s, pp[0], pp[1], pp[2]);
+  const int64_t nsel = eff_count(dcount, nsel_cap);
+  for (int64_t k = blockIdx.y; k < nsel; k += gridDim.y) {
+    const int64_t c = sel ? sel[k] : k;
+    load_pose(s, rows[c], lins[c], R, t);
+    const int i = blockIdx.x * kExactThreads + threadIdx.x;
+    if (i < s.n) {
+      double pp[3];
+      pose_point(R, t, s.x + 3 * i, pp);
+      vals[(size_t)k * s.n + i] = exact_point_best(s, pp[0], pp[1], pp[2]);
+    }
+    __syncthreads();
+  }
 }
 
-__global__ void exact_sum_kernel(const double* vals, int n, int64_t nsel, double* out) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= nsel) return;
-  const double* v = vals + (size_t)c * n;
-  double total = 0.0;
-  for (int i = 0; i < n; ++i) total = dadd(total, v[i]);
-  out[c] = total;
+__global__ void exact_sum_kernel(const double* vals, int n, int64_t nsel_cap, double* out,
+                                 const unsigned long long* dcount) {
+  const int64_t nsel = eff_count(dcount, nsel_cap);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nsel;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const double* v = vals + (size_t)c * n;
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) total = dadd(total, v[i]);
+    out[c] = total;
+  }
 }
 
 // lexicographic (error, row) minimum over the re-scored set; single block.
 __global__ void winner_kernel(const double* err64, const int* sel, const int64_t* rows,
-                              int64_t nsel, double* best_err, int64_t* best_row, int* best_c,
-                              const int* lins) {
+                              int64_t nsel_cap, double* best_err, int64_t* best_row, int* best_c,
+                              const int* lins, const unsigned long long* dcount) {
+  const int64_t nsel = eff_count(dcount, nsel_cap);
   __shared__ double se[32];
   __shared__ int64_t sr[32];
   __shared__ int sc[32];
@@ -535,56 +581,50 @@ cudaError_t launch_select_stats(const int* counts, int64_t nrot, unsigned long l
 }
 
 cudaError_t launch_argmax(const int* counts, int64_t nrot, int64_t r_begin, int mstar,
-                          unsigned long long* row, int sms, cudaStream_t st) {
+                          unsigned long long* row, int sms, cudaStream_t st,
+                          const unsigned long long* dmstar) {
   const int grid = (int)std::min<int64_t>((nrot + 255) / 256, (int64_t)sms * 8);
-  argmax_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(counts, nrot, r_begin, mstar, row);
+  argmax_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(counts, nrot, r_begin, mstar, row, dmstar);
   return cudaGetLastError();
 }
 
 cudaError_t launch_compact(const int* counts, const int* lins, int64_t nrot, int64_t r_begin,
                            double cutoff, int64_t* rows, int* cl, unsigned long long* ncand, int sms,
-                           cudaStream_t st) {
+                           cudaStream_t st, const unsigned long long* dmstar, double q) {
   const int grid = (int)std::min<int64_t>((nrot + 255) / 256, (int64_t)sms * 8);
   compact_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(counts, lins, nrot, r_begin, cutoff, rows, cl,
-                                                      ncand);
+                                                      ncand, dmstar, q);
   return cudaGetLastError();
 }
 
+// `ncand` is the exact count (dcount == nullptr) or an upper bound of the
+// device counter *dcount; the grid is capped (candidate-strided kernels).
 cudaError_t launch_screen(const ScoreParams& s, const int64_t* rows, const int* lins,
                           int64_t ncand, double* partial, double* err,
-                          unsigned long long* minbits, cudaStream_t st) {
+                          unsigned long long* minbits, cudaStream_t st,
+                          const unsigned long long* dcount) {
   if (ncand <= 0) return cudaSuccess;
   const int nblk = (s.n + kScreenThreads - 1) / kScreenThreads;
+  const int64_t cap_y = std::max<int64_t>(1, std::min<int64_t>(65535, 4096 / nblk));
   if (s.code == kL1 || s.code == kL2) {
     const int64_t ng = (ncand + kScanCands - 1) / kScanCands;
-    for (int64_t g0 = 0; g0 < ng; g0 += 65535) {
-      const int64_t gn = std::min<int64_t>(65535, ng - g0);
-      const int64_t c0 = g0 * kScanCands;
-      if (s.code == kL1)
-        screen_scan_kernel<false><<<dim3(nblk, (unsigned)gn), kScreenThreads, 0, st>>>(
-            s, rows + c0, lins + c0, ncand - c0, partial + c0 * nblk);
-      else
-        screen_scan_kernel<true><<<dim3(nblk, (unsigned)gn), kScreenThreads, 0, st>>>(
-            s, rows + c0, lins + c0, ncand - c0, partial + c0 * nblk);
-    }
-    screen_reduce_kernel<<<(int)((ncand + 255) / 256), 256, 0, st>>>(partial, nblk, ncand, err,
-                                                                     minbits);
-    return cudaGetLastError();
-  }
-  for (int64_t c0 = 0; c0 < ncand; c0 += 65535) {
-    const int64_t cn = std::min<int64_t>(65535, ncand - c0);
+    const dim3 grid(nblk, (unsigned)std::min<int64_t>(ng, dcount ? cap_y : 65535));
+    if (s.code == kL1)
+      screen_scan_kernel<false><<<grid, kScreenThreads, 0, st>>>(s, rows, lins, ncand, partial, dcount);
+    else
+      screen_scan_kernel<true><<<grid, kScreenThreads, 0, st>>>(s, rows, lins, ncand, partial, dcount);
+  } else {
     // truncated metrics: grid lookups bounded by tau; L1 / L2 (unbounded
     // nearest neighbour, far points in poorly aligned candidates) and sat_l0
     // keep the streamed full / windowed scan, measured faster for them
+    const dim3 grid(nblk, (unsigned)std::min<int64_t>(ncand, dcount ? cap_y : 65535));
     if (s.code != kTruncL1 && s.code != kTruncL2)
-      screen_kernel<<<dim3(nblk, (unsigned)cn), kScreenThreads, 0, st>>>(s, rows + c0, lins + c0,
-                                                                       partial + c0 * nblk);
+      screen_kernel<<<grid, kScreenThreads, 0, st>>>(s, rows, lins, partial, dcount, ncand);
     else
-      screen_grid_kernel<<<dim3(nblk, (unsigned)cn), kScreenThreads, 0, st>>>(
-          s, rows + c0, lins + c0, partial + c0 * nblk);
+      screen_grid_kernel<<<grid, kScreenThreads, 0, st>>>(s, rows, lins, partial, dcount, ncand);
   }
-  screen_reduce_kernel<<<(int)((ncand + 255) / 256), 256, 0, st>>>(partial, nblk, ncand, err,
-                                                                   minbits);
+  const int rb = (int)std::min<int64_t>(dcount ? 256 : 65535, (ncand + 255) / 256);
+  screen_reduce_kernel<<<std::max(rb, 1), 256, 0, st>>>(partial, nblk, ncand, err, minbits, dcount);
   return cudaGetLastError();
 }
 
@@ -606,29 +646,34 @@ cudaError_t launch_enumerate_poses(int64_t p0, int64_t np, int64_t ntrans, int64
 }
 
 cudaError_t launch_rescore_compact(const double* err, int64_t ncand, double thr, int* sel,
-                                   unsigned long long* nsel, cudaStream_t st) {
+                                   unsigned long long* nsel, cudaStream_t st,
+                                   const unsigned long long* dcount,
+                                   const unsigned long long* dmin, double tol) {
   if (ncand <= 0) return cudaSuccess;
-  rescore_compact_kernel<<<(int)((ncand + 255) / 256), 256, 0, st>>>(err, ncand, thr, sel, nsel);
+  const int rb = (int)std::min<int64_t>(dcount ? 256 : 65535, (ncand + 255) / 256);
+  rescore_compact_kernel<<<std::max(rb, 1), 256, 0, st>>>(err, ncand, thr, sel, nsel, dcount, dmin,
+                                                          tol);
   return cudaGetLastError();
 }
 
 cudaError_t launch_exact(const ScoreParams& s, const int64_t* rows, const int* lins, const int* sel,
-                         int64_t nsel, double* vals, double* out, cudaStream_t st) {
+                         int64_t nsel, double* vals, double* out, cudaStream_t st,
+                         const unsigned long long* dcount) {
   if (nsel <= 0) return cudaSuccess;
   const int nblk = (s.n + kExactThreads - 1) / kExactThreads;
-  for (int64_t c0 = 0; c0 < nsel; c0 += 65535) {
-    const int64_t cn = std::min<int64_t>(65535, nsel - c0);
-    exact_points_kernel<<<dim3(nblk, (unsigned)cn), kExactThreads, 0, st>>>(s, rows, lins, sel,
-                                                                              c0, vals);
-  }
-  exact_sum_kernel<<<(int)((nsel + 127) / 128), 128, 0, st>>>(vals, s.n, nsel, out);
+  const int64_t cap_y = std::max<int64_t>(1, std::min<int64_t>(65535, 4096 / nblk));
+  exact_points_kernel<<<dim3(nblk, (unsigned)std::min<int64_t>(nsel, dcount ? cap_y : 65535)),
+                        kExactThreads, 0, st>>>(s, rows, lins, sel, nsel, vals, dcount);
+  const int rb = (int)std::min<int64_t>(dcount ? 64 : 65535, (nsel + 127) / 128);
+  exact_sum_kernel<<<std::max(rb, 1), 128, 0, st>>>(vals, s.n, nsel, out, dcount);
   return cudaGetLastError();
 }
 
 cudaError_t launch_winner(const double* err64, const int* sel, const int64_t* rows, int64_t nsel,
                           double* best_err, int64_t* best_row, int* best_c, cudaStream_t st,
-                          const int* lins) {
-  winner_kernel<<<1, 1024, 0, st>>>(err64, sel, rows, nsel, best_err, best_row, best_c, lins);
+                          const int* lins, const unsigned long long* dcount) {
+  winner_kernel<<<1, 1024, 0, st>>>(err64, sel, rows, nsel, best_err, best_row, best_c, lins,
+                                    dcount);
   return cudaGetLastError();
 }
 
