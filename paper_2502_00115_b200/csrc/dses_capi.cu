@@ -60,6 +60,12 @@ cudaError_t launch_winner(const double* err64, const int* sel, const int64_t* ro
                           const int* lins = nullptr, const unsigned long long* dcount = nullptr);
 cudaError_t launch_enumerate_poses(int64_t p0, int64_t np, int64_t ntrans, int64_t* rows, int* lins,
                                    cudaStream_t st);
+cudaError_t launch_pick_argmax(const unsigned long long* row, const int* lins, int64_t r_begin,
+                               int64_t* cand_rows, int* cand_lins, int* win_c, cudaStream_t st);
+cudaError_t launch_finalize(const unsigned long long* scal, const double* win_err, const int* win_c,
+                            const int64_t* cand_rows, const int* cand_lins, const int* counts,
+                            int64_t r_begin, const double* miss, unsigned long long* stats,
+                            long long* rec, cudaStream_t st);
 int screen_threads();
 int exact_threads();
 }  // namespace dses
@@ -1218,57 +1224,134 @@ extern "C" int dses_stage_stats(dses_plan* P, int64_t* pairs, int64_t* votes, in
   return DSES_OK;
 }
 
+// At most this many screened candidates are re-scored inside the fused tail
+// (more -- a flat landscape of near-ties -- falls back to the staged path).
+static constexpr int64_t kFusedRescoreCap = 4096;
+
 extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t r_count,
                            double q, int code, double param, int skip_refine, dses_result* out,
                            void* stream) {
+  // engines.dses on one GPU.  After the vote, every stage reads the previous
+  // stage's counters on the device (M*, kept, screened minimum, selected), so
+  // the whole search is one stream of launches and ONE device->host read.
   TrafficScope ts_(P);
-  if (!P || !g || !out) return fail(DSES_E_INVALID, "bad arguments");
+  if (!P || !g || !out || code < 0 || code > 4) return fail(DSES_E_INVALID, "bad arguments");
   std::memset(out, 0, sizeof(*out));
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
+  const int64_t total = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);
+  if (r_count < 0) r_count = total - r_begin;
+  if (r_begin < 0 || r_begin + r_count > total) return fail(DSES_E_INVALID, "rotation range beyond the grid");
+  if (P->sparse)
+    return fail(DSES_E_INVALID, "translation window of %.3g bins is beyond the search's dense "
+                "limit (%d bins)", (double)P->dims[0] * P->dims[1] * P->dims[2], kDenseMaxBins);
   CK(cudaEventRecord(P->ev[0], st));
-  int64_t mstar = 0, nvalid = 0;
-  int rc = dses_stage_vote(P, g, r_begin, r_count, &mstar, &nvalid, stream);
+  RotSource rs;
+  int rc = set_grid(P, g, &rs, st);
   if (rc) return rc;
+  P->cur_k = g->k;
+  rc = run_vote(P, rs, r_begin, r_count, st);
+  if (rc) return rc;
+  const int64_t nr = std::max<int64_t>(r_count, 1);
+  unsigned long long* sc = P->scal.as<unsigned long long>();
+  // scal: [0] M* [1] valid [2] argmax row [3] kept [4] min screen bits [5] selected
+  CK(cudaMemsetAsync(sc, 0, 6 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(sc + 2, 0xff, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(sc + 4, 0x7f, sizeof(unsigned long long), st));
+  if (r_count > 0) CK(launched(launch_select_stats(P->counts.as<int>(), r_count, sc, sc + 1, P->sms, st)));
   CK(cudaEventRecord(P->ev[1], st));
-  out->mstar = mstar;
-  out->candidates_evaluated = nvalid;
-  out->winner_row = -1;
-  if (nvalid == 0) return DSES_OK;  // caller raises NoCandidateError (engines.py:255-259)
-  int64_t row;
-  double best_err = 0.0;
+  CK(P->cand_rows.ensure(sizeof(int64_t) * nr));
+  CK(P->cand_lins.ensure(sizeof(int) * nr));
+  CK(P->win_err.ensure(sizeof(double)));
+  CK(P->win_row.ensure(sizeof(int64_t)));
+  CK(P->win_c.ensure(sizeof(int)));
+  CK(P->tvec.ensure(sizeof(double) * (P->n + 16)));  // the winner's inlier pass (+ miss, record)
+  double* inl_vals = P->tvec.as<double>();
+  double* miss = inl_vals + P->n;
+  long long* rec = reinterpret_cast<long long*>(inl_vals + P->n + 2);
+  const int64_t cap = std::min<int64_t>(nr, kFusedRescoreCap);
   if (skip_refine) {
-    rc = dses_stage_argmax(P, mstar, &row, stream);
-    if (rc) return rc;
+    CK(launched(launch_argmax(P->counts.as<int>(), r_count, r_begin, 0, sc + 2, P->sms, st, sc)));
+    CK(launched(launch_pick_argmax(sc + 2, P->lins.as<int>(), r_begin, P->cand_rows.as<int64_t>(),
+                                   P->cand_lins.as<int>(), P->win_c.as<int>(), st)));
     CK(cudaEventRecord(P->ev[2], st));
     CK(cudaEventRecord(P->ev[3], st));
-    out->candidates_refined = 0;
   } else {
-    int64_t kept;
-    double mn, tol;
-    rc = dses_stage_screen(P, q, mstar, code, param, &kept, &mn, &tol, stream);
-    if (rc) return rc;
+    CK(launched(launch_compact(P->counts.as<int>(), P->lins.as<int>(), r_count, r_begin, 0.0,
+                               P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), sc + 3, P->sms,
+                               st, sc, q)));
     CK(cudaEventRecord(P->ev[2], st));
-    int64_t rescored;
-    rc = dses_stage_rescore(P, mn + tol, code, param, &best_err, &row, &rescored, stream);
-    if (rc) return rc;
+    const int nblk = (int)((P->n + screen_threads() - 1) / screen_threads());
+    CK(P->partial.ensure(sizeof(double) * nblk * nr));
+    CK(P->err32.ensure(sizeof(double) * nr));
+    CK(P->sel.ensure(sizeof(int) * nr));
+    CK(P->vals.ensure(sizeof(double) * P->n * cap));
+    CK(P->err64.ensure(sizeof(double) * cap));
+    const ScoreParams s = score_params(P, rs, code, param);
+    CK(launched(launch_screen(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), nr,
+                              P->partial.as<double>(), P->err32.as<double>(), sc + 4, st, sc + 3), 2));
+    CK(launched(launch_rescore_compact(P->err32.as<double>(), nr, 0.0, P->sel.as<int>(), sc + 5, st,
+                                       sc + 3, sc + 4, screen_tolerance(P, code))));
+    CK(launched(launch_exact(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->sel.as<int>(),
+                             cap, P->vals.as<double>(), P->err64.as<double>(), st, sc + 5), 2));
+    CK(launched(launch_winner(P->err64.as<double>(), P->sel.as<int>(), P->cand_rows.as<int64_t>(),
+                              cap, P->win_err.as<double>(), P->win_row.as<int64_t>(),
+                              P->win_c.as<int>(), st, nullptr, sc + 5)));
     CK(cudaEventRecord(P->ev[3], st));
-    out->candidates_refined = std::max<int64_t>(1, kept);
-    out->rescored = rescored;
   }
-  int64_t lin, cnt;
-  rc = dses_stage_row_info(P, row, &lin, &cnt, stream);
-  if (rc) return rc;
-  double miss;
-  rc = dses_pose_error(P, g, row, lin, kSatL0, P->bin, &miss, stream);
-  if (rc) return rc;
+  // inlier count of the winner: exact sat_l0 at the bin size (metrics.py:143-150)
+  const ScoreParams si = score_params(P, rs, kSatL0, P->bin);
+  CK(launched(launch_exact(si, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->win_c.as<int>(),
+                           1, inl_vals, miss, st), 2));
+  CK(launched(launch_finalize(sc, P->win_err.as<double>(), P->win_c.as<int>(),
+                              P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(),
+                              P->counts.as<int>(), r_begin, miss,
+                              P->stats.as<unsigned long long>(), rec, st)));
+  long long h[12];
+  CK(d2h(h, rec, sizeof h, st));
   CK(cudaEventRecord(P->ev[4], st));
   CK(cudaEventSynchronize(P->ev[4]));
-  out->winner_row = row;
-  out->winner_lin = lin;
-  out->winner_count = cnt;
-  out->best_error = skip_refine ? miss : best_err;
-  out->best_inliers = P->n - (int64_t)std::llround(miss);
+  out->mstar = h[0];
+  out->candidates_evaluated = h[1];
+  out->pairs_evaluated = h[7];
+  out->votes = h[8];
+  out->rechecks = h[9];
+  out->winner_row = -1;
+  if (out->candidates_evaluated == 0) return DSES_OK;  // caller raises NoCandidateError
+  const int64_t kept = h[2], nsel = h[3];
+  if (!skip_refine && nsel > cap) {
+    // more near-minimum candidates than the fused tail re-scores: staged path
+    double mn32;
+    double tol;
+    int64_t kept2;
+    P->cur_r_begin = r_begin;
+    P->cur_r_count = r_count;
+    rc = dses_stage_screen(P, q, out->mstar, code, param, &kept2, &mn32, &tol, stream);
+    if (rc) return rc;
+    double e;
+    int64_t row, rescored;
+    rc = dses_stage_rescore(P, mn32 + tol, code, param, &e, &row, &rescored, stream);
+    if (rc) return rc;
+    int64_t lin, cnt;
+    rc = dses_stage_row_info(P, row, &lin, &cnt, stream);
+    if (rc) return rc;
+    double m2;
+    rc = dses_pose_error(P, g, row, lin, kSatL0, P->bin, &m2, stream);
+    if (rc) return rc;
+    h[4] = row; h[5] = lin; h[6] = cnt;
+    std::memcpy(&h[10], &e, sizeof e);
+    std::memcpy(&h[11], &m2, sizeof m2);
+  }
+  double best_err, miss_h;
+  std::memcpy(&best_err, &h[10], sizeof best_err);
+  std::memcpy(&miss_h, &h[11], sizeof miss_h);
+  out->winner_row = h[4];
+  out->winner_lin = h[5];
+  out->winner_count = h[6];
+  out->candidates_refined = skip_refine ? 0 : std::max<int64_t>(1, kept);
+  out->rescored = skip_refine ? 0 : nsel;
+  out->best_error = skip_refine ? miss_h : best_err;
+  out->best_inliers = P->n - (int64_t)std::llround(miss_h);
   float ms;
   cudaEventElapsedTime(&ms, P->ev[5], P->ev[6]); out->ms_vote_kernel = ms;
   cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]); out->ms_vote = ms;
@@ -1278,7 +1361,7 @@ extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, in
   out->launches = P->traffic.launches;
   out->h2d_bytes = P->traffic.h2d;
   out->d2h_bytes = P->traffic.d2h;
-  return dses_stage_stats(P, &out->pairs_evaluated, &out->votes, &out->rechecks);
+  return DSES_OK;
 }
 
 extern "C" int dses_exhaustive(dses_plan* P, const dses_grid* g, int64_t k_trans,

@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(kExactThreads) exact_points_kernel(ScoreParams
   const int64_t nsel = eff_count(dcount, nsel_cap);
   for (int64_t k = blockIdx.y; k < nsel; k += gridDim.y) {
     const int64_t c = sel ? sel[k] : k;
+    if (c < 0) continue;  // no winner (block-uniform)
     load_pose(s, rows[c], lins[c], R, t);
     const int i = blockIdx.x * kExactThreads + threadIdx.x;
     if (i < s.n) {
@@ -625,6 +626,58 @@ cudaError_t launch_screen(const ScoreParams& s, const int64_t* rows, const int* 
   }
   const int rb = (int)std::min<int64_t>(dcount ? 256 : 65535, (ncand + 255) / 256);
   screen_reduce_kernel<<<std::max(rb, 1), 256, 0, st>>>(partial, nblk, ncand, err, minbits, dcount);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// single-GPU search tail without host round trips (dses_search)
+// ---------------------------------------------------------------------------
+// sat_l0 shortcut winner (engines.py:265-268): the argmax row becomes
+// candidate 0 so the inlier pass below reads it like a re-scored winner
+__global__ void pick_argmax_kernel(const unsigned long long* row, const int* lins, int64_t r_begin,
+                                   int64_t* cand_rows, int* cand_lins, int* win_c) {
+  const unsigned long long r = *row;
+  if (r == ~0ull) { cand_rows[0] = 0; cand_lins[0] = 0; *win_c = -1; return; }
+  cand_rows[0] = (int64_t)r;
+  cand_lins[0] = lins[(int64_t)r - r_begin];
+  *win_c = 0;
+}
+
+// result record: [0] mstar [1] nvalid [2] kept [3] nsel [4] winner row [5] winner lin
+// [6] winner count [7] pairs [8] votes [9] rechecks, doubles: [10] best error [11] miss
+__global__ void finalize_kernel(const unsigned long long* scal, const double* win_err,
+                                const int* win_c, const int64_t* cand_rows, const int* cand_lins,
+                                const int* counts, int64_t r_begin, const double* miss,
+                                unsigned long long* stats, long long* rec) {
+  rec[0] = (long long)scal[0];
+  rec[1] = (long long)scal[1];
+  rec[2] = (long long)scal[3];
+  rec[3] = (long long)scal[5];
+  const int c = *win_c;
+  const int64_t row = c >= 0 ? cand_rows[c] : -1;
+  rec[4] = row;
+  rec[5] = c >= 0 ? cand_lins[c] : -1;
+  rec[6] = c >= 0 ? counts[row - r_begin] : 0;
+  rec[7] = (long long)stats[0];
+  rec[8] = (long long)stats[1];
+  rec[9] = (long long)stats[2];
+  stats[0] = stats[1] = stats[2] = 0;
+  reinterpret_cast<double*>(rec)[10] = c >= 0 ? *win_err : 0.0;
+  reinterpret_cast<double*>(rec)[11] = c >= 0 ? *miss : 0.0;
+}
+
+cudaError_t launch_pick_argmax(const unsigned long long* row, const int* lins, int64_t r_begin,
+                               int64_t* cand_rows, int* cand_lins, int* win_c, cudaStream_t st) {
+  pick_argmax_kernel<<<1, 1, 0, st>>>(row, lins, r_begin, cand_rows, cand_lins, win_c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const unsigned long long* scal, const double* win_err, const int* win_c,
+                            const int64_t* cand_rows, const int* cand_lins, const int* counts,
+                            int64_t r_begin, const double* miss, unsigned long long* stats,
+                            long long* rec, cudaStream_t st) {
+  finalize_kernel<<<1, 1, 0, st>>>(scal, win_err, win_c, cand_rows, cand_lins, counts, r_begin, miss,
+                                   stats, rec);
   return cudaGetLastError();
 }
 
