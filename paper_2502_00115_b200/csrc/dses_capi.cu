@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <limits>
 #include <numeric>
 #include <string>
@@ -427,6 +428,71 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     tmax = std::max(tmax, (std::fabs((double)P->ilo[k]) + (double)P->dims[k]) * P->bin);
   P->bx = xnorm + tmax;
 
+  // ---- scoring layout (y sorted by axis 0, fp32 copy, uniform grid) on a
+  //      helper thread: independent of the vote layout built below
+  std::vector<double> c0, c1, c2;
+  std::vector<float4> yf, gp;
+  std::vector<int2> range;
+  // (small clouds: deferred, i.e. run inline at get(); a thread costs more)
+  auto scoring = std::async(m >= 4096 ? std::launch::async : std::launch::deferred, [&]() {
+  // ---- scoring layout: x original order, y sorted by axis 0 (stable)
+  trace("scoring layout");
+  std::vector<int> sy(m);
+  {  // stable sort by axis 0 == sort by (y0, index)
+    std::vector<std::pair<double, int>> k0(m);
+    for (int64_t j = 0; j < m; ++j) k0[j] = {y[3 * j], (int)j};
+    std::sort(k0.begin(), k0.end());
+    for (int64_t j = 0; j < m; ++j) sy[j] = k0[j].second;
+  }
+  c0.resize(m); c1.resize(m); c2.resize(m);
+  yf.resize(m);
+  for (int64_t j = 0; j < m; ++j) {
+    c0[j] = y[3 * sy[j]];
+    c1[j] = y[3 * sy[j] + 1];
+    c2[j] = y[3 * sy[j] + 2];
+    yf[j] = make_float4((float)c0[j], (float)c1[j], (float)c2[j], 0.f);
+  }
+  {  // uniform grid over y for the screen's nearest-neighbour search: cells of
+     // 4 translation bins (grown until the grid has <= 2^20 cells)
+    trace("score grid");
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t j = 0; j < m; ++j)
+      for (int k = 0; k < 3; ++k) {
+        const float v = (&yf[j].x)[k];
+        mn[k] = std::min(mn[k], v);
+        mx[k] = std::max(mx[k], v);
+      }
+    double h = 4.0 * P->bin;
+    int dim[3];
+    for (;;) {
+      int64_t cells = 1;
+      for (int k = 0; k < 3; ++k) {
+        dim[k] = (int)std::min<double>(std::floor((mx[k] - mn[k]) / h) + 1.0, 1 << 20);
+        cells *= dim[k];
+      }
+      if (cells <= (1 << 20)) break;
+      h *= 1.25;
+    }
+    const float hf = (float)h, inv = (float)(1.0 / h);
+    auto cell_of = [&](const float4& q) {
+      int c[3];
+      for (int k = 0; k < 3; ++k)
+        c[k] = std::min(dim[k] - 1, std::max(0, (int)std::floor(((&q.x)[k] - mn[k]) * inv)));
+      return (c[0] * dim[1] + c[1]) * dim[2] + c[2];
+    };
+    const int ncell = dim[0] * dim[1] * dim[2];
+    std::vector<int> cnt(ncell + 1, 0), cid(m);
+    for (int64_t j = 0; j < m; ++j) { cid[j] = cell_of(yf[j]); ++cnt[cid[j] + 1]; }
+    for (int c = 0; c < ncell; ++c) cnt[c + 1] += cnt[c];
+    range.resize(ncell);
+    for (int c = 0; c < ncell; ++c) range[c] = make_int2(cnt[c], cnt[c + 1]);
+    gp.resize(m);
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t j = 0; j < m; ++j) gp[fill[cid[j]]++] = yf[j];
+    for (int k = 0; k < 3; ++k) { P->gorg[k] = mn[k]; P->gdim[k] = dim[k]; }
+    P->gh = hf;
+  }
+  });
   // ---- spatial tiles
   trace("spatial tiles");
   std::vector<int> px(n);
@@ -601,30 +667,12 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       if (noff[q + 1] - noff[q] > 1) std::sort(nidx.begin() + noff[q], nidx.begin() + noff[q + 1]);
   }
   P->near_pairs = npairs;
-  // ---- scoring layout: x original order, y sorted by axis 0 (stable)
-  trace("scoring layout");
-  std::vector<int> sy(m);
-  {  // stable sort by axis 0 == sort by (y0, index)
-    std::vector<std::pair<double, int>> k0(m);
-    for (int64_t j = 0; j < m; ++j) k0[j] = {y[3 * j], (int)j};
-    std::sort(k0.begin(), k0.end());
-    for (int64_t j = 0; j < m; ++j) sy[j] = k0[j].second;
-  }
-  std::vector<double> c0(m), c1(m), c2(m);
-  std::vector<float4> yf(m);
-  for (int64_t j = 0; j < m; ++j) {
-    c0[j] = y[3 * sy[j]];
-    c1[j] = y[3 * sy[j] + 1];
-    c2[j] = y[3 * sy[j] + 2];
-    yf[j] = make_float4((float)c0[j], (float)c1[j], (float)c2[j], 0.f);
-  }
   std::vector<double> xv(x, x + 3 * n);
+  scoring.get();
   // ---- uploads
   UploadPack pack;
   const std::vector<double> yv(y, y + 3 * m);
   pack.add(P->yorig, yv);
-  std::vector<int2> range;  // score grid (filled below)
-  std::vector<float4> gp;
   pack.add(P->xs, xs);
   pack.add(P->ys, ys);
   pack.add(P->yq, yq);
@@ -638,48 +686,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   pack.add(P->ys1, c1);
   pack.add(P->ys2, c2);
   pack.add(P->ysf, yf);
-  {  // uniform grid over y for the screen's nearest-neighbour search: cells of
-     // 4 translation bins (grown until the grid has <= 2^20 cells)
-    trace("score grid");
-    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int64_t j = 0; j < m; ++j)
-      for (int k = 0; k < 3; ++k) {
-        const float v = (&yf[j].x)[k];
-        mn[k] = std::min(mn[k], v);
-        mx[k] = std::max(mx[k], v);
-      }
-    double h = 4.0 * P->bin;
-    int dim[3];
-    for (;;) {
-      int64_t cells = 1;
-      for (int k = 0; k < 3; ++k) {
-        dim[k] = (int)std::min<double>(std::floor((mx[k] - mn[k]) / h) + 1.0, 1 << 20);
-        cells *= dim[k];
-      }
-      if (cells <= (1 << 20)) break;
-      h *= 1.25;
-    }
-    const float hf = (float)h, inv = (float)(1.0 / h);
-    auto cell_of = [&](const float4& q) {
-      int c[3];
-      for (int k = 0; k < 3; ++k)
-        c[k] = std::min(dim[k] - 1, std::max(0, (int)std::floor(((&q.x)[k] - mn[k]) * inv)));
-      return (c[0] * dim[1] + c[1]) * dim[2] + c[2];
-    };
-    const int ncell = dim[0] * dim[1] * dim[2];
-    std::vector<int> cnt(ncell + 1, 0), cid(m);
-    for (int64_t j = 0; j < m; ++j) { cid[j] = cell_of(yf[j]); ++cnt[cid[j] + 1]; }
-    for (int c = 0; c < ncell; ++c) cnt[c + 1] += cnt[c];
-    range.resize(ncell);
-    for (int c = 0; c < ncell; ++c) range[c] = make_int2(cnt[c], cnt[c + 1]);
-    gp.resize(m);
-    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
-    for (int64_t j = 0; j < m; ++j) gp[fill[cid[j]]++] = yf[j];
-    pack.add(P->gcell, range);
-    pack.add(P->gpts, gp);
-    for (int k = 0; k < 3; ++k) { P->gorg[k] = mn[k]; P->gdim[k] = dim[k]; }
-    P->gh = hf;
-  }
+  pack.add(P->gcell, range);
+  pack.add(P->gpts, gp);
   CK(pack.commit(P->arena, st));
   CK(P->stats.ensure(4 * sizeof(unsigned long long)));
   CK(cudaMemsetAsync(P->stats.p, 0, 4 * sizeof(unsigned long long), st));
