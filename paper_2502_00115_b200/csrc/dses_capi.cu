@@ -307,10 +307,12 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
 // floor(leaves / 2) * cap weight; a leaf that ends up over capacity is simply
 // split again.
 void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int64_t hi,
-                 std::vector<int>& perm, std::vector<std::pair<int, int>>& tiles, int cap) {
+                 std::vector<int>& perm, std::vector<std::pair<int, int>>& tiles, int cap,
+                 int64_t leaves) {
   int64_t W = 0;
   for (int64_t q = lo; q < hi; ++q) W += wt[perm[q]];
-  if (W <= cap || hi - lo <= 1) {
+  leaves = std::max<int64_t>(leaves, (W + cap - 1) / cap);
+  if (leaves <= 1 || hi - lo <= 1) {
     if (hi > lo) tiles.emplace_back((int)lo, (int)(hi - lo));
     return;
   }
@@ -323,8 +325,11 @@ void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int6
   int axis = 0;
   for (int k = 1; k < 3; ++k)
     if (mx[k] - mn[k] > mx[axis] - mn[axis]) axis = k;
-  const int64_t ntile = (W + cap - 1) / cap;
-  const int64_t target = std::max<int64_t>(1, ntile / 2) * cap;
+  // the left part gets half the leaf budget and the same share of the weight,
+  // so both parts keep the parent's fill fraction (slack is spread evenly
+  // instead of spilling one item into an extra, nearly empty leaf).
+  const int64_t lleaves = leaves / 2;
+  const int64_t target = std::max<int64_t>(1, W * lleaves / leaves);
   // split index s: the left part (the s - lo smallest along `axis`) carries as
   // close to `target` weight as the item weights allow without exceeding it.
   // nth_element partitions in O(n); a few corrections settle s.
@@ -350,8 +355,8 @@ void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int6
       while (s < hi - 1 && s < s + k && wl + wt[perm[s]] <= target) wl += wt[perm[s++]];
     }
   }
-  kd_weighted(cen, wt, lo, s, perm, tiles, cap);
-  kd_weighted(cen, wt, s, hi, perm, tiles, cap);
+  kd_weighted(cen, wt, lo, s, perm, tiles, cap, lleaves);
+  kd_weighted(cen, wt, s, hi, perm, tiles, cap, leaves - lleaves);
 }
 
 // Unordered pairs (a, b), a != b, of reference points closer than thr in
@@ -586,7 +591,9 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   std::vector<int> iperm(nitems);
   std::iota(iperm.begin(), iperm.end(), 0);
   std::vector<std::pair<int, int>> itiles;
-  kd_weighted(cen.data(), wt, 0, (int64_t)nitems, iperm, itiles, kTile);
+  // leaf budget = ceil(total / 32); a looser budget (fewer-filled groups) grew
+  // the group boxes more than it saved lanes (experiments)
+  kd_weighted(cen.data(), wt, 0, (int64_t)nitems, iperm, itiles, kTile, 0);
   trace("  component k-d tiles");
   std::vector<int> yidx;  // tile-order entry -> original reference index
   std::vector<char> yfar;
