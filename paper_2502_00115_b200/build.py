@@ -43,21 +43,28 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT) -> str:
+    """defines: extra -D flags (kernel variants for A/B timing, tools/gpu_ab.sh)."""
     if not force and not needs_build():
         return OUT
     exe = nvcc()
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     cmd = [exe, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall,-Wextra,-Winfinite-recursion", "-shared",
-           f'-DDSES_NVCC_VERSION="{nvcc_version(exe)}"', "-o", OUT + ".tmp",
+           f'-DDSES_NVCC_VERSION="{nvcc_version(exe)}"', *[f"-D{d}" for d in defines],
+           "-o", out + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2502_00115_b200.build [--force] [-v] [-DNAME=V ... -o OUT.so]
+    args = sys.argv[1:]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    dest = args[args.index("-o") + 1] if "-o" in args else OUT
+    print(build(force="--force" in args or bool(defs) or dest != OUT, verbose="-v" in args,
+                defines=defs, out=dest))

@@ -35,6 +35,13 @@
 #define DSES_NS4 0  // four source points per slot (measured slower at 768 threads)
 #endif
 
+#ifndef DSES_CHUNKBOX
+#define DSES_CHUNKBOX 1
+#endif
+#ifndef DSES_POP
+#define DSES_POP 2  // units per claim when the round's overlap is sparse
+#endif
+
 namespace dses {
 
 // Fast fixed-point bin of pair (Yq, Pq); returns 0 = out of window, 1 = in
@@ -280,8 +287,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   int4* P;
   if (PSMEM) { P = reinterpret_cast<int4*>(smem + off); off += (size_t)p.n_pad * 16; }
   else P = p.p_global + (size_t)blockIdx.x * p.n_pad;
+  const int nxc = (p.nxt + 31) >> 5;                // chunks of 32 units
   int4* XB = reinterpret_cast<int4*>(smem + off);  // [2*nxt] rotated unit boxes (lo, hi)
-  off += (size_t)p.nxt * 32;
+  int4* CB = XB + 2 * p.nxt;                       // [2*nxc] their union per chunk
+  off += (size_t)(p.nxt + nxc) * 32;
   double* R = reinterpret_cast<double*>(smem + off);
   off += 16 * 8;
   int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + counters
@@ -340,11 +349,24 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       }
       if (PSMEM) P[i] = v; else __stcg(&P[i], v);
     }
-    for (int t = tid; t < p.nxt; t += nthreads) {
-      int4 lo, hi;
-      tile_box(p, R, p.xt[t], exact_mode, lo, hi);
-      XB[2 * t] = lo;
-      XB[2 * t + 1] = hi;
+    for (int c = warp; c < nxc; c += nwarps) {  // warp = chunk, lane = unit
+      const int t = 32 * c + lane;
+      int4 lo = make_int4(INT_MAX, INT_MAX, INT_MAX, 0), hi = make_int4(INT_MIN, INT_MIN, INT_MIN, 0);
+      if (t < p.nxt) {
+        tile_box(p, R, p.xt[t], exact_mode, lo, hi);
+        XB[2 * t] = lo;
+        XB[2 * t + 1] = hi;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo.x = min(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
+        lo.y = min(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, o));
+        lo.z = min(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, o));
+        hi.x = max(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, o));
+        hi.y = max(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, o));
+        hi.z = max(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, o));
+      }
+      if (lane == 0) { CB[2 * c] = lo; CB[2 * c + 1] = hi; }
     }
     __syncthreads();
 
@@ -364,6 +386,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       for (int b = b0 + warp; b < b1; b += nwarps) {
         const YTile yt = load_ytile(p.yt, b);
         for (int a0 = 0; a0 < p.nxt; a0 += 32) {
+          // whole chunk outside the group's reach: one warp-uniform test
+          if (DSES_CHUNKBOX && nxc > 1 && !exact_mode &&
+              !boxes_meet(p, yt, CB[2 * (a0 >> 5)], CB[2 * (a0 >> 5) + 1]))
+            continue;
           const int a = a0 + lane;
           const bool ov = a < p.nxt && (exact_mode || boxes_meet(p, yt, XB[2 * a], XB[2 * a + 1]));
           const unsigned m = __ballot_sync(0xffffffffu, ov);
@@ -377,11 +403,17 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       }
       __syncthreads();
       const int nunits = *s_nunits;
-      for (;;) {
-        int u = 0;
-        if (lane == 0) u = atomicAdd(s_next, 1);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= nunits) break;
+      // sparse overlap (< 1/4 of the round's (group, unit) pairs) means light
+      // units: claim DSES_POP at a time to amortise the claim; dense overlap
+      // (heavy units) claims one at a time to keep the round's tail balanced
+      const int kpop = (4 * nunits < (b1 - b0) * p.nxt) ? DSES_POP : 1;
+      for (int u = nunits, uend = nunits;; ++u) {
+        if (u >= uend) {  // claim the next kpop units
+          if (lane == 0) u = atomicAdd(s_next, kpop);
+          u = __shfl_sync(0xffffffffu, u, 0);
+          if (u >= nunits) break;
+          uend = min(nunits, u + kpop);
+        }
         const int unit = units[u];
         const YTile yt = load_ytile(p.yt, unit >> 16);
         const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + (unit & 0xffff)));
@@ -529,7 +561,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
   size_t b = 0;
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n_pad * 16;
-  b += (size_t)p.nxt * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)p.unit_cap * 4;
+  b += (size_t)(p.nxt + (p.nxt + 31) / 32) * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)p.unit_cap * 4;
   b += (size_t)(threads / 32) * kRare * 8;
   return b;
 }
