@@ -106,6 +106,16 @@ int dses_mode_batch(dses_plan* plan, const double* rots, int64_t nrot, int64_t* 
 /* Same for rotations [r_begin, r_begin + nrot) of an Euler grid. */
 int dses_mode_grid(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t nrot,
                    int64_t* counts, int64_t* lins, int64_t* ties, void* stream);
+/* Full translation vote map of ONE rotation (rot: host (3,3) f64) over the
+ * plan's lattice -- mode_search.translation_histogram (mode_search.py:205-235):
+ * bins in ascending flat order with their counts (distinct source points per
+ * bin when `dedup`, raw pair votes otherwise).  Pair bins use the vote
+ * kernel's binary64 operation order (_kernels.py:244-253).  *nbins = number of
+ * non-empty bins (DSES_E_INVALID if > cap; cap = n*m always suffices),
+ * *npairs (optional) = pairs inside the lattice. */
+int dses_translation_histogram(dses_plan* plan, const double* rot, int dedup, int64_t* lins,
+                               int64_t* counts, int64_t cap, int64_t* nbins, int64_t* npairs,
+                               void* stream);
 /* Exact fp64 alignment error of `ncand` poses (rots (c,3,3), ts (c,3)) in
  * refine_batch's operation order -- _kernels.py:297-324. */
 int dses_refine_batch(dses_plan* plan, const double* rots, const double* ts, int64_t ncand,

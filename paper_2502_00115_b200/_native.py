@@ -70,6 +70,8 @@ _SIGS = [
     ("dses_mode_grid", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, _ip, _ip, _ip, _vp]),
     ("dses_refine_batch", ctypes.c_int, [_vp, _dp, _dp, _i64, ctypes.c_int, ctypes.c_double, _dp,
                                          _vp]),
+    ("dses_translation_histogram", ctypes.c_int, [_vp, _dp, ctypes.c_int, _ip, _ip, _i64, _ip, _ip,
+                                                  _vp]),
     ("dses_mode_dense_batch", ctypes.c_int, [ctypes.c_int, _dp, _i64, _dp, _i64, _dp, _i64,
                                              ctypes.c_double, _ip, _ip, _ip, _ip, _ip]),
     ("dses_search", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, ctypes.c_double,
@@ -229,6 +231,18 @@ class Plan:
         check(self._L.dses_mode_grid(self._h, ctypes.byref(grid), int(r_begin), int(nrot), iptr(c),
                                      iptr(l), iptr(t), stream), "dses_mode_grid")
         return c, l, t
+
+    def histogram(self, rot, dedup=True, stream=None):
+        """(flat bins ascending, counts, pairs in lattice) of one rotation."""
+        rot = np.ascontiguousarray(rot, dtype=np.float64).reshape(9)
+        cap = self.n * self.m
+        lins, counts = np.empty(cap, dtype=np.int64), np.empty(cap, dtype=np.int64)
+        nb, npairs = ctypes.c_int64(0), ctypes.c_int64(0)
+        check(self._L.dses_translation_histogram(self._h, dptr(rot), int(bool(dedup)), iptr(lins),
+                                                 iptr(counts), cap, ctypes.byref(nb),
+                                                 ctypes.byref(npairs), stream),
+              "dses_translation_histogram")
+        return lins[:nb.value].copy(), counts[:nb.value].copy(), npairs.value
 
     def refine_batch(self, rots, ts, code, param, stream=None):
         rots = np.ascontiguousarray(rots, dtype=np.float64).reshape(-1, 9)

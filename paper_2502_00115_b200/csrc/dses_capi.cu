@@ -36,6 +36,10 @@ size_t sparse_scratch_bytes(int64_t n, int64_t m);
 cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t r_count,
                                 void* scratch, size_t scratch_bytes, unsigned long long* counters,
                                 int* counts, long long* lins, int* ties, int sms, cudaStream_t st);
+cudaError_t launch_sparse_histogram(const SparseParams& s, bool dedup, void* scratch,
+                                    size_t scratch_bytes, unsigned long long* counter,
+                                    unsigned long long** out_lins, int** out_counts, int** out_n,
+                                    unsigned long long* nkeys_host, int sms, cudaStream_t st);
 // dses_score.cu
 cudaError_t launch_select_stats(const int* counts, int64_t nrot, unsigned long long* mstar,
                                 unsigned long long* nvalid, int sms, cudaStream_t st);
@@ -779,14 +783,7 @@ int set_grid(dses_plan* P, const dses_grid* g, RotSource* rs, cudaStream_t st) {
   return DSES_OK;
 }
 
-int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
-  CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
-  CK(P->lins64.ensure(sizeof(long long) * std::max<int64_t>(r_count, 1)));
-  CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
-  P->cur_r_begin = r_begin;
-  P->cur_r_count = r_count;
-  P->cur_rot = rs;
-  if (r_count <= 0) return DSES_OK;
+static SparseParams sparse_params(const dses_plan* P, const RotSource& rs) {
   SparseParams sp{};
   sp.n = (int)P->n;
   sp.m = (int)P->m;
@@ -798,6 +795,18 @@ int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_cou
   sp.d1 = P->dims[1];
   sp.d2 = P->dims[2];
   sp.rot = rs;
+  return sp;
+}
+
+int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
+  CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  CK(P->lins64.ensure(sizeof(long long) * std::max<int64_t>(r_count, 1)));
+  CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  P->cur_r_begin = r_begin;
+  P->cur_r_count = r_count;
+  P->cur_rot = rs;
+  if (r_count <= 0) return DSES_OK;
+  const SparseParams sp = sparse_params(P, rs);
   const size_t sb = sparse_scratch_bytes(P->n, P->m);
   CK(P->sparse_scratch.ensure(sb));
   CK(P->scal.ensure(64));
@@ -1017,6 +1026,46 @@ extern "C" int dses_mode_dense_batch(int device, const double* rots, int64_t nro
   rc = dses_mode_batch(P, rots, nrot, counts, lins, ties, nullptr);
   dses_plan_destroy(P);
   return rc;
+}
+
+extern "C" int dses_translation_histogram(dses_plan* P, const double* rot, int dedup,
+                                          int64_t* lins, int64_t* counts, int64_t cap,
+                                          int64_t* nbins, int64_t* npairs, void* stream) {
+  TrafficScope ts_(P);
+  if (!P || !rot || !nbins || cap < 0 || (cap > 0 && (!lins || !counts)))
+    return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(P->rots.ensure(sizeof(double) * 9));
+  CK(h2d(P->rots.p, rot, sizeof(double) * 9, st));
+  RotSource rs{};
+  rs.rots = P->rots.as<double>();
+  const SparseParams sp = sparse_params(P, rs);
+  CK(P->sparse_scratch.ensure(sparse_scratch_bytes(P->n, P->m)));
+  CK(P->scal.ensure(64));
+  unsigned long long* dl = nullptr;
+  int *dc = nullptr, *dn = nullptr;
+  unsigned long long nk = 0;
+  CK(launched(launch_sparse_histogram(sp, dedup != 0, P->sparse_scratch.p, P->sparse_scratch.cap,
+                                      P->scal.as<unsigned long long>() + 6, &dl, &dc, &dn, &nk,
+                                      P->sms, st),
+              dedup ? 5 : 4));
+  int nr = 0;
+  CK(d2h(&nr, dn, sizeof nr, st));
+  *nbins = nr;
+  if (npairs) *npairs = (int64_t)nk;
+  if (nr > cap) return fail(DSES_E_INVALID, "histogram has more bins than cap");
+  std::vector<unsigned long long> hl(nr);
+  std::vector<int> hc(nr);
+  if (nr > 0) {
+    CK(d2h(hl.data(), dl, sizeof(unsigned long long) * nr, st));
+    CK(d2h(hc.data(), dc, sizeof(int) * nr, st));
+  }
+  for (int k = 0; k < nr; ++k) {
+    lins[k] = (int64_t)hl[k];
+    counts[k] = hc[k];
+  }
+  return DSES_OK;
 }
 
 extern "C" int dses_refine_batch(dses_plan* P, const double* rots, const double* ts, int64_t ncand,

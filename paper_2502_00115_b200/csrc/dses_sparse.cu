@@ -68,10 +68,10 @@ __global__ void sparse_keys_kernel(SparseParams s, int64_t r, unsigned long long
   }
 }
 
-__global__ void keys_to_lins_kernel(const unsigned long long* ukeys, const int* nunique, int n,
+__global__ void keys_to_lins_kernel(const unsigned long long* ukeys, int64_t count, int n,
                                     unsigned long long* lins) {
-  const int u = *nunique;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < u; k += gridDim.x * blockDim.x)
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+       k += (int64_t)gridDim.x * blockDim.x)
     lins[k] = ukeys[k] / (unsigned long long)n;
 }
 
@@ -180,7 +180,7 @@ cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t 
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
     keys_to_lins_kernel<<<std::max(1, std::min(sms * 8, (nu + 255) / 256)), 256, 0, st>>>(
-        ukeys, nunique, s.n, ulins);
+        ukeys, nu, s.n, ulins);
     // runs over the (sorted) unique lins; RLE writes the run lins into `sorted`
     tb = temp_bytes;
     e = cub::DeviceRunLengthEncode::Encode(temp, tb, ulins, sorted, runlen, nruns, (int64_t)nu, st);
@@ -190,6 +190,66 @@ cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t 
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// The full vote map of one rotation (mode_search.translation_histogram,
+// mode_search.py:205-235): keys of rotation 0 of `s.rot` sorted, deduplicated
+// per (bin, source) when `dedup`, run-length encoded by bin.  Outputs live in
+// the scratch: *out_lins (ascending flat bins, u64), *out_counts (int32) and
+// *out_n (device int, number of bins); *nkeys_host = pairs in the lattice.
+cudaError_t launch_sparse_histogram(const SparseParams& s, bool dedup, void* scratch,
+                                    size_t scratch_bytes, unsigned long long* counter,
+                                    unsigned long long** out_lins, int** out_counts, int** out_n,
+                                    unsigned long long* nkeys_host, int sms, cudaStream_t st) {
+  const size_t k = (size_t)((int64_t)s.n * s.m);
+  auto align = [](size_t v) { return (v + 255) & ~size_t(255); };
+  unsigned char* base = static_cast<unsigned char*>(scratch);
+  size_t off = 0;
+  auto* keys = reinterpret_cast<unsigned long long*>(base + off); off = align(off + k * 8);
+  auto* sorted = reinterpret_cast<unsigned long long*>(base + off); off = align(off + k * 8);
+  auto* ukeys = reinterpret_cast<unsigned long long*>(base + off); off = align(off + k * 8);
+  auto* ulins = reinterpret_cast<unsigned long long*>(base + off); off = align(off + k * 8);
+  auto* runlen = reinterpret_cast<int*>(base + off); off = align(off + k * 4);
+  int* nunique = reinterpret_cast<int*>(base + off); off = align(off + 16);
+  int* nruns = nunique + 1;
+  void* temp = base + off;
+  const size_t temp_bytes = scratch_bytes > off ? scratch_bytes - off : 0;
+  *out_lins = keys;  // free once the keys are sorted
+  *out_counts = runlen;
+  *out_n = nruns;
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(nruns, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  const int blocks = (int)std::min<int64_t>((int64_t)sms * 8, ((int64_t)k + 255) / 256);
+  sparse_keys_kernel<<<std::max(blocks, 1), 256, 0, st>>>(s, 0, keys, counter);
+  unsigned long long nk = 0;
+  e = cudaMemcpyAsync(&nk, counter, sizeof nk, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  *nkeys_host = nk;
+  if (nk == 0) return cudaSuccess;
+  size_t tb = temp_bytes;
+  e = cub::DeviceRadixSort::SortKeys(temp, tb, keys, sorted, (int64_t)nk, 0, 64, st);
+  if (e != cudaSuccess) return e;
+  const unsigned long long* src = sorted;
+  int64_t count = (int64_t)nk;
+  if (dedup) {
+    tb = temp_bytes;
+    e = cub::DeviceSelect::Unique(temp, tb, sorted, ukeys, nunique, (int64_t)nk, st);
+    if (e != cudaSuccess) return e;
+    int nu = 0;
+    e = cudaMemcpyAsync(&nu, nunique, sizeof nu, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    src = ukeys;
+    count = nu;
+  }
+  keys_to_lins_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, (count + 255) / 256)),
+                        256, 0, st>>>(src, count, s.n, ulins);
+  tb = temp_bytes;
+  e = cub::DeviceRunLengthEncode::Encode(temp, tb, ulins, keys, runlen, nruns, count, st);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 }  // namespace dses

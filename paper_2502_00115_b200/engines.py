@@ -265,3 +265,41 @@ def exhaustive_search(source, reference, cfg: SearchConfig, device: int = 0) -> 
                               elapsed={"search": total, "total": total,
                                        "device_total": res["ms_total"] * 1e-3,
                                        "rescored": res["rescored"]})
+
+
+CUTOFF_EPS = 1e-9  # engines.py:_CUTOFF_EPS
+
+
+def refine_cutoff(counts_desc, q: float) -> int:
+    """Length of the re-scored prefix of a count-descending list: every entry
+    with count >= q * best - 1e-9, at least one (engines.py:196-201)."""
+    cutoff = q * counts_desc[0] - CUTOFF_EPS
+    return max(1, int(np.searchsorted(-np.asarray(counts_desc, dtype=np.float64), -cutoff,
+                                      side="right")))
+
+
+def refine_candidates(candidates, source, reference, metric: ErrorMetric, q: float,
+                      device: int = 0):
+    """Re-score the high-vote prefix of a count-sorted candidate list
+    (engines.py:204-226): the candidates with inlier_count >= q * best get
+    refined_error from the exact binary64 refine kernel (dses_refine_batch),
+    the rest are returned unchanged."""
+    from dataclasses import replace
+
+    from .metrics import _pose_errors
+    if not candidates:
+        raise InvalidInputError("candidate list is empty")
+    if not (0.0 < q <= 1.0):
+        raise InvalidInputError("q must lie in (0, 1]")
+    counts = [c.inlier_count for c in candidates]
+    if any(counts[i] < counts[i + 1] for i in range(len(counts) - 1)):
+        raise InvalidInputError("candidates must be sorted by inlier_count descending")
+    x = as_point_cloud(source)
+    y = as_point_cloud(reference)
+    n_score = refine_cutoff(counts, q)
+    rots = np.stack([c.transform.rotation for c in candidates[:n_score]])
+    ts = np.stack([c.transform.translation for c in candidates[:n_score]])
+    errs = _pose_errors(x, y, rots, ts, metric, device)
+    out = [replace(c, refined_error=float(e)) for c, e in zip(candidates[:n_score], errs)]
+    out.extend(candidates[n_score:])
+    return out

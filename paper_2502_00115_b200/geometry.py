@@ -145,6 +145,26 @@ def apply_transform(transform: RigidTransform, points) -> np.ndarray:
     return transform.apply(points)
 
 
+def compose(a: RigidTransform, b: RigidTransform) -> RigidTransform:
+    """a after b (geometry.py:225-227)."""
+    return a.compose(b)
+
+
+def wrap_angle(a):
+    """Angles wrapped to [-pi, pi) (geometry.py:80-82)."""
+    return (np.asarray(a) + np.pi) % (2.0 * np.pi) - np.pi
+
+
+def random_rotation(rng: np.random.Generator) -> np.ndarray:
+    """Uniformly distributed rotation from a normalised Gaussian quaternion
+    (geometry.py:307-318; same draws, same matrix)."""
+    q = rng.standard_normal(4)
+    w, a, b, c = q / np.linalg.norm(q)
+    return np.array([[1 - 2 * (b * b + c * c), 2 * (a * b - w * c), 2 * (a * c + w * b)],
+                     [2 * (a * b + w * c), 1 - 2 * (a * a + c * c), 2 * (b * c - w * a)],
+                     [2 * (a * c - w * b), 2 * (b * c + w * a), 1 - 2 * (a * a + b * b)]])
+
+
 def check_grid_args(half_width, step):
     """Validation of build_rotation_grid (geometry.py:259-267)."""
     k = int(half_width)

@@ -2,10 +2,13 @@
 
 Drop-in for gridreg/mode_search.py: ``bin_index``/``bin_center`` (40-54),
 ``_decode_flat`` (167-171), the window helpers (101-129), ``ModeResult`` and
-``mode_translation`` (174-202).  The vote itself runs on the B200 vote kernel
-(csrc/dses_vote.cu) for any lattice size: dense shared-memory histograms when
-they fit, per-CTA global-memory histograms beyond that (the reference's
-sparse path, _kernels.py:196-294, returns the same triple).
+``mode_translation`` (174-202), ``TranslationHistogram`` /
+``translation_histogram`` (74-99, 205-235).  The mode runs on the B200 vote
+kernel (csrc/dses_vote.cu) for any lattice size: dense shared-memory
+histograms when they fit, per-CTA global-memory histograms beyond that, the
+sort-based path (csrc/dses_sparse.cu, the reference's sparse algorithm
+_kernels.py:196-294) for huge lattices; the full vote map is the sort-based
+path's run-length encoding.
 """
 from __future__ import annotations
 
@@ -112,3 +115,53 @@ def mode_translation(source, reference, rotation, bin_size: float, t_bounds=None
     idx = decode_flat(lins[0], ilo, dims)
     return ModeResult(t_star=bin_center(idx, bin_size), count=int(counts[0]),
                       num_tied_bins=int(ties[0]), index=idx)
+
+
+@dataclass(frozen=True)
+class TranslationHistogram:
+    """Sparse vote map {bin index triple: count} (mode_search.py:74-99);
+    counts are distinct source points per bin with dedup, raw pair votes
+    without (then total = N*M when unbounded)."""
+    bin_size: float
+    counts: dict
+    total: int
+    dedup: bool
+
+    def mode(self) -> ModeResult:
+        if not self.counts:
+            raise NoCandidateError("histogram is empty")
+        best = max(self.counts.values())
+        tied = sorted(k for k, c in self.counts.items() if c == best)
+        return ModeResult(t_star=bin_center(tied[0], self.bin_size), count=int(best),
+                          num_tied_bins=len(tied), index=tied[0])
+
+
+def translation_histogram(source, reference, rotation, bin_size: float, t_bounds=None,
+                          dedup: bool = True, device: int = 0) -> TranslationHistogram:
+    """Full vote map of one rotation on the GPU (mode_search.py:205-235): every
+    pair's bin (binary64, the vote kernel's operation order) inside the
+    lattice -- t_bounds' bins, or all of them -- sorted, deduplicated per
+    source when `dedup`, run-length encoded (csrc/dses_sparse.cu)."""
+    from . import _native
+
+    x = as_point_cloud(source)
+    y = as_point_cloud(reference)
+    rot = np.asarray(rotation, dtype=np.float64)
+    check_rotation(rot)
+    if not (bin_size > 0) or not np.isfinite(bin_size):
+        raise InvalidInputError("bin_size must be positive and finite")
+    if t_bounds is None:
+        ilo, ihi = data_index_range(x, y, bin_size)
+    else:
+        ilo, ihi = bounds_to_index_range(t_bounds, bin_size)
+    dims = ihi - ilo + 1
+    check_key_space(int(np.prod(dims.astype(object))), x.shape[0])
+    with _native.Plan(x, y, bin_size, ilo, dims, device) as plan:
+        lins, counts, _ = plan.histogram(rot.reshape(9), dedup)
+    d12 = int(dims[1]) * int(dims[2])
+    a, rem = np.divmod(lins, d12)
+    b, c = np.divmod(rem, int(dims[2]))
+    idx = np.stack([a + ilo[0], b + ilo[1], c + ilo[2]], axis=1)
+    table = {(int(i0), int(i1), int(i2)): int(k) for (i0, i1, i2), k in zip(idx.tolist(), counts)}
+    return TranslationHistogram(bin_size=float(bin_size), counts=table, total=int(counts.sum()),
+                                dedup=bool(dedup))

@@ -312,8 +312,132 @@ def make_harness():
     save("harness", rec)
 
 
+from make_golden_records import BATCHIO_RECORDS, SEARCH_JSON_CASES  # noqa: E402
+
+
+def make_batchio():
+    """harness.write_batch_csv / write_batch_json / search_to_dict /
+    search_from_json outputs for fixed records and config files."""
+    import json
+    import tempfile
+    from gridreg import harness
+    from gridreg.metrics import EvalReport
+
+    recs = []
+    for d in BATCHIO_RECORDS:
+        e = d["eval"]
+        ev = None if e is None else EvalReport(mie_r=e[0], mie_t=e[1], mae_r=e[2], mae_t=e[3],
+                                                is_recall_hit=e[4], chamfer=e[5])
+        recs.append(harness.TrialRecord(**dict(d, eval=ev)))
+    summary = harness._summarize(recs)
+    search = SearchConfig(k_rot=3, rot_step=math.radians(2.0), k_trans=8, trans_bin=0.02,
+                          metric=ErrorMetric.from_name("trunc-l1", 0.02, 0.05),
+                          center=geometry.RigidTransform(np.eye(3), np.array([0.5, 0.0, -0.25])))
+    scenario = benchgen.ScenarioConfig(shape="blob", rng_seed=100)
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        harness.write_batch_csv(os.path.join(tmp, "b.csv"), recs)
+        harness.write_batch_json(os.path.join(tmp, "b.json"), scenario, search, summary, recs,
+                                 extra={"note": "golden"})
+        out["csv"] = open(os.path.join(tmp, "b.csv"), encoding="utf-8").read()
+        out["json"] = open(os.path.join(tmp, "b.json"), encoding="utf-8").read()
+        parsed = []
+        for k, case in enumerate(SEARCH_JSON_CASES):
+            path = os.path.join(tmp, f"s{k}.json")
+            with open(path, "w", encoding="utf-8") as fh:
+                json.dump(case, fh)
+            try:
+                cfg = harness.search_from_json(path)
+                parsed.append({"ok": harness.search_to_dict(cfg)})
+            except Exception as exc:  # noqa: BLE001
+                parsed.append({"error": type(exc).__name__, "message": str(exc)})
+    out["scenario"] = json.loads(json.dumps(harness.asdict(scenario)))
+    out["search_to_dict"] = harness.search_to_dict(search)
+    out["search_cases"] = parsed
+    rec = {"batchio": np.array(json.dumps(out, sort_keys=True))}
+    save("batchio", rec)
+
+
+def _seq_bins_agree(x, y, rot, b):
+    """True when numpy's BLAS product gives the same pair bins as the vote
+    kernels' sequential binary64 order (then both define the same map)."""
+    p_blas = x @ rot.T
+    p_seq = np.empty_like(p_blas)
+    for k in range(3):
+        p_seq[:, k] = (rot[k, 0] * x[:, 0] + rot[k, 1] * x[:, 1]) + rot[k, 2] * x[:, 2]
+    c1 = (y[None] - p_blas[:, None]).reshape(-1, 3)
+    c2 = (y[None] - p_seq[:, None]).reshape(-1, 3)
+    return np.array_equal(mode_search.bin_index(c1, b), mode_search.bin_index(c2, b))
+
+
+def make_histo():
+    """mode_search.translation_histogram (+ .mode()) and
+    engines.refine_candidates on small clouds."""
+    rec = {}
+    cases = []
+    rng = np.random.default_rng(77)
+    for k in range(6):
+        n, m = [(40, 60), (64, 64), (30, 90), (50, 50), (20, 40), (45, 70)][k]
+        while True:
+            x = rng.normal(scale=0.2, size=(n, 3))
+            h = min(n, m // 2)
+            y = np.concatenate([x[:h] + rng.normal(scale=0.01, size=(h, 3)),
+                                rng.normal(scale=0.2, size=(m - h, 3))])
+            if k == 3:  # duplicated reference points: dedup matters
+                y[h:] = y[: m - h]
+            if k == 4:  # permutation rotation (exact products)
+                rot = np.array([[0.0, 1.0, 0.0], [0.0, 0.0, -1.0], [-1.0, 0.0, 0.0]])
+            else:
+                rot = geometry.rotation_from_euler(rng.uniform(-0.5, 0.5, 3))
+            b = [0.05, 0.03, 0.1, 0.05, 0.04, 0.02][k]
+            if _seq_bins_agree(x, y, rot, b):
+                break
+        bounds = None
+        if k in (1, 5):
+            bounds = np.array([[-0.2, -0.15, -0.3], [0.25, 0.2, 0.1]])
+        cases.append((x, y, rot, b, bounds))
+    # bounds with no pair inside: empty histogram, mode() raises
+    x, y, rot, b, _ = cases[0]
+    cases.append((x, y, rot, b, np.array([[50.0, 50.0, 50.0], [50.2, 50.2, 50.2]])))
+    for k, (x, y, rot, b, bounds) in enumerate(cases):
+        p = f"t{k}"
+        rec[f"{p}_x"], rec[f"{p}_y"], rec[f"{p}_rot"], rec[f"{p}_bin"] = x, y, rot, np.float64(b)
+        if bounds is not None:
+            rec[f"{p}_bounds"] = bounds
+        for dedup in (True, False):
+            h = mode_search.translation_histogram(x, y, rot, b, t_bounds=bounds, dedup=dedup)
+            q = f"{p}_{'d' if dedup else 'r'}"
+            keys = sorted(h.counts)
+            rec[f"{q}_keys"] = np.array(keys, dtype=np.int64).reshape(-1, 3)
+            rec[f"{q}_vals"] = np.array([h.counts[kk] for kk in keys], dtype=np.int64)
+            rec[f"{q}_total"] = np.int64(h.total)
+            if h.counts:
+                md = h.mode()
+                rec[f"{q}_mode"] = np.array([*md.index, md.count, md.num_tied_bins], dtype=np.int64)
+        print(f"  {p}: {len(h.counts)} raw bins, total {h.total}")
+    rec["n_histo_cases"] = np.int64(len(cases))
+    # refine_candidates: a count-sorted list of poses on the c1 pair
+    x, y = cases[1][0], cases[1][1]
+    cands = []
+    for j, cnt in enumerate([30, 30, 22, 16, 15, 9, 3]):
+        r = geometry.rotation_from_euler(rng.uniform(-0.3, 0.3, 3))
+        t = rng.normal(scale=0.05, size=3)
+        cands.append(engines.PoseCandidate(transform=geometry.RigidTransform(r, t), inlier_count=cnt))
+        rec[f"rc_R{j}"], rec[f"rc_t{j}"] = r, t
+    rec["rc_counts"] = np.array([c.inlier_count for c in cands], dtype=np.int64)
+    rec["rc_x"], rec["rc_y"] = x, y
+    for mname, metric in (("l1", ErrorMetric.l1()), ("tl1", ErrorMetric.truncated_l1(0.05)),
+                          ("l2", ErrorMetric.l2()), ("sat", ErrorMetric.saturated_l0(0.03))):
+        for q in (0.5, 0.75, 1.0):
+            out = engines.refine_candidates(cands, x, y, metric, q)
+            rec[f"rc_{mname}_{int(q * 100)}"] = np.array(
+                [np.nan if c.refined_error is None else c.refined_error for c in out])
+    save("histo", rec)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "exh", "harness"]
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "exh", "harness", "batchio",
+                             "histo"]
     for w in which:
         print(w)
         globals()[f"make_{w}"]()
