@@ -99,6 +99,14 @@ class ClockSampler:
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+            return self
+        # nvidia-smi's start-up (NVML init) must not overlap the timed steps:
+        # wait for its first sample before the caller starts timing
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and self.proc.poll() is None:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.01)
         return self
 
     def __exit__(self, *exc):
@@ -413,8 +421,10 @@ def main():
     value = args.steps * R * world / (ms_max * 1e-3)
 
     # ---- end to end through the public API with host buffers
-    e2e_pairs = [make_pair(c["spec"], 1000 * rank + 500 + s) for s in range(args.steps)]
-    dses(e2e_pairs[0][0], e2e_pairs[0][1], cfg, device=local)  # warm
+    # the same host pairs as the timed device-resident steps, so that e2e -
+    # value is exactly the host-side cost (validation, plan build, copies)
+    e2e_pairs = pairs[args.warmup:]
+    dses(pairs[0][0], pairs[0][1], cfg, device=local)  # warm
     torch.cuda.synchronize()
     e_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -439,7 +449,7 @@ def main():
     # ---- end to end, batched: dses_batch over the same host pairs (plan
     #      construction of pair k+1 on a host thread overlaps the search of k)
     from paper_2502_00115_b200 import dses_batch
-    dses_batch([p[0] for p in e2e_pairs[:2]], [p[1] for p in e2e_pairs[:2]], cfg, device=local)
+    dses_batch([p[0] for p in pairs[:2]], [p[1] for p in pairs[:2]], cfg, device=local)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
