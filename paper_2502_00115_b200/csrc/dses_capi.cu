@@ -849,6 +849,7 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
     }
   }
   CK(cudaEventRecord(P->ev[5], st));
+  CK(cudaMemsetAsync(v.stats + 3, 0, sizeof(unsigned long long), st));  // rotation queue
   CK(launched(launch_vote(v, P->hsmem, P->psmem, grid, P->vote_threads, st)));
   CK(cudaEventRecord(P->ev[6], st));
   P->vote_timed = true;

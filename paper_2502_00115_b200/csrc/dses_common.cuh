@@ -111,7 +111,7 @@ struct VoteParams {
   int* counts;
   int* lins;
   int* ties;
-  unsigned long long* stats;  // [pairs, votes, rechecks]
+  unsigned long long* stats;  // [pairs, votes, rechecks, rotation counter (zeroed per launch)]
   // global fallbacks when the histogram / rotated points do not fit shared memory
   unsigned* hist_global;      // per-CTA slabs of hist_words (u32 counts when !count16)
   int4* p_global;             // per-CTA slabs of n_pad entries

@@ -35,6 +35,9 @@
 #define DSES_NS4 0  // four source points per slot (measured slower at 768 threads)
 #endif
 
+#ifndef DSES_DYNROT
+#define DSES_DYNROT 1  // rotations claimed from a global queue
+#endif
 #ifndef DSES_CHUNKBOX
 #define DSES_CHUNKBOX 1
 #endif
@@ -332,7 +335,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   // reference groups per round so that the round's units fit `units`
   const int tiles_per_round = max(1, p.unit_cap / max(1, p.nxt));
 
-  for (int64_t rr = blockIdx.x; rr < p.r_count; rr += gridDim.x) {
+  // rotations: the first one static, the rest from a global queue (the cost
+  // of a rotation varies with its angle; dynamic claims balance the tail)
+  __shared__ long long s_rr;
+  for (int64_t rr = blockIdx.x; rr < p.r_count;) {
     const int64_t r = p.r_begin + rr;
     if (tid < 9) R[tid] = rotation_entry(p.rot, r, tid);
     __syncthreads();
@@ -537,9 +543,12 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         p.counts[rr] = best;
         p.lins[rr] = best > 0 ? blin : -1;
         p.ties[rr] = best > 0 ? bties : 0;
+        s_rr = DSES_DYNROT ? (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull)
+                           : rr + gridDim.x;
       }
     }
     __syncthreads();
+    rr = s_rr;
   }
 
   // kernel statistics
