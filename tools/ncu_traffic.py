@@ -18,7 +18,7 @@ def main(rep, out, what):
 
     def val(k):
         v = float(d[k].replace(",", ""))
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "usecond": 1e-3,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "nsecond": 1e-6, "usecond": 1e-3, "us": 1e-3, "ms": 1.0,
                  "msecond": 1.0, "%": 1.0, "": 1.0}.get(u.get(k, ""), 1.0)
         return v * scale
 
