@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <thread>
 #include <cstring>
 #include <future>
 #include <limits>
@@ -279,7 +280,7 @@ inline int64_t rint64(double v) { return (int64_t)std::llrint(v); }
 // recursive median split until tiles hold <= kTile points; splits at a
 // multiple of kTile so that all but the last tile of each branch are full.
 void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
-              std::vector<std::pair<int, int>>& tiles, int tile) {
+              std::vector<std::pair<int, int>>& tiles, int tile, int spawn = 0) {
   const int64_t cnt = hi - lo;
   if (cnt <= tile) {
     if (cnt > 0) tiles.emplace_back((int)lo, (int)cnt);
@@ -301,6 +302,15 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
                      const double va = pts[3 * a + axis], vb = pts[3 * b + axis];
                      return va < vb || (va == vb && a < b);
                    });
+  if (spawn > 0 && cnt >= 4096) {  // disjoint halves: left on a helper thread
+    std::vector<std::pair<int, int>> lt, rt;
+    std::thread th([&] { kd_tiles(pts, lo, lo + left, perm, lt, tile, spawn - 1); });
+    kd_tiles(pts, lo + left, hi, perm, rt, tile, spawn - 1);
+    th.join();
+    tiles.insert(tiles.end(), lt.begin(), lt.end());
+    tiles.insert(tiles.end(), rt.begin(), rt.end());
+    return;
+  }
   kd_tiles(pts, lo, lo + left, perm, tiles, tile);
   kd_tiles(pts, lo + left, hi, perm, tiles, tile);
 }
@@ -312,7 +322,7 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
 // split again.
 void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int64_t hi,
                  std::vector<int>& perm, std::vector<std::pair<int, int>>& tiles, int cap,
-                 int64_t leaves) {
+                 int64_t leaves, int spawn = 0) {
   int64_t W = 0;
   for (int64_t q = lo; q < hi; ++q) W += wt[perm[q]];
   leaves = std::max<int64_t>(leaves, (W + cap - 1) / cap);
@@ -359,6 +369,16 @@ void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int6
       while (s < hi - 1 && s < s + k && wl + wt[perm[s]] <= target) wl += wt[perm[s++]];
     }
   }
+  if (spawn > 0 && hi - lo >= 4096) {  // disjoint halves: left on a helper thread
+    std::vector<std::pair<int, int>> left;
+    std::thread th([&] { kd_weighted(cen, wt, lo, s, perm, left, cap, lleaves, spawn - 1); });
+    std::vector<std::pair<int, int>> right;
+    kd_weighted(cen, wt, s, hi, perm, right, cap, leaves - lleaves, spawn - 1);
+    th.join();
+    tiles.insert(tiles.end(), left.begin(), left.end());
+    tiles.insert(tiles.end(), right.begin(), right.end());
+    return;
+  }
   kd_weighted(cen, wt, lo, s, perm, tiles, cap, lleaves);
   kd_weighted(cen, wt, s, hi, perm, tiles, cap, leaves - lleaves);
 }
@@ -368,44 +388,101 @@ void kd_weighted(const double* cen, const std::vector<int>& wt, int64_t lo, int6
 // sorted by axis 1 inside each strip; a point's partners lie in its own strip
 // (later in axis-1 order) or in the next strip (an axis-1 window found by
 // binary search), so each pair is found once.
+// host threads for plan construction of large clouds (at most 8)
+static int host_threads() {
+  static const int n = [] {
+    const unsigned h = std::thread::hardware_concurrency();
+    return (int)std::max(1u, std::min(8u, h));
+  }();
+  return n;
+}
+
 std::vector<std::pair<int, int>> near_pairs(const double* y, int64_t m, double thr) {
   double mn0 = INFINITY;
   for (int64_t j = 0; j < m; ++j) mn0 = std::min(mn0, y[3 * j]);
   const double width = thr * (1.0 + 1e-9);  // partners are never two strips apart
   struct Key { int64_t strip; double y1; int idx; };
-  std::vector<Key> keys(m);
-  for (int64_t j = 0; j < m; ++j)
-    keys[j] = {(int64_t)std::floor((y[3 * j] - mn0) / width), y[3 * j + 1], (int)j};
-  std::sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
-    if (a.strip != b.strip) return a.strip < b.strip;
+  auto by_y1 = [](const Key& a, const Key& b) {
     return a.y1 < b.y1 || (a.y1 == b.y1 && a.idx < b.idx);
-  });
+  };
+  std::vector<Key> keys(m);
+  int64_t smax = 0;
+  for (int64_t j = 0; j < m; ++j) {
+    keys[j] = {(int64_t)std::floor((y[3 * j] - mn0) / width), y[3 * j + 1], (int)j};
+    smax = std::max(smax, keys[j].strip);
+  }
+  if (smax <= 4 * m + 1024) {
+    // counting sort by strip, then each strip by (y1, index) -- strips over
+    // host threads for large clouds
+    std::vector<int64_t> so(smax + 2, 0);
+    for (const Key& k : keys) ++so[k.strip + 1];
+    for (int64_t t = 0; t <= smax; ++t) so[t + 1] += so[t];
+    std::vector<Key> sorted(m);
+    {
+      std::vector<int64_t> fill(so.begin(), so.end() - 1);
+      for (const Key& k : keys) sorted[fill[k.strip]++] = k;
+    }
+    keys.swap(sorted);
+    auto sort_strips = [&](int64_t t0, int64_t t1) {
+      for (int64_t t = t0; t < t1; ++t)
+        if (so[t + 1] - so[t] > 1) std::sort(keys.begin() + so[t], keys.begin() + so[t + 1], by_y1);
+    };
+    const int nt = m >= 8192 ? host_threads() : 1;
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t)
+      pool.emplace_back(sort_strips, (smax + 1) * t / nt, (smax + 1) * (t + 1) / nt);
+    sort_strips(0, (smax + 1) / nt);
+    for (auto& th : pool) th.join();
+  } else {
+    std::sort(keys.begin(), keys.end(), [&](const Key& a, const Key& b) {
+      return a.strip != b.strip ? a.strip < b.strip : by_y1(a, b);
+    });
+  }
   auto close = [&](int a, int b) {
     return std::fabs(y[3 * a] - y[3 * b]) < thr && std::fabs(y[3 * a + 1] - y[3 * b + 1]) < thr &&
            std::fabs(y[3 * a + 2] - y[3 * b + 2]) < thr;
   };
-  std::vector<std::pair<int, int>> out;
-  for (int64_t p = 0; p < m;) {
-    const int64_t sp = keys[p].strip;
-    int64_t e = p;
-    while (e < m && keys[e].strip == sp) ++e;  // current strip [p, e)
-    int64_t ne = e;
-    while (ne < m && keys[ne].strip == sp + 1) ++ne;  // next strip [e, ne)
-    for (int64_t q = p; q < e; ++q) {
-      const int a = keys[q].idx;
-      const double y1 = keys[q].y1;
-      for (int64_t r = q + 1; r < e && keys[r].y1 - y1 < thr; ++r)
-        if (close(a, keys[r].idx)) out.emplace_back(a, keys[r].idx);
-      int64_t lo = e, hi2 = ne;  // next strip: axis-1 window (y1 - thr, y1 + thr)
-      while (lo < hi2) {
-        const int64_t mid = (lo + hi2) / 2;
-        if (keys[mid].y1 <= y1 - thr) lo = mid + 1; else hi2 = mid;
+  // strips [p, e) scanned against themselves and the next strip; large
+  // clouds split the key range at strip boundaries over host threads and
+  // concatenate in key order (the same pair order as one thread)
+  auto scan = [&](int64_t p, int64_t end, std::vector<std::pair<int, int>>& out) {
+    while (p < end) {
+      const int64_t sp = keys[p].strip;
+      int64_t e = p;
+      while (e < m && keys[e].strip == sp) ++e;  // current strip [p, e)
+      int64_t ne = e;
+      while (ne < m && keys[ne].strip == sp + 1) ++ne;  // next strip [e, ne)
+      for (int64_t q = p; q < e; ++q) {
+        const int a = keys[q].idx;
+        const double y1 = keys[q].y1;
+        for (int64_t r = q + 1; r < e && keys[r].y1 - y1 < thr; ++r)
+          if (close(a, keys[r].idx)) out.emplace_back(a, keys[r].idx);
+        int64_t lo = e, hi2 = ne;  // next strip: axis-1 window (y1 - thr, y1 + thr)
+        while (lo < hi2) {
+          const int64_t mid = (lo + hi2) / 2;
+          if (keys[mid].y1 <= y1 - thr) lo = mid + 1; else hi2 = mid;
+        }
+        for (int64_t r = lo; r < ne && keys[r].y1 - y1 < thr; ++r)
+          if (close(a, keys[r].idx)) out.emplace_back(a, keys[r].idx);
       }
-      for (int64_t r = lo; r < ne && keys[r].y1 - y1 < thr; ++r)
-        if (close(a, keys[r].idx)) out.emplace_back(a, keys[r].idx);
+      p = e;
     }
-    p = e;
+  };
+  const int nt = m >= 8192 ? host_threads() : 1;
+  std::vector<int64_t> cut(nt + 1, m);
+  cut[0] = 0;
+  for (int t = 1; t < nt; ++t) {  // chunk starts moved forward to a strip boundary
+    int64_t c = std::max(cut[t - 1], m * t / nt);
+    while (c > 0 && c < m && keys[c].strip == keys[c - 1].strip) ++c;
+    cut[t] = c;
   }
+  std::vector<std::vector<std::pair<int, int>>> parts(nt);
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(scan, cut[t], cut[t + 1], std::ref(parts[t]));
+  scan(cut[0], cut[1], parts[0]);
+  for (auto& th : pool) th.join();
+  std::vector<std::pair<int, int>> out = std::move(parts[0]);
+  for (int t = 1; t < nt; ++t) out.insert(out.end(), parts[t].begin(), parts[t].end());
   return out;
 }
 
@@ -507,7 +584,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   std::vector<int> px(n);
   std::iota(px.begin(), px.end(), 0);
   std::vector<std::pair<int, int>> tx;
-  kd_tiles(x, 0, n, px, tx, kTile);  // source units
+  kd_tiles(x, 0, n, px, tx, kTile, host_threads() >= 4 ? 2 : 0);  // source units
   std::vector<double> xs(3 * n);
   for (int64_t i = 0; i < n; ++i)
     for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
@@ -597,7 +674,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   std::vector<std::pair<int, int>> itiles;
   // leaf budget = ceil(total / 32); a looser budget (fewer-filled groups) grew
   // the group boxes more than it saved lanes (experiments)
-  kd_weighted(cen.data(), wt, 0, (int64_t)nitems, iperm, itiles, kTile, 0);
+  kd_weighted(cen.data(), wt, 0, (int64_t)nitems, iperm, itiles, kTile, 0,
+              host_threads() >= 8 ? 3 : host_threads() >= 4 ? 2 : 0);
   trace("  component k-d tiles");
   std::vector<int> yidx;  // tile-order entry -> original reference index
   std::vector<char> yfar;
