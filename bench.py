@@ -5,9 +5,12 @@
 
 One step = one full DSES registration (phase 1 vote over every grid rotation,
 phase 2 selection, phase 3 screen + exact re-score, winner inlier count) of one
-synthetic ModelNet40-shaped pair.  Default workload = BASELINE.json configs[1]
+ModelNet40-shaped pair.  Default workload = BASELINE.json configs[1]
 (SURVEY.md 8(d) c2): 1024-pt reference / 717-pt partial, k_rot=15 @ 3 deg
 (29,791 rotations), k_trans=20 @ 25 mm (41^3 bins), truncated-L1 at 5 bins.
+Inputs (--inputs benchgen, the default): the reference generator's own clouds
+for seeds 0..15 (SURVEY.md 8(d)), committed as bench_data/benchgen_<cfg>.npz;
+--inputs synth uses the independent generator paper_2502_00115_b200/synth.py.
 
 Under torchrun every rank registers its own pairs (replicas, weak scaling, no
 data-path collective); the timed region is bracketed by a
@@ -21,7 +24,7 @@ scaling (skip with --no-sharded).
 `--impl reference` times the reference's own CPU implementation on the box's
 host cores, on rank 0 only: the unmodified `gridreg` package (pure Python +
 numba, installed offline into baseline/_ref, every host thread) through its
-public `gridreg.dses` on the same synthetic pair, full registrations when they
+public `gridreg.dses` on the same pair, full registrations when they
 fit the time budget, else `gridreg.mode_search._mode_batch` (phase 1, 99.8% of
 the reference's time) over a contiguous rotation slice.  Without baseline/_ref
 it falls back to the oracle port (oracle/gridreg_oracle.c, the C restatement
@@ -57,6 +60,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="wall-clock budget of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--inputs", default="benchgen", choices=["benchgen", "synth"],
+                    help="clouds: the reference generator's (committed) or synth.py's")
     ap.add_argument("--no-sharded", action="store_true",
                     help="skip the rotation-grid-sharded registration (distributed.dses_sharded)")
     return ap.parse_args()
@@ -68,6 +73,28 @@ def workload(name, metric_override=None):
     if metric_override:
         c["metric"] = metric_override
     return c
+
+
+def bench_pairs(config, count, offset=0, inputs="benchgen"):
+    """`count` (source, reference, truth) pairs of a workload.  "benchgen":
+    the reference generator's own clouds for the listed seeds
+    (bench_data/benchgen_<cfg>.npz, made by bench_data/make_bench_data.py;
+    SURVEY.md 8(d)), cycled when more are needed; configs without a file, or
+    inputs="synth", use the independent generator synth.make_pair."""
+    from paper_2502_00115_b200 import RigidTransform
+    from paper_2502_00115_b200.synth import make_pair
+    path = os.path.join(ROOT, "bench_data", f"benchgen_{config}.npz")
+    if inputs == "benchgen" and os.path.exists(path):
+        d = np.load(path)
+        n = int(d["count"])
+        out = []
+        for s in range(count):
+            k = (offset + s) % n
+            out.append((d[f"x{k}"], d[f"y{k}"], RigidTransform(d[f"gt_R{k}"], d[f"gt_t{k}"])))
+        return out, f"reference benchgen clouds (bench_data/benchgen_{config}.npz, seeds 0..{n - 1})"
+    c = workload(config)
+    return ([make_pair(c["spec"], offset + s) for s in range(count)],
+            "synthetic (seeded ModelNet40-shaped pairs, paper_2502_00115_b200/synth.py)")
 
 
 def search_config(c):
@@ -270,10 +297,9 @@ def run_reference(args):
     if rank != 0:
         return
     sys.path.insert(0, ROOT)
-    from paper_2502_00115_b200.synth import make_pair
     c = workload(args.config, args.metric)
     cfg = search_config(c)
-    x, y, _ = make_pair(c["spec"], 0)
+    (x, y, _), = bench_pairs(args.config, 1, 0, args.inputs)[0]
     ref = load_reference()
     if ref is not None:
         return run_reference_package(args, ref, c, cfg, x, y)
@@ -304,7 +330,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64", "data": bench_pairs(args.config, 1, 0, args.inputs)[1],
         "config": {"workload": describe(args.config, c, cfg, x.shape[0], y.shape[0]),
                    "metric": cfg.metric.kind, "l2_flush": "n/a (CPU)"},
         "registrations_per_sec": value / total,
@@ -349,7 +375,7 @@ def run_reference_package(args, ref, c, cfg, x, y):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64", "data": bench_pairs(args.config, 1, 0, args.inputs)[1],
         "config": {"workload": describe(args.config, c, cfg, x.shape[0], y.shape[0]),
                    "metric": cfg.metric.kind, "l2_flush": "n/a (CPU)"},
         "registrations_per_sec": value / total,
@@ -371,11 +397,10 @@ def sharded_registration(args, rank, world, local, steps=3):
     import torch
     import torch.distributed as dist
     from paper_2502_00115_b200.distributed import dses_sharded
-    from paper_2502_00115_b200.synth import make_pair
     try:
         c = workload("c3")
         cfg = search_config(c)
-        x, y, _ = make_pair(c["spec"], 7)
+        (x, y, _), = bench_pairs("c3", 1, 0, args.inputs)[0]
         dses_sharded(x, y, cfg, device=local)  # warm
         torch.cuda.synchronize()
         if world > 1:
@@ -401,7 +426,7 @@ def sharded_registration(args, rank, world, local, steps=3):
         return {"value": R / (ms * 1e-3), "unit": UNIT, "scaling": "strong", "n_gpus": world,
                 "ms_per_registration": ms, "steps": steps, "rotations": R,
                 "config": "c3: 717-pt noisy partial (+20% outliers) vs 1024-pt cloud, k_rot=45 @ 1 deg, "
-                          "k_trans=20 @ 25 mm, metric l1, seed 7",
+                          "k_trans=20 @ 25 mm, metric l1, pair 0 of --inputs",
                 "collectives": "2 all_gathers per registration (global M*; min (error, row))",
                 "winner_grid": list(res.best.grid_coords), "winner_identical_on_all_ranks": same,
                 "candidates_refined": int(res.candidates_refined)}
@@ -426,12 +451,11 @@ def main():
 
     from paper_2502_00115_b200 import _native, dses
     from paper_2502_00115_b200.engines import prepare
-    from paper_2502_00115_b200.synth import make_pair
 
     c = workload(args.config, args.metric)
     cfg = search_config(c)
     nsteps = args.warmup + args.steps
-    pairs = [make_pair(c["spec"], 1000 * rank + s) for s in range(nsteps)]
+    pairs, data_desc = bench_pairs(args.config, nsteps, rank * nsteps, args.inputs)
     stream = torch.cuda.current_stream().cuda_stream
 
     # ---- device-resident value: plans (clouds in HBM) built before timing
@@ -543,7 +567,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "i32 fixed-point vote / f32 screen / f64 exact",
-            "data": "synthetic (seeded ModelNet40-shaped pairs, paper_2502_00115_b200/synth.py)",
+            "data": data_desc,
             "config": {"workload": describe(args.config, c, cfg, n_src, preps[0].y.shape[0]),
                        "metric": cfg.metric.kind, "rotations": R,
                        "parallelism": f"replicas x{world} (registrations sharded, no collective)",
