@@ -445,9 +445,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_SHARE_DEVICE=1: code-path check of the N-rank protocol on a 1-GPU
+    # box (every rank on cuda:0, gloo collectives; its numbers are not a
+    # measurement -- the ranks time-share one GPU)
+    share = os.environ.get("BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2502_00115_b200 import _native, dses
     from paper_2502_00115_b200.engines import prepare
