@@ -6,11 +6,10 @@ sys.path.insert(0, '.')
 import bench
 from paper_2502_00115_b200 import _native
 from paper_2502_00115_b200.engines import prepare
-from paper_2502_00115_b200.synth import make_pair
 for name in sys.argv[1:] or ["c2", "c4"]:
     c = bench.workload(name)
     cfg = bench.search_config(c)
-    x, y, _ = make_pair(c["spec"], 0)
+    x, y, _ = bench.bench_pairs(name, 1)[0][0]
     best = 1e9
     for _ in range(5):
         t0 = time.perf_counter()

@@ -15,11 +15,11 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 from paper_2502_00115_b200 import ErrorMetric, SearchConfig, _native  # noqa: E402
 from paper_2502_00115_b200.engines import prepare  # noqa: E402
-from paper_2502_00115_b200.synth import CONFIGS, make_pair  # noqa: E402
 
 
-def run(name, cfg, spec, seed=0, reps=3):
-    x, y, _ = make_pair(spec, seed)
+def run(name, cfg, pair_cfg, reps=3):
+    (pairs, inputs) = bench.bench_pairs(pair_cfg, 1)
+    x, y, _ = pairs[0]
     p = prepare(x, y, cfg)
     g = _native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot)
     best = None
@@ -29,7 +29,8 @@ def run(name, cfg, spec, seed=0, reps=3):
             if best is None or r["ms_total"] < best["ms_total"]:
                 best = r
     R = cfg.rotation_count
-    return {"config": name, "rotations": R, "n_source": x.shape[0], "n_reference": y.shape[0],
+    return {"config": name, "inputs": inputs, "rotations": R, "n_source": x.shape[0],
+            "n_reference": y.shape[0],
             "metric": cfg.metric.kind, "ms_total": best["ms_total"],
             "ms_vote_kernel": best["ms_vote_kernel"],
             "rotations_per_sec": R / (best["ms_total"] * 1e-3),
@@ -40,15 +41,14 @@ def run(name, cfg, spec, seed=0, reps=3):
 
 def main():
     rows = []
-    for name in ("c1", "c2", "c3", "c4"):
+    for name in ("c1", "c2", "c3", "c4", "c2local"):
         c = bench.workload(name)
-        rows.append(run(name, bench.search_config(c), c["spec"], reps=2 if name == "c3" else 3))
+        rows.append(run(name, bench.search_config(c), name, reps=2 if name == "c3" else 3))
         print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
-    spec = CONFIGS["c2"]["spec"]
-    for K in (10, 22, 50, 108):
+    for K in (10, 22, 50, 108):  # c5: the c2 seed-0 pair
         cfg = SearchConfig(k_rot=K, rot_step=math.radians(45.0 / K), k_trans=20, trans_bin=0.025,
                            metric=ErrorMetric.truncated_l1(0.125))
-        rows.append(run(f"c5_K{K}", cfg, spec, reps=1 if K >= 108 else 2))
+        rows.append(run(f"c5_K{K}", cfg, "c2", reps=1 if K >= 108 else 2))
         print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
     print(json.dumps({"device": "B200 (1 GPU)", "rows": rows}, indent=1))
 

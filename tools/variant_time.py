@@ -7,14 +7,13 @@ if len(sys.argv) > 2:
 _native.load(_native.LIB_PATH)
 import bench
 from paper_2502_00115_b200.engines import prepare
-from paper_2502_00115_b200.synth import make_pair
 c = bench.workload(sys.argv[1])
 cfg = bench.search_config(c)
 import os
 seeds = [int(v) for v in os.environ.get('SEEDS', '0').split(',')]
 vsum = tsum = 0.0
 for seed in seeds:  # best of 3 per seed pair, summed over the seeds
-    x, y, _ = make_pair(c['spec'], seed)
+    x, y, _ = bench.bench_pairs(sys.argv[1], 1, seed)[0][0]
     p = prepare(x, y, cfg)
     plan = _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims)
     g = _native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot)
