@@ -132,6 +132,13 @@ int dses_mode_dense_batch(int device, const double* rots, int64_t nrot, const do
 int dses_search(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t r_count, double q,
                 int metric_code, double metric_param, int skip_refine, dses_result* out,
                 void* stream);
+/* dses_search split in two: _async enqueues the whole search on `stream` and
+ * returns (grid's host tables must stay valid until _wait); _wait blocks on
+ * it and fills `out`.  Lets a caller queue registration k+1 before reading
+ * the result of k (engines.dses_batch).  One search in flight per plan. */
+int dses_search_async(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t r_count,
+                      double q, int metric_code, double param, int skip_refine, void* stream);
+int dses_search_wait(dses_plan* plan, dses_result* out);
 
 /* engines.exhaustive_search (engines.py:156-193, _kernels.exhaustive_batch
  * _kernels.py:327-381): the metric at every pose of the 6-D grid, rotations

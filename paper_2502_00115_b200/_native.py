@@ -77,6 +77,9 @@ _SIGS = [
     ("dses_search", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, ctypes.c_double,
                                    ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                    ctypes.POINTER(Result), _vp]),
+    ("dses_search_async", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, ctypes.c_double,
+                                         ctypes.c_int, ctypes.c_double, ctypes.c_int, _vp]),
+    ("dses_search_wait", ctypes.c_int, [_vp, ctypes.POINTER(Result)]),
     ("dses_exhaustive", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _dp, ctypes.c_int,
                                        ctypes.c_double, ctypes.POINTER(Result), _vp]),
     ("dses_stage_vote", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, _ip, _ip, _vp]),
@@ -257,6 +260,22 @@ class Plan:
         check(self._L.dses_search(self._h, ctypes.byref(grid), int(r_begin), int(r_count), float(q),
                                   int(code), float(param), int(bool(skip_refine)),
                                   ctypes.byref(res), stream), "dses_search")
+        return res.as_dict()
+
+    def search_async(self, grid: Grid, q, code, param, skip_refine, r_begin=0, r_count=-1,
+                     stream=None):
+        """Enqueue a search; search_wait() returns its result dict."""
+        check(self._L.dses_search_async(self._h, ctypes.byref(grid), int(r_begin), int(r_count),
+                                        float(q), int(code), float(param), int(bool(skip_refine)),
+                                        stream), "dses_search_async")
+        self._inflight = grid  # its host tables must outlive the search
+
+    def search_wait(self):
+        res = Result()
+        try:
+            check(self._L.dses_search_wait(self._h, ctypes.byref(res)), "dses_search_wait")
+        finally:
+            self._inflight = None
         return res.as_dict()
 
     def exhaustive(self, grid: Grid, k_trans, t_center, code, param, stream=None):

@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <thread>
 #include <cstring>
 #include <future>
@@ -129,6 +130,10 @@ static void keep_pool(int device) {
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // a plan built on the upload stream must not wait for memory freed behind
+    // a search still running on another stream (the pool grows instead)
+    int no = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   }
   done[device] = true;
 }
@@ -137,11 +142,11 @@ struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
   bool borrowed = false;  // points into another buffer (an upload arena): never freed here
-  cudaError_t ensure(size_t bytes) {
+  cudaError_t ensure(size_t bytes, cudaStream_t st = 0) {
     if (bytes <= cap && p) return cudaSuccess;
     release();
     size_t want = std::max<size_t>(bytes + bytes / 2, 256);
-    cudaError_t e = cudaMallocAsync(&p, want, 0);
+    cudaError_t e = cudaMallocAsync(&p, want, st);
     if (e == cudaSuccess) cap = want;
     return e;
   }
@@ -204,7 +209,7 @@ struct UploadPack {
     }
     for (const Item& it : items)
       if (it.bytes) std::memcpy(static_cast<unsigned char*>(staging) + it.off, it.src, it.bytes);
-    cudaError_t e = arena.ensure(total);
+    cudaError_t e = arena.ensure(total, st);
     if (e != cudaSuccess) return e;
     e = h2d(arena.p, staging, total, st);
     if (e != cudaSuccess) return e;
@@ -252,7 +257,48 @@ struct dses_plan {
   cudaEvent_t ev[8];
   Traffic traffic;       // counters since the last dses_stage_stats / dses_search
   bool vote_timed = false;
+  long long* rec_host = nullptr;  // pinned result record of dses_search (12 slots)
+  struct Pending {                // a dses_search_async awaiting dses_search_wait
+    bool active = false;
+    dses_grid g{};
+    int64_t r_begin = 0, r_count = 0, cap = 0;
+    double q = 0, param = 0;
+    int code = 0, skip_refine = 0;
+    void* stream = nullptr;
+  } pend;
 };
+
+// Pinned 128-byte result records, carved from page-locked slabs (one
+// cudaHostAlloc per 256 plans instead of one per plan).
+static std::mutex g_rec_mu;
+static std::vector<long long*> g_rec_free;
+static long long* rec_take() {
+  std::lock_guard<std::mutex> lk(g_rec_mu);
+  if (g_rec_free.empty()) {
+    void* slab = nullptr;
+    if (cudaHostAlloc(&slab, 256 * 128, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    for (int k = 255; k >= 0; --k)
+      g_rec_free.push_back(reinterpret_cast<long long*>(static_cast<char*>(slab) + 128 * k));
+  }
+  long long* r = g_rec_free.back();
+  g_rec_free.pop_back();
+  return r;
+}
+static void rec_give(long long* r) {
+  if (!r) return;
+  std::lock_guard<std::mutex> lk(g_rec_mu);
+  g_rec_free.push_back(r);
+}
+
+// Plan construction uploads on a non-blocking stream of the calling thread,
+// so building the next registration's plan never waits for a search running
+// on the caller's stream.
+static cudaStream_t upload_stream(int device) {
+  static thread_local cudaStream_t streams[64] = {};
+  if (device < 0 || device >= 64) return 0;
+  if (!streams[device]) cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+  return streams[device];
+}
 
 // RAII: route the copy/launch counters of this call to the plan
 struct TrafficScope {
@@ -488,7 +534,7 @@ std::vector<std::pair<int, int>> near_pairs(const double* y, int64_t m, double t
 
 int build_plan(dses_plan* P, const double* x, const double* y) {
   const int64_t n = P->n, m = P->m;
-  cudaStream_t st = 0;
+  cudaStream_t st = upload_stream(P->device);
   // ---- fixed-point scale
   trace("fixed-point scale");
   double ymax = 0, xnorm = 0;
@@ -778,10 +824,10 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   pack.add(P->gcell, range);
   pack.add(P->gpts, gp);
   CK(pack.commit(P->arena, st));
-  CK(P->stats.ensure(4 * sizeof(unsigned long long)));
+  CK(P->stats.ensure(4 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(P->stats.p, 0, 4 * sizeof(unsigned long long), st));
-  CK(P->scal.ensure(64));
-  CK(cudaStreamSynchronize(st));
+  CK(P->scal.ensure(64, st));
+  CK(cudaStreamSynchronize(st));  // this thread's upload stream only
 
   // ---- vote kernel parameters
   trace("vote kernel parameters");
@@ -1013,6 +1059,8 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
   for (int k = 0; k < 3; ++k) { P->ilo[k] = ilo[k]; P->dims[k] = dims[k]; }
   P->sparse = nbins > (double)kDenseMaxBins;
   for (auto& e : P->ev) cudaEventCreate(&e);
+  P->rec_host = rec_take();
+  if (!P->rec_host) { dses_plan_destroy(P); return fail(DSES_E_NOMEM, "pinned record"); }
   TrafficScope ts_(P);
   const int rc = build_plan(P, x, y);
   if (rc != DSES_OK) { dses_plan_destroy(P); return rc; }
@@ -1029,8 +1077,10 @@ extern "C" int dses_plan_destroy(dses_plan* P) {
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,
                     &P->err64, &P->win_err, &P->win_row, &P->win_c, &P->tmp_rows, &P->tmp_lins,
                     &P->tvec};
+  if (P->pend.active) cudaEventSynchronize(P->ev[4]);  // an unwaited search
   for (DevBuf* b : bufs) b->release();
   for (auto& e : P->ev) cudaEventDestroy(e);
+  rec_give(P->rec_host);
   delete P;
   return DSES_OK;
 }
@@ -1371,15 +1421,16 @@ extern "C" int dses_stage_stats(dses_plan* P, int64_t* pairs, int64_t* votes, in
 // (more -- a flat landscape of near-ties -- falls back to the staged path).
 static constexpr int64_t kFusedRescoreCap = 4096;
 
-extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t r_count,
-                           double q, int code, double param, int skip_refine, dses_result* out,
-                           void* stream) {
+extern "C" int dses_search_async(dses_plan* P, const dses_grid* g, int64_t r_begin,
+                                 int64_t r_count, double q, int code, double param, int skip_refine,
+                                 void* stream) {
   // engines.dses on one GPU.  After the vote, every stage reads the previous
   // stage's counters on the device (M*, kept, screened minimum, selected), so
-  // the whole search is one stream of launches and ONE device->host read.
+  // the whole search is one stream of launches and ONE device->host read
+  // (into the plan's pinned record); dses_search_wait completes it.
   TrafficScope ts_(P);
-  if (!P || !g || !out || code < 0 || code > 4) return fail(DSES_E_INVALID, "bad arguments");
-  std::memset(out, 0, sizeof(*out));
+  if (!P || !g || code < 0 || code > 4) return fail(DSES_E_INVALID, "bad arguments");
+  if (P->pend.active) return fail(DSES_E_INVALID, "plan has a search in flight");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t total = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);
@@ -1450,10 +1501,37 @@ extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, in
                               P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(),
                               P->counts.as<int>(), r_begin, miss,
                               P->stats.as<unsigned long long>(), rec, st)));
-  long long h[12];
-  CK(d2h(h, rec, sizeof h, st));
+  CK(d2h(P->rec_host, rec, 12 * sizeof(long long), st));
   CK(cudaEventRecord(P->ev[4], st));
+  P->pend.active = true;
+  P->pend.g = *g;
+  P->pend.r_begin = r_begin;
+  P->pend.r_count = r_count;
+  P->pend.cap = cap;
+  P->pend.q = q;
+  P->pend.code = code;
+  P->pend.param = param;
+  P->pend.skip_refine = skip_refine;
+  P->pend.stream = stream;
+  return DSES_OK;
+}
+
+extern "C" int dses_search_wait(dses_plan* P, dses_result* out) {
+  TrafficScope ts_(P);
+  if (!P || !out) return fail(DSES_E_INVALID, "bad arguments");
+  if (!P->pend.active) return fail(DSES_E_INVALID, "no search in flight on this plan");
+  std::memset(out, 0, sizeof(*out));
+  CK(cudaSetDevice(P->device));
+  P->pend.active = false;
+  const dses_grid* g = &P->pend.g;
+  const int64_t r_begin = P->pend.r_begin, r_count = P->pend.r_count, cap = P->pend.cap;
+  const double q = P->pend.q, param = P->pend.param;
+  const int code = P->pend.code, skip_refine = P->pend.skip_refine;
+  void* stream = P->pend.stream;
+  int rc = DSES_OK;
   CK(cudaEventSynchronize(P->ev[4]));
+  long long h[12];
+  std::memcpy(h, P->rec_host, sizeof h);
   out->mstar = h[0];
   out->candidates_evaluated = h[1];
   out->pairs_evaluated = h[7];
@@ -1505,6 +1583,16 @@ extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, in
   out->h2d_bytes = P->traffic.h2d;
   out->d2h_bytes = P->traffic.d2h;
   return DSES_OK;
+}
+
+extern "C" int dses_search(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t r_count,
+                           double q, int code, double param, int skip_refine, dses_result* out,
+                           void* stream) {
+  if (!out) return fail(DSES_E_INVALID, "bad arguments");
+  std::memset(out, 0, sizeof(*out));
+  const int rc = dses_search_async(P, g, r_begin, r_count, q, code, param, skip_refine, stream);
+  if (rc) return rc;
+  return dses_search_wait(P, out);
 }
 
 extern "C" int dses_exhaustive(dses_plan* P, const dses_grid* g, int64_t k_trans,

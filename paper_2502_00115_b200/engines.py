@@ -195,9 +195,11 @@ def dses(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationR
 
 def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     """dses over a batch of (source, reference) pairs (the registration loop of
-    harness.run_batch, harness.py:145-162): the host preparation and plan
-    construction of pair k+1 (a worker thread; the C ABI releases the GIL)
-    overlap the GPU search of pair k.  Results are identical to calling
+    harness.run_batch, harness.py:145-162), pipelined: the host preparation
+    and plan construction of pair k+1 run on a worker thread (the C ABI
+    releases the GIL; plans upload on their own stream) while the GPU searches
+    pair k, and search k+1 is queued before the result of k is read, so the
+    GPU runs the searches back to back.  Results are identical to calling
     dses() on each pair; errors are raised for the first failing pair."""
     import concurrent.futures as cf
 
@@ -205,15 +207,40 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     out = []
     if not pairs:
         return out
-    with cf.ThreadPoolExecutor(max_workers=1) as ex:
-        fut = ex.submit(_build, pairs[0][0], pairs[0][1], cfg, device)
-        for k in range(len(pairs)):
-            t0, prep, grid, plan = fut.result()
-            if k + 1 < len(pairs):
-                fut = ex.submit(_build, pairs[k + 1][0], pairs[k + 1][1], cfg, device)
-            with plan:
-                res = plan.search(grid, cfg.q, prep.code, prep.param, prep.skip_refine)
-            out.append(_result(prep, cfg, res, t0))
+    pending = None  # (t0, prep, grid, plan) whose search is queued on the GPU
+    try:
+        with cf.ThreadPoolExecutor(max_workers=1) as ex:
+            fut = ex.submit(_build, pairs[0][0], pairs[0][1], cfg, device)
+            for k in range(len(pairs) + 1):
+                item, err = None, None
+                if k < len(pairs):
+                    try:
+                        item = fut.result()
+                        if k + 1 < len(pairs):
+                            fut = ex.submit(_build, pairs[k + 1][0], pairs[k + 1][1], cfg, device)
+                        _, prep, grid, plan = item
+                        plan.search_async(grid, cfg.q, prep.code, prep.param, prep.skip_refine)
+                    except Exception as exc:  # raised after pair k-1's own outcome
+                        if item is not None:
+                            item[3].close()
+                        item, err = None, exc
+                prev, pending = pending, item
+                if prev is not None:
+                    t0, prep, grid, plan = prev
+                    try:
+                        res = plan.search_wait()
+                    finally:
+                        plan.close()
+                    out.append(_result(prep, cfg, res, t0))
+                if err is not None:
+                    raise err
+    finally:
+        if pending is not None:
+            try:
+                pending[3].search_wait()
+            except Exception:
+                pass
+            pending[3].close()
     return out
 
 

@@ -304,6 +304,39 @@ def test_dses_batch_equals_single_calls(api):
     assert api.dses_batch([], [], cfg) == []
 
 
+def test_dses_batch_error_order_and_async_misuse(api):
+    """A pair without any in-window vote raises NoCandidateError from
+    dses_batch exactly like dses() (the first failing pair wins, earlier pairs
+    are not lost to a later failure); the async entry points reject misuse."""
+    from paper_2502_00115_b200 import _native
+    from paper_2502_00115_b200.engines import prepare
+    from paper_2502_00115_b200.synth import CONFIGS, make_pair
+    pairs = [make_pair(CONFIGS["c1"]["spec"], s) for s in range(3)]
+    cfg = api.SearchConfig(k_rot=1, rot_step=math.radians(9), k_trans=2, trans_bin=0.025)
+    far = (pairs[1][0] + 100.0, pairs[1][1])  # translation far outside the window
+    xs = [pairs[0][0], far[0], pairs[2][0]]
+    ys = [pairs[0][1], far[1], pairs[2][1]]
+    with pytest.raises(api.NoCandidateError):
+        api.dses(xs[1], ys[1], cfg)
+    with pytest.raises(api.NoCandidateError):
+        api.dses_batch(xs, ys, cfg)
+    ok = api.dses_batch(xs[:1], ys[:1], cfg)
+    assert len(ok) == 1
+    p = prepare(pairs[0][0], pairs[0][1], cfg)
+    g = _native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot)
+    with _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims) as plan:
+        with pytest.raises(ValueError):  # _native maps DSES_E_INVALID to ValueError
+            plan.search_wait()  # nothing in flight
+        plan.search_async(g, cfg.q, p.code, p.param, p.skip_refine)
+        with pytest.raises(ValueError):
+            plan.search_async(g, cfg.q, p.code, p.param, p.skip_refine)  # one at a time
+        r = plan.search_wait()
+        r2 = plan.search(g, cfg.q, p.code, p.param, p.skip_refine)
+        assert (r["winner_row"], r["winner_lin"], r["best_error"]) == \
+            (r2["winner_row"], r2["winner_lin"], r2["best_error"])
+        plan.search_async(g, cfg.q, p.code, p.param, p.skip_refine)  # destroyed in flight: safe
+
+
 def test_source_cloud_beyond_shared_memory():
     """41^3 histogram in shared memory + 6,000 rotated source points in global
     memory (the vote kernel's <HSMEM, !PSMEM> instantiation)."""
