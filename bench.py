@@ -470,6 +470,8 @@ def main():
     # ---- device-resident value: plans (clouds in HBM) built before timing
     preps = [prepare(x, y, cfg) for x, y, _ in pairs]
     plans = [_native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims, local) for p in preps]
+    for plan in plans:  # plan construction includes the search scratch (dses_plan_reserve)
+        plan.reserve(cfg.rotation_count)
     grids = [_native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot) for p in preps]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 

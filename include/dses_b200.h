@@ -85,6 +85,11 @@ typedef struct {
 const char* dses_last_error(void);
 int dses_device_count(int* out);
 const char* dses_build_info(void);
+/* A non-blocking CUDA stream on `device` (an opaque cudaStream_t for the
+ * `stream` arguments); destroy synchronises it first.  Two of them let
+ * consecutive registrations overlap at their boundaries (engines.dses_batch). */
+int dses_stream_create(int device, void** stream);
+int dses_stream_destroy(void* stream);
 
 /* ---- plan lifecycle ----------------------------------------------------- */
 /* x: source (n,3) row-major f64; y: reference (m,3).  bin_size = trans_bin;
@@ -132,6 +137,10 @@ int dses_mode_dense_batch(int device, const double* rots, int64_t nrot, const do
 int dses_search(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t r_count, double q,
                 int metric_code, double metric_param, int skip_refine, dses_result* out,
                 void* stream);
+/* Allocate every device buffer a search over `r_count` rotations uses (also
+ * done at the top of each search; calling it at plan construction keeps
+ * memory-pool growth off the search's timeline). */
+int dses_plan_reserve(dses_plan* plan, int64_t r_count);
 /* dses_search split in two: _async enqueues the whole search on `stream` and
  * returns (grid's host tables must stay valid until _wait); _wait blocks on
  * it and fills `out`.  Lets a caller queue registration k+1 before reading

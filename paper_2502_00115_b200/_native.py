@@ -77,6 +77,9 @@ _SIGS = [
     ("dses_search", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, ctypes.c_double,
                                    ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                    ctypes.POINTER(Result), _vp]),
+    ("dses_plan_reserve", ctypes.c_int, [_vp, _i64]),
+    ("dses_stream_create", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("dses_stream_destroy", ctypes.c_int, [_vp]),
     ("dses_search_async", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, ctypes.c_double,
                                          ctypes.c_int, ctypes.c_double, ctypes.c_int, _vp]),
     ("dses_search_wait", ctypes.c_int, [_vp, ctypes.POINTER(Result)]),
@@ -174,6 +177,27 @@ def make_grid(k: int, cos_tab: np.ndarray, sin_tab: np.ndarray, center=None):
     return g
 
 
+class Stream:
+    """A non-blocking CUDA stream owned by the library (dses_stream_*)."""
+
+    def __init__(self, device=0):
+        self._L = load()
+        h = _vp()
+        check(self._L.dses_stream_create(int(device), ctypes.byref(h)), "dses_stream_create")
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            check(self._L.dses_stream_destroy(self.handle), "dses_stream_destroy")
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 class Plan:
     """One (source, reference, translation lattice) problem resident on a GPU
     (wraps dses_plan_*)."""
@@ -261,6 +285,10 @@ class Plan:
                                   int(code), float(param), int(bool(skip_refine)),
                                   ctypes.byref(res), stream), "dses_search")
         return res.as_dict()
+
+    def reserve(self, r_count):
+        """Pre-allocate the search buffers for r_count rotations."""
+        check(self._L.dses_plan_reserve(self._h, int(r_count)), "dses_plan_reserve")
 
     def search_async(self, grid: Grid, q, code, param, skip_refine, r_begin=0, r_count=-1,
                      stream=None):

@@ -6,6 +6,7 @@
 // the small host<->device scalar traffic between stages.  The Python layer
 // (paper_2502_00115_b200/engines.py) mirrors gridreg's API and exceptions on top.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -116,6 +117,26 @@ extern "C" int dses_device_count(int* out) {
   return DSES_OK;
 }
 
+extern "C" int dses_stream_create(int device, void** out) {
+  if (!out) return fail(DSES_E_INVALID, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)
+    return fail(DSES_E_NODEVICE, "bad device %d", device);
+  CK(cudaSetDevice(device));
+  cudaStream_t s = nullptr;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = (void*)s;
+  return DSES_OK;
+}
+
+extern "C" int dses_stream_destroy(void* stream) {
+  if (!stream) return DSES_OK;
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  CK(cudaStreamDestroy((cudaStream_t)stream));
+  return DSES_OK;
+}
+
 // ---------------------------------------------------------------------------
 // device buffers
 // ---------------------------------------------------------------------------
@@ -124,8 +145,8 @@ extern "C" int dses_device_count(int* out) {
 // a registration that creates a fresh plan reuses cached memory instead of
 // paying cudaMalloc/cudaFree device synchronisations.
 static void keep_pool(int device) {
-  static bool done[64] = {false};
-  if (device < 0 || device >= 64 || done[device]) return;
+  static std::atomic<bool> done[64];
+  if (device < 0 || device >= 64 || done[device].exchange(true)) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
@@ -135,7 +156,6 @@ static void keep_pool(int device) {
     int no = 0;
     cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   }
-  done[device] = true;
 }
 
 struct DevBuf {
@@ -1421,6 +1441,50 @@ extern "C" int dses_stage_stats(dses_plan* P, int64_t* pairs, int64_t* votes, in
 // (more -- a flat landscape of near-ties -- falls back to the staged path).
 static constexpr int64_t kFusedRescoreCap = 4096;
 
+// Every device buffer a dses_search over `nr` rotations touches, allocated up
+// front (plan construction via dses_plan_reserve, or at the top of the
+// search): a search never grows the memory pool between its launches.
+static int reserve_search(dses_plan* P, int64_t nr, cudaStream_t st = 0) {
+  nr = std::max<int64_t>(nr, 1);
+  CK(P->counts.ensure(sizeof(int) * nr, st));
+  CK(P->lins.ensure(sizeof(int) * nr, st));
+  CK(P->ties.ensure(sizeof(int) * nr, st));
+  const VoteParams& v = P->vp;
+  const size_t per_cta = (P->hsmem ? 0 : (size_t)v.hist_words * 4) + (P->psmem ? 0 : (size_t)v.n_pad * 16);
+  if (per_cta && !P->sparse) {
+    const size_t budget = (size_t)4 << 30;
+    const int grid = (int)std::max<size_t>(
+        1, std::min<size_t>((size_t)std::min<int64_t>(P->vote_grid, nr), budget / per_cta));
+    if (!P->hsmem) CK(P->hist_g.ensure((size_t)grid * v.hist_words * 4, st));
+    if (!P->psmem) CK(P->p_g.ensure((size_t)grid * v.n_pad * 16, st));
+  }
+  const int64_t cap = std::min<int64_t>(nr, kFusedRescoreCap);
+  const int nblk = (int)((P->n + screen_threads() - 1) / screen_threads());
+  CK(P->cand_rows.ensure(sizeof(int64_t) * nr, st));
+  CK(P->cand_lins.ensure(sizeof(int) * nr, st));
+  CK(P->win_err.ensure(sizeof(double), st));
+  CK(P->win_row.ensure(sizeof(int64_t), st));
+  CK(P->win_c.ensure(sizeof(int), st));
+  CK(P->tvec.ensure(sizeof(double) * (P->n + 16), st));
+  CK(P->partial.ensure(sizeof(double) * nblk * nr, st));
+  CK(P->err32.ensure(sizeof(double) * nr, st));
+  CK(P->sel.ensure(sizeof(int) * nr, st));
+  CK(P->vals.ensure(sizeof(double) * P->n * cap, st));
+  CK(P->err64.ensure(sizeof(double) * cap, st));
+  return DSES_OK;
+}
+
+extern "C" int dses_plan_reserve(dses_plan* P, int64_t r_count) {
+  if (!P || r_count < 0) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  if (P->sparse) return DSES_OK;
+  cudaStream_t st = upload_stream(P->device);
+  const int rc = reserve_search(P, r_count, st);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(st));
+  return DSES_OK;
+}
+
 extern "C" int dses_search_async(dses_plan* P, const dses_grid* g, int64_t r_begin,
                                  int64_t r_count, double q, int code, double param, int skip_refine,
                                  void* stream) {
@@ -1439,6 +1503,10 @@ extern "C" int dses_search_async(dses_plan* P, const dses_grid* g, int64_t r_beg
   if (P->sparse)
     return fail(DSES_E_INVALID, "translation window of %.3g bins is beyond the search's dense "
                 "limit (%d bins)", (double)P->dims[0] * P->dims[1] * P->dims[2], kDenseMaxBins);
+  {
+    const int rr = reserve_search(P, r_count);
+    if (rr) return rr;
+  }
   CK(cudaEventRecord(P->ev[0], st));
   RotSource rs;
   int rc = set_grid(P, g, &rs, st);

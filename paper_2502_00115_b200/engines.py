@@ -182,6 +182,7 @@ def _build(source, reference, cfg: SearchConfig, device: int):
     prep = prepare(source, reference, cfg)
     grid = _native.make_grid(cfg.k_rot, prep.cos_tab, prep.sin_tab, prep.center_rot)
     plan = _native.Plan(prep.x, prep.y, cfg.trans_bin, prep.ilo, prep.dims, device)
+    plan.reserve(cfg.rotation_count)  # search scratch allocated with the plan
     return t0, prep, grid, plan
 
 
@@ -207,7 +208,11 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     out = []
     if not pairs:
         return out
+    from . import _native
+
     pending = None  # (t0, prep, grid, plan) whose search is queued on the GPU
+    streams = [_native.Stream(device), _native.Stream(device)]  # alternate: the
+    # vote of k+1 fills the SMs that k's last rotations and score stage leave idle
     try:
         with cf.ThreadPoolExecutor(max_workers=1) as ex:
             fut = ex.submit(_build, pairs[0][0], pairs[0][1], cfg, device)
@@ -219,7 +224,8 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
                         if k + 1 < len(pairs):
                             fut = ex.submit(_build, pairs[k + 1][0], pairs[k + 1][1], cfg, device)
                         _, prep, grid, plan = item
-                        plan.search_async(grid, cfg.q, prep.code, prep.param, prep.skip_refine)
+                        plan.search_async(grid, cfg.q, prep.code, prep.param, prep.skip_refine,
+                                          stream=streams[k % 2].handle)
                     except Exception as exc:  # raised after pair k-1's own outcome
                         if item is not None:
                             item[3].close()
@@ -241,6 +247,8 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
             except Exception:
                 pass
             pending[3].close()
+        for st in streams:
+            st.close()
     return out
 
 
