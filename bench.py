@@ -588,8 +588,9 @@ def main():
                     "registrations_per_sec": args.steps * world / (float(tb.item()) * 1e-3),
                     "h2d_bytes_per_step": bh2d // args.steps, "d2h_bytes_per_step": bd2h // args.steps,
                     "path": "paper_2502_00115_b200.dses_batch(numpy sources, numpy references, "
-                            "SearchConfig): K registrations, plan construction of k+1 overlapping "
-                            "the search of k (harness.run_batch's loop)",
+                            "SearchConfig): K registrations (harness.run_batch's loop), plan "
+                            "construction of k+1 on a worker thread overlapping the search of k, "
+                            "search k+1 queued on the other of two streams before k is read",
                     "single_call": {"value": e_value, "unit": UNIT,
                                     "registrations_per_sec": args.steps * world / (float(te.item()) * 1e-3),
                                     "h2d_bytes_per_step": h2d // args.steps,
