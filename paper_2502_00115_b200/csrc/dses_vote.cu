@@ -38,6 +38,15 @@
 #ifndef DSES_DYNROT
 #define DSES_DYNROT 1  // rotations claimed from a global queue
 #endif
+#ifndef DSES_FRAC_IMAD
+#define DSES_FRAC_IMAD 1  // fractions on the multiply pipe (ALU-pipe relief, c2 -2.5%)
+#endif
+#ifndef DSES_VOTE_IMAD
+#define DSES_VOTE_IMAD 0
+#endif
+#ifndef DSES_FAR_GTHR
+#define DSES_FAR_GTHR 1  // far lanes: all-ones guard threshold (c2 -5%)
+#endif
 #ifndef DSES_CHUNKBOX
 #define DSES_CHUNKBOX 1
 #endif
@@ -191,6 +200,8 @@ __device__ __forceinline__ void defer_pairs(const VoteParams& p, const double* R
 struct FastK {
   unsigned W0, W1, W2, fmask, gthr, d1, d2;
   int F;
+  unsigned negP;  // -(2^F): fraction = u + (u >> F) * negP on the multiply pipe
+  unsigned c_ffff;  // 0xffff, opaque to the compiler (vote value by IMAD)
 };
 
 // Fixed-point decision for one pair: candidate (inside the guard-extended
@@ -205,16 +216,30 @@ __device__ __forceinline__ PairBin fixed_bin(const FastK& k, const int4& Y, cons
   r.cand = (u0 < k.W0) & (u1 < k.W1) & (u2 < k.W2);
   // a candidate with every fraction >= 2G lies inside [0, D) (u in [D, W) has
   // a fraction < 2G) and its fixed-point bin u >> F is the exact bin
+#if DSES_FRAC_IMAD
+  // the bins u >> F are needed anyway; the fractions u - (u >> F) * 2^F then
+  // cost one IMAD each (FMA pipe) instead of an AND on the saturated ALU pipe
+  const unsigned q0 = u0 >> k.F, q1 = u1 >> k.F, q2 = u2 >> k.F;
+  r.near = r.cand & (__vimin3_u32(u0 + q0 * k.negP, u1 + q1 * k.negP, u2 + q2 * k.negP) < k.gthr);
+  r.lin = (q0 * k.d1 + q1) * k.d2 + q2;
+#else
   r.near = r.cand & (__vimin3_u32(u0 & k.fmask, u1 & k.fmask, u2 & k.fmask) < k.gthr);
   r.lin = ((u0 >> k.F) * k.d1 + (u1 >> k.F)) * k.d2 + (u2 >> k.F);
+#endif
   return r;
 }
 
 template <bool HSMEM>
 __device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsigned lin, bool ok,
-                                        unsigned nbins = 0xffffffffu) {
+                                        unsigned nbins = 0xffffffffu, unsigned c_ffff = 0xffffu) {
   DSES_ASSERT(!ok || lin < nbins);
+#if DSES_VOTE_IMAD
+  // 1 or 0x10000 as (lin & 1) * 0xffff + 1 with the 0xffff from shared memory
+  // (a runtime multiplier stays an IMAD on the multiply pipe)
+  if (HSMEM) reds_add_if(hist_sh + ((lin >> 1) << 2), (lin & 1u) * c_ffff + 1u, ok);
+#else
   if (HSMEM) reds_add_if(hist_sh + ((lin >> 1) << 2), 1u << ((lin & 1u) << 4), ok);
+#endif
   else if (ok) atomicAdd(&hist[lin], 1u);
 }
 
@@ -247,8 +272,16 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     const bool decided = b[s].cand & !b[s].near;
+#if DSES_FAR_GTHR
+    // far lanes carry an all-ones guard threshold: every candidate of theirs
+    // is "near" (exact path), so `far` drops out of the per-pair logic
+    bool ok = decided;
+    defer[s] = b[s].near;
+    (void)far;
+#else
     bool ok = decided & !far;
     defer[s] = b[s].near | (decided & far);
+#endif
     if (GP > 0) {
       const int key = decided ? (int)b[s].lin : (b[s].near ? -2 : -1);
       const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
@@ -260,10 +293,15 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
         und |= (l1 >= 0) & (k1 == -2);
       }
       dup &= decided;
+#if DSES_FAR_GTHR
+      ok = decided & !dup & !und;
+      defer[s] = b[s].near | (decided & !dup & und);
+#else
       ok = decided & !far & !dup & !und;
       defer[s] = b[s].near | (decided & !dup & (far | und));
+#endif
     }
-    vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins);
+    vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins, fk.c_ffff);
     DSES_ASSERT(is[s] >= 0 && is[s] < p.n && j >= 0 && j < p.m_pad);
     anydef |= defer[s];
   }
@@ -308,16 +346,18 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   const uint32_t P_sh = PSMEM ? (uint32_t)__cvta_generic_to_shared(P) : 0u;
   // fast-path constants through shared memory: loaded into regular registers
   // once, instead of being re-loaded into uniform registers in the hot loop
-  __shared__ unsigned kc[9];
+  __shared__ unsigned kc[11];
   if (tid == 0) {
     kc[0] = p.W0; kc[1] = p.W1; kc[2] = p.W2; kc[3] = p.fmask; kc[4] = p.gthr;
     kc[5] = (unsigned)p.d1; kc[6] = (unsigned)p.d2; kc[7] = (unsigned)p.F;
     kc[8] = HSMEM ? (uint32_t)__cvta_generic_to_shared(hist) : 0u;
+    kc[9] = 0u - (1u << p.F);
+    kc[10] = 0xffffu;
   }
   __syncthreads();
   FastK fk;
   fk.W0 = kc[0]; fk.W1 = kc[1]; fk.W2 = kc[2]; fk.fmask = kc[3]; fk.gthr = kc[4];
-  fk.d1 = kc[5]; fk.d2 = kc[6]; fk.F = (int)kc[7];
+  fk.d1 = kc[5]; fk.d2 = kc[6]; fk.F = (int)kc[7]; fk.negP = kc[9]; fk.c_ffff = kc[10];
   const uint32_t hist_sh = kc[8];
   Lane L;
   L.rare_sh = (uint32_t)__cvta_generic_to_shared(rare);
@@ -430,6 +470,12 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         int4 Y = __ldg(&p.yq[j]);
         if (!valid) Y = make_int4(kNoRef, 0, 0, 0);
         const bool far = (Y.w & kFarFlag) != 0;
+#if DSES_FAR_GTHR
+        FastK fkl = fk;
+        fkl.gthr = far ? 0xffffffffu : fk.gthr;
+#else
+        const FastK& fkl = fk;
+#endif
         const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
         bool sok = false;
         if (lane < ucount) {
@@ -448,16 +494,16 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       int is[4];                                                                               \
       is[0] = i0;                                                                              \
       for (int q = 1; q < 4; ++q) { is[q] = ustart + __ffs(sm) - 1; sm &= sm - 1; }            \
-      vote_slot<HSMEM, PSMEM, GP, 4>(p, fk, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
+      vote_slot<HSMEM, PSMEM, GP, 4>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
                                      j, lane, lanemask_lt);                                    \
     } else if (sm) {                                                                           \
       const int is[2] = {i0, ustart + __ffs(sm) - 1};                                          \
       sm &= sm - 1;                                                                            \
-      vote_slot<HSMEM, PSMEM, GP, 2>(p, fk, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
+      vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
                                      j, lane, lanemask_lt);                                    \
     } else {                                                                                   \
       const int is[1] = {i0};                                                                  \
-      vote_slot<HSMEM, PSMEM, GP, 1>(p, fk, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
+      vote_slot<HSMEM, PSMEM, GP, 1>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
                                      j, lane, lanemask_lt);                                    \
     }                                                                                          \
   }
