@@ -47,6 +47,9 @@
 #ifndef DSES_FAR_GTHR
 #define DSES_FAR_GTHR 1  // far lanes: all-ones guard threshold (c2 -5%)
 #endif
+#ifndef DSES_EXACT_INLINE
+#define DSES_EXACT_INLINE __forceinline__  // __noinline__: smaller code, BRA.DIV-guarded syncs
+#endif
 #ifndef DSES_CHUNKBOX
 #define DSES_CHUNKBOX 1
 #endif
@@ -138,7 +141,7 @@ __device__ __forceinline__ void hist_inc(unsigned* hist, uint32_t hist_sh, int l
 // lands in the same bin for the same i (_kernels.py:144-158).
 // Returns (votes << 16) | rechecks.
 template <bool HSMEM, bool PSMEM>
-__device__ __noinline__ unsigned vote_exact(const VoteParams& p, const double* R, const int4* P,
+__device__ DSES_EXACT_INLINE unsigned vote_exact(const VoteParams& p, const double* R, const int4* P,
                                             unsigned* hist, uint32_t hist_sh, int i, int j) {
   unsigned rechecks = 0;
   const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
@@ -156,15 +159,21 @@ __device__ __noinline__ unsigned vote_exact(const VoteParams& p, const double* R
 }
 
 // Flush a warp's deferred list (n entries, <= kRare) through vote_exact.
+// Inlined, with a warp-uniform trip count: ptxas then proves the warp
+// converged around the slot loop's shuffles / votes (a call into a
+// non-inlined divergent function made it guard each of them with BRA.DIV).
 template <bool HSMEM, bool PSMEM>
-__device__ __noinline__ unsigned flush_rare(const VoteParams& p, const double* R, const int4* P,
-                                            unsigned* hist, uint32_t hist_sh, uint32_t rare_sh,
-                                            int n, int lane) {
+__device__ DSES_EXACT_INLINE unsigned flush_rare(const VoteParams& p, const double* R,
+                                                 const int4* P, unsigned* hist, uint32_t hist_sh,
+                                                 uint32_t rare_sh, int n, int lane) {
   unsigned acc = 0;
   __syncwarp();
-  for (int e = lane; e < n; e += 32) {
-    const int2 ij = lds_v2(rare_sh + 8u * (unsigned)e);
-    acc += vote_exact<HSMEM, PSMEM>(p, R, P, hist, hist_sh, ij.x, ij.y);
+  for (int base = 0; base < n; base += 32) {
+    const int e = base + lane;
+    if (e < n) {
+      const int2 ij = lds_v2(rare_sh + 8u * (unsigned)e);
+      acc += vote_exact<HSMEM, PSMEM>(p, R, P, hist, hist_sh, ij.x, ij.y);
+    }
   }
   __syncwarp();
   return acc;
