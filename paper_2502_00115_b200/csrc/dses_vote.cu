@@ -50,6 +50,9 @@
 #ifndef DSES_EXACT_INLINE
 #define DSES_EXACT_INLINE __forceinline__  // __noinline__: smaller code, BRA.DIV-guarded syncs
 #endif
+#ifndef DSES_STAGE_SRC
+#define DSES_STAGE_SRC 1  // a unit's surviving sources staged per warp (no per-slot bit scans)
+#endif
 #ifndef DSES_CHUNKBOX
 #define DSES_CHUNKBOX 1
 #endif
@@ -119,6 +122,10 @@ __device__ __forceinline__ int4 lds_v4(uint32_t a) {
 }
 __device__ __forceinline__ void reds_add(uint32_t a, unsigned v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, const int4& v) {
+  asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
 }
 __device__ __forceinline__ void sts_v2(uint32_t a, int x, int y) {
   asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
@@ -264,15 +271,25 @@ template <bool HSMEM, bool PSMEM, int GP, int NS>
 __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, const double* R,
                                           const int4* P, uint32_t P_sh, unsigned* hist,
                                           uint32_t hist_sh, Lane& L, const int4& Y, int l0, int l1,
-                                          bool far, const int (&is)[NS], int j, int lane,
-                                          unsigned lanemask_lt) {
+                                          bool far, const int (&is_in)[NS], uint32_t src_sh,
+                                          int j, int lane, unsigned lanemask_lt) {
   // NS source points per call: their independent work interleaves and the
   // warp votes / loop overhead are shared.
   PairBin b[NS];
+  int is[NS];
   bool any = false;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
+#if DSES_STAGE_SRC
+    // the unit's surviving sources, staged (Pq, i) per warp: uniform address
+    const int4 Pi = lds_v4(src_sh + 16u * (unsigned)s);
+    is[s] = Pi.w;
+    (void)is_in;
+#else
+    is[s] = is_in[s];
     const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)is[s]) : __ldcg(&P[is[s]]);
+    (void)src_sh;
+#endif
     b[s] = fixed_bin(fk, Y, Pi);
     any |= b[s].cand;
   }
@@ -348,6 +365,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   int* units = reinterpret_cast<int*>(smem + off);  // [unit_cap] overlapping (group, unit) pairs
   off += (size_t)p.unit_cap * 4;
   int2* rare = reinterpret_cast<int2*>(smem + off) + warp * kRare;
+  off += (size_t)nwarps * kRare * 8;
+  int4* stage = reinterpret_cast<int4*>(smem + off) + warp * 32;  // a unit's surviving sources
+  const uint32_t stage_sh = (uint32_t)__cvta_generic_to_shared(stage);
 
   int* s_nunits = red + 96;
   int* s_next = red + 97;
@@ -487,14 +507,38 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 #endif
         const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
         bool sok = false;
+        int4 Pl = make_int4(0, 0, 0, 0);
         if (lane < ucount) {
-          const int4 Pl = PSMEM ? lds_v4(P_sh + 16u * (unsigned)(ustart + lane)) : __ldcg(&P[ustart + lane]);
+          Pl = PSMEM ? lds_v4(P_sh + 16u * (unsigned)(ustart + lane)) : __ldcg(&P[ustart + lane]);
           sok = exact_mode || ((yt.hi[0] - Pl.x >= 0) & (yt.lo[0] - Pl.x < (int)p.W0) &
                                (yt.hi[1] - Pl.y >= 0) & (yt.lo[1] - Pl.y < (int)p.W1) &
                                (yt.hi[2] - Pl.z >= 0) & (yt.lo[2] - Pl.z < (int)p.W2));
         }
         unsigned sm = __ballot_sync(0xffffffffu, sok);
         if (lane == 0) st_pairs += (unsigned long long)__popc(sm) * (unsigned)yt.count;
+#if DSES_STAGE_SRC
+        const int nsrc = __popc(sm);
+        __syncwarp();  // the previous unit's slots have read the stage
+        if (sok) sts_v4(stage_sh + 16u * (unsigned)__popc(sm & lanemask_lt),
+                        make_int4(Pl.x, Pl.y, Pl.z, ustart + lane));
+        __syncwarp();
+#else
+        (void)Pl;
+#endif
+#if DSES_STAGE_SRC
+#define DSES_SLOTS(GP)                                                                         \
+  for (int t = 0; t < nsrc; t += 2) {                                                          \
+    const int none[2] = {0, 0};                                                                \
+    if (t + 1 < nsrc) {                                                                        \
+      vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
+                                     none, stage_sh + 16u * (unsigned)t, j, lane, lanemask_lt);\
+    } else {                                                                                   \
+      const int one[1] = {0};                                                                  \
+      vote_slot<HSMEM, PSMEM, GP, 1>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
+                                     one, stage_sh + 16u * (unsigned)t, j, lane, lanemask_lt); \
+    }                                                                                          \
+  }
+#else
 #define DSES_SLOTS(GP)                                                                         \
   while (sm) {                                                                                 \
     const int i0 = ustart + __ffs(sm) - 1;                                                     \
@@ -504,18 +548,19 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       is[0] = i0;                                                                              \
       for (int q = 1; q < 4; ++q) { is[q] = ustart + __ffs(sm) - 1; sm &= sm - 1; }            \
       vote_slot<HSMEM, PSMEM, GP, 4>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
-                                     j, lane, lanemask_lt);                                    \
+                                     0u, j, lane, lanemask_lt);                                    \
     } else if (sm) {                                                                           \
       const int is[2] = {i0, ustart + __ffs(sm) - 1};                                          \
       sm &= sm - 1;                                                                            \
       vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
-                                     j, lane, lanemask_lt);                                    \
+                                     0u, j, lane, lanemask_lt);                                    \
     } else {                                                                                   \
       const int is[1] = {i0};                                                                  \
       vote_slot<HSMEM, PSMEM, GP, 1>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
-                                     j, lane, lanemask_lt);                                    \
+                                     0u, j, lane, lanemask_lt);                                    \
     }                                                                                          \
   }
+#endif
         if (gp == 0) { DSES_SLOTS(0) }
         else if (gp == 1) { DSES_SLOTS(1) }
         else { DSES_SLOTS(2) }
@@ -627,6 +672,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
   if (psmem) b += (size_t)p.n_pad * 16;
   b += (size_t)(p.nxt + (p.nxt + 31) / 32) * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)p.unit_cap * 4;
   b += (size_t)(threads / 32) * kRare * 8;
+  b += (size_t)(threads / 32) * 32 * 16;  // per-warp staged sources
   return b;
 }
 
