@@ -802,6 +802,34 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       if (!far) T.gm = std::max(T.gm, ne);
       yq[q].w = far ? kFarFlag : w;
     }
+#if DSES_SAFE_LANES
+    // unused partner slots (below the group's shuffle count gm) -> a safe
+    // lane: an empty lane of the group, else the first non-far point that is
+    // no dedup partner of q; a point without one takes the exact path
+    if (T.gm > 0) {
+      for (int q = T.start; q < T.start + T.count; ++q) {
+        if (yq[q].w & kFarFlag) continue;
+        int ne = 0;
+        while (ne < 2 && ((yq[q].w >> (6 * ne)) & 63)) ++ne;
+        if (ne >= T.gm) continue;
+        int safe = -1;
+        if (T.count < kTile) {
+          safe = T.count;  // empty lane: key -1 in every slot
+        } else {
+          for (int c = 0; c < T.count && safe < 0; ++c) {
+            const int q2 = T.start + c;
+            if (q2 == q || (yq[q2].w & kFarFlag)) continue;
+            bool partner = false;
+            for (int a = aoff[yidx[q]]; a < aoff[yidx[q] + 1] && !partner; ++a)
+              partner = pos[aidx[a]] == q2;
+            if (!partner) safe = c;
+          }
+        }
+        if (safe < 0) { yq[q].w = kFarFlag; continue; }
+        for (; ne < T.gm; ++ne) yq[q].w |= (safe + 1) << (6 * ne);
+      }
+    }
+#endif
   }
   if (yt.size() >= 65536 || xt.size() >= 65536)
     return fail(DSES_E_INVALID, "cloud too large for the 16-bit work-unit encoding");

@@ -38,6 +38,13 @@ constexpr int kDenseMaxBins = 1 << 26;  // beyond: sort-based (sparse) mode quer
 constexpr int kNoRef = -3 * (1 << 29);
 constexpr int kMaxComp = 16;     // dedup components up to this size stay in one warp
 constexpr int kFarFlag = 1 << 12; // Yq.w: the point's dedup needs the exact path
+#ifndef DSES_SAFE_LANES
+// Partner slots a lane does not use hold a "safe" lane of its group (an
+// empty lane, or a point that is no dedup partner of it: it can never be
+// decided in the same bin for the same source), so the vote kernel shuffles
+// unconditionally instead of testing l >= 0 per pair.
+#define DSES_SAFE_LANES 1
+#endif
 #ifndef DSES_VOTE_THREADS
 #define DSES_VOTE_THREADS 768
 #endif

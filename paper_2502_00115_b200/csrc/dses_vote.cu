@@ -311,12 +311,22 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
     if (GP > 0) {
       const int key = decided ? (int)b[s].lin : (b[s].near ? -2 : -1);
       const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
+#if DSES_SAFE_LANES
+      bool dup = k0 == key;  // l0 is always a lane: a partner or a safe one
+      bool und = k0 == -2;
+#else
       bool dup = (l0 >= 0) & (k0 == key);
       bool und = (l0 >= 0) & (k0 == -2);
+#endif
       if (GP > 1) {
         const int k1 = __shfl_sync(0xffffffffu, key, l1 & 31);
+#if DSES_SAFE_LANES
+        dup |= k1 == key;
+        und |= k1 == -2;
+#else
         dup |= (l1 >= 0) & (k1 == key);
         und |= (l1 >= 0) & (k1 == -2);
+#endif
       }
       dup &= decided;
 #if DSES_FAR_GTHR
@@ -518,8 +528,12 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         if (lane == 0) st_pairs += (unsigned long long)__popc(sm) * (unsigned)yt.count;
 #if DSES_STAGE_SRC
         const int nsrc = __popc(sm);
+        // opaque copy: keeps the stage base in a register (otherwise it is
+        // re-derived from kernel parameters in every slot)
+        uint32_t sbase;
+        asm volatile("mov.u32 %0, %1;" : "=r"(sbase) : "r"(stage_sh));
         __syncwarp();  // the previous unit's slots have read the stage
-        if (sok) sts_v4(stage_sh + 16u * (unsigned)__popc(sm & lanemask_lt),
+        if (sok) sts_v4(sbase + 16u * (unsigned)__popc(sm & lanemask_lt),
                         make_int4(Pl.x, Pl.y, Pl.z, ustart + lane));
         __syncwarp();
 #else
@@ -531,11 +545,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     const int none[2] = {0, 0};                                                                \
     if (t + 1 < nsrc) {                                                                        \
       vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
-                                     none, stage_sh + 16u * (unsigned)t, j, lane, lanemask_lt);\
+                                     none, sbase + 16u * (unsigned)t, j, lane, lanemask_lt);\
     } else {                                                                                   \
       const int one[1] = {0};                                                                  \
       vote_slot<HSMEM, PSMEM, GP, 1>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
-                                     one, stage_sh + 16u * (unsigned)t, j, lane, lanemask_lt); \
+                                     one, sbase + 16u * (unsigned)t, j, lane, lanemask_lt); \
     }                                                                                          \
   }
 #else
