@@ -41,9 +41,6 @@
 #ifndef DSES_FRAC_IMAD
 #define DSES_FRAC_IMAD 1  // fractions on the multiply pipe (ALU-pipe relief, c2 -2.5%)
 #endif
-#ifndef DSES_VOTE_IMAD
-#define DSES_VOTE_IMAD 0
-#endif
 #ifndef DSES_FAR_GTHR
 #define DSES_FAR_GTHR 1  // far lanes: all-ones guard threshold (c2 -5%)
 #endif
@@ -199,6 +196,13 @@ struct Lane {          // per-warp deferred list state (warp-uniform)
   unsigned rechecks;
 };
 
+// Generic pointers of the exact path, published once per CTA: the slot loop
+// reads them only when it flushes (otherwise the compiler re-derives them
+// from kernel parameters in every slot).
+__shared__ const double* g_exR;
+__shared__ const int4* g_exP;
+__shared__ unsigned* g_exH;
+
 // Append the lanes in `dm` (pairs (i, j)) to the warp's exact-path list.
 template <bool HSMEM, bool PSMEM>
 __device__ __forceinline__ void defer_pairs(const VoteParams& p, const double* R, const int4* P,
@@ -207,9 +211,11 @@ __device__ __forceinline__ void defer_pairs(const VoteParams& p, const double* R
   if (mine) sts_v2(L.rare_sh + 8u * (unsigned)(L.nrare + __popc(dm & lanemask_lt)), i, j);
   L.nrare += __popc(dm);
   if (L.nrare > kRare - 32) {
-    L.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L.rare_sh, L.nrare, lane) & 0xffffu;
+    L.rechecks += flush_rare<HSMEM, PSMEM>(p, g_exR, g_exP, g_exH, hist_sh, L.rare_sh, L.nrare,
+                                           lane) & 0xffffu;
     L.nrare = 0;
   }
+  (void)R; (void)P; (void)hist;
 }
 
 // Fast-path constants in per-lane registers.
@@ -217,7 +223,6 @@ struct FastK {
   unsigned W0, W1, W2, fmask, gthr, d1, d2;
   int F;
   unsigned negP;  // -(2^F): fraction = u + (u >> F) * negP on the multiply pipe
-  unsigned c_ffff;  // 0xffff, opaque to the compiler (vote value by IMAD)
 };
 
 // Fixed-point decision for one pair: candidate (inside the guard-extended
@@ -247,15 +252,9 @@ __device__ __forceinline__ PairBin fixed_bin(const FastK& k, const int4& Y, cons
 
 template <bool HSMEM>
 __device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsigned lin, bool ok,
-                                        unsigned nbins = 0xffffffffu, unsigned c_ffff = 0xffffu) {
+                                        unsigned nbins = 0xffffffffu) {
   DSES_ASSERT(!ok || lin < nbins);
-#if DSES_VOTE_IMAD
-  // 1 or 0x10000 as (lin & 1) * 0xffff + 1 with the 0xffff from shared memory
-  // (a runtime multiplier stays an IMAD on the multiply pipe)
-  if (HSMEM) reds_add_if(hist_sh + ((lin >> 1) << 2), (lin & 1u) * c_ffff + 1u, ok);
-#else
   if (HSMEM) reds_add_if(hist_sh + ((lin >> 1) << 2), 1u << ((lin & 1u) << 4), ok);
-#endif
   else if (ok) atomicAdd(&hist[lin], 1u);
 }
 
@@ -337,7 +336,7 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
       defer[s] = b[s].near | (decided & !dup & (far | und));
 #endif
     }
-    vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins, fk.c_ffff);
+    vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins);
     DSES_ASSERT(is[s] >= 0 && is[s] < p.n && j >= 0 && j < p.m_pad);
     anydef |= defer[s];
   }
@@ -385,21 +384,24 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   const uint32_t P_sh = PSMEM ? (uint32_t)__cvta_generic_to_shared(P) : 0u;
   // fast-path constants through shared memory: loaded into regular registers
   // once, instead of being re-loaded into uniform registers in the hot loop
-  __shared__ unsigned kc[11];
+  __shared__ unsigned kc[10];
   if (tid == 0) {
     kc[0] = p.W0; kc[1] = p.W1; kc[2] = p.W2; kc[3] = p.fmask; kc[4] = p.gthr;
     kc[5] = (unsigned)p.d1; kc[6] = (unsigned)p.d2; kc[7] = (unsigned)p.F;
     kc[8] = HSMEM ? (uint32_t)__cvta_generic_to_shared(hist) : 0u;
     kc[9] = 0u - (1u << p.F);
-    kc[10] = 0xffffu;
+    g_exR = R;
+    g_exP = P;
+    g_exH = hist;
   }
   __syncthreads();
   FastK fk;
   fk.W0 = kc[0]; fk.W1 = kc[1]; fk.W2 = kc[2]; fk.fmask = kc[3]; fk.gthr = kc[4];
-  fk.d1 = kc[5]; fk.d2 = kc[6]; fk.F = (int)kc[7]; fk.negP = kc[9]; fk.c_ffff = kc[10];
+  fk.d1 = kc[5]; fk.d2 = kc[6]; fk.F = (int)kc[7]; fk.negP = kc[9];
   const uint32_t hist_sh = kc[8];
   Lane L;
-  L.rare_sh = (uint32_t)__cvta_generic_to_shared(rare);
+  // opaque copy: a register, not re-derived from kernel parameters per slot
+  asm volatile("mov.u32 %0, %1;" : "=r"(L.rare_sh) : "r"((uint32_t)__cvta_generic_to_shared(rare)));
   L.nrare = 0;
   L.rechecks = 0;
 
