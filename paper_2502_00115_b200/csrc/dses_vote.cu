@@ -32,7 +32,7 @@
 #include "dses_common.cuh"
 
 #ifndef DSES_NS4
-#define DSES_NS4 0  // four source points per slot (measured slower at 768 threads)
+#define DSES_NS4 1  // four staged source points per slot while at least four remain
 #endif
 
 #ifndef DSES_DYNROT
@@ -543,7 +543,14 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 #endif
 #if DSES_STAGE_SRC
 #define DSES_SLOTS(GP)                                                                         \
-  for (int t = 0; t < nsrc; t += 2) {                                                          \
+  int t = 0;                                                                                   \
+  if (DSES_NS4)                                                                                \
+    for (; t + 3 < nsrc; t += 4) {                                                             \
+      const int four[4] = {0, 0, 0, 0};                                                        \
+      vote_slot<HSMEM, PSMEM, GP, 4>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
+                                     four, sbase + 16u * (unsigned)t, j, lane, lanemask_lt);   \
+    }                                                                                          \
+  for (; t < nsrc; t += 2) {                                                                   \
     const int none[2] = {0, 0};                                                                \
     if (t + 1 < nsrc) {                                                                        \
       vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
