@@ -46,7 +46,7 @@ constexpr int kFarFlag = 1 << 12; // Yq.w: the point's dedup needs the exact pat
 #define DSES_SAFE_LANES 1
 #endif
 #ifndef DSES_VOTE_THREADS
-#define DSES_VOTE_THREADS 768
+#define DSES_VOTE_THREADS 1024
 #endif
 constexpr int kVoteThreads = DSES_VOTE_THREADS;
 
