@@ -194,6 +194,20 @@ def dses(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationR
     return _result(prep, cfg, res, t0)
 
 
+_BUILD_POOL = None
+
+
+def _build_pool():
+    """One persistent plan-construction thread: its upload stream and pinned
+    staging buffer (per host thread in the C ABI) are created once, not on
+    every dses_batch call."""
+    global _BUILD_POOL
+    if _BUILD_POOL is None:
+        import concurrent.futures as cf
+        _BUILD_POOL = cf.ThreadPoolExecutor(max_workers=1, thread_name_prefix="dses-plan")
+    return _BUILD_POOL
+
+
 def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     """dses over a batch of (source, reference) pairs (the registration loop of
     harness.run_batch, harness.py:145-162), pipelined: the host preparation
@@ -202,8 +216,6 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     pair k, and search k+1 is queued before the result of k is read, so the
     GPU runs the searches back to back.  Results are identical to calling
     dses() on each pair; errors are raised for the first failing pair."""
-    import concurrent.futures as cf
-
     pairs = list(zip(sources, references))
     out = []
     if not pairs:
@@ -213,33 +225,34 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     pending = None  # (t0, prep, grid, plan) whose search is queued on the GPU
     streams = [_native.Stream(device), _native.Stream(device)]  # alternate: the
     # vote of k+1 fills the SMs that k's last rotations and score stage leave idle
+    ex = _build_pool()
+    fut = ex.submit(_build, pairs[0][0], pairs[0][1], cfg, device)  # not yet consumed
     try:
-        with cf.ThreadPoolExecutor(max_workers=1) as ex:
-            fut = ex.submit(_build, pairs[0][0], pairs[0][1], cfg, device)
-            for k in range(len(pairs) + 1):
-                item, err = None, None
-                if k < len(pairs):
-                    try:
-                        item = fut.result()
-                        if k + 1 < len(pairs):
-                            fut = ex.submit(_build, pairs[k + 1][0], pairs[k + 1][1], cfg, device)
-                        _, prep, grid, plan = item
-                        plan.search_async(grid, cfg.q, prep.code, prep.param, prep.skip_refine,
-                                          stream=streams[k % 2].handle)
-                    except Exception as exc:  # raised after pair k-1's own outcome
-                        if item is not None:
-                            item[3].close()
-                        item, err = None, exc
-                prev, pending = pending, item
-                if prev is not None:
-                    t0, prep, grid, plan = prev
-                    try:
-                        res = plan.search_wait()
-                    finally:
-                        plan.close()
-                    out.append(_result(prep, cfg, res, t0))
-                if err is not None:
-                    raise err
+        for k in range(len(pairs) + 1):
+            item, err = None, None
+            if k < len(pairs):
+                try:
+                    cur, fut = fut, None
+                    item = cur.result()
+                    if k + 1 < len(pairs):
+                        fut = ex.submit(_build, pairs[k + 1][0], pairs[k + 1][1], cfg, device)
+                    _, prep, grid, plan = item
+                    plan.search_async(grid, cfg.q, prep.code, prep.param, prep.skip_refine,
+                                      stream=streams[k % 2].handle)
+                except Exception as exc:  # raised after pair k-1's own outcome
+                    if item is not None:
+                        item[3].close()
+                    item, err = None, exc
+            prev, pending = pending, item
+            if prev is not None:
+                t0, prep, grid, plan = prev
+                try:
+                    res = plan.search_wait()
+                finally:
+                    plan.close()
+                out.append(_result(prep, cfg, res, t0))
+            if err is not None:
+                raise err
     finally:
         if pending is not None:
             try:
@@ -247,6 +260,11 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
             except Exception:
                 pass
             pending[3].close()
+        if fut is not None:  # a prefetched plan nobody will use
+            try:
+                fut.result()[3].close()
+            except Exception:
+                pass
         for st in streams:
             st.close()
     return out
