@@ -396,6 +396,34 @@ __global__ void __launch_bounds__(kScreenThreads) screen_grid_kernel(ScoreParams
 // LDS feeds kScanCands distance evaluations).
 // ---------------------------------------------------------------------------
 constexpr int kScanCands = 4;
+#ifndef DSES_SCAN_F32X2
+#define DSES_SCAN_F32X2 1
+#endif
+// f32x2 helpers (sm_100 packed single precision)
+__device__ __forceinline__ unsigned long long pack_f2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack_f2(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long sub_f2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul_f2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fma_f2(unsigned long long a, unsigned long long b,
+                                                     unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
 
 template <bool L2>
 __global__ void __launch_bounds__(kScreenThreads) screen_scan_kernel(ScoreParams s, const int64_t* rows,
@@ -433,6 +461,39 @@ __global__ void __launch_bounds__(kScreenThreads) screen_scan_kernel(ScoreParams
     __syncthreads();
     for (int k = threadIdx.x; k < cnt; k += kScreenThreads) ych[k] = s.ysf[base + k];
     __syncthreads();
+#if DSES_SCAN_F32X2
+    // candidate pairs packed in f32x2 registers (FADD2 / FMUL2 / FFMA2: one
+    // instruction per two candidates, same IEEE rounding as the scalar ops)
+    unsigned long long PX[kScanCands / 2], PY[kScanCands / 2], PZ[kScanCands / 2];
+#pragma unroll
+    for (int h = 0; h < kScanCands / 2; ++h) {
+      PX[h] = pack_f2(px[2 * h], px[2 * h + 1]);
+      PY[h] = pack_f2(py[2 * h], py[2 * h + 1]);
+      PZ[h] = pack_f2(pz[2 * h], pz[2 * h + 1]);
+    }
+#pragma unroll 4
+    for (int k = 0; k < cnt; ++k) {
+      const float4 y = ych[k];
+      const unsigned long long yx = pack_f2(y.x, y.x), yy = pack_f2(y.y, y.y), yz = pack_f2(y.z, y.z);
+#pragma unroll
+      for (int h = 0; h < kScanCands / 2; ++h) {
+        const unsigned long long a = sub_f2(yx, PX[h]), b = sub_f2(yy, PY[h]), d = sub_f2(yz, PZ[h]);
+        float lo, hi;
+        if (L2) {
+          unpack_f2(fma_f2(d, d, fma_f2(b, b, mul_f2(a, a))), lo, hi);
+        } else {
+          float a0, a1, b0, b1, d0, d1;
+          unpack_f2(a, a0, a1);
+          unpack_f2(b, b0, b1);
+          unpack_f2(d, d0, d1);
+          lo = fabsf(a0) + fabsf(b0) + fabsf(d0);
+          hi = fabsf(a1) + fabsf(b1) + fabsf(d1);
+        }
+        best[2 * h] = fminf(best[2 * h], lo);
+        best[2 * h + 1] = fminf(best[2 * h + 1], hi);
+      }
+    }
+#else
 #pragma unroll 4
     for (int k = 0; k < cnt; ++k) {
       const float4 y = ych[k];
@@ -442,6 +503,7 @@ __global__ void __launch_bounds__(kScreenThreads) screen_scan_kernel(ScoreParams
         best[q] = fminf(best[q], L2 ? fmaf(d, d, fmaf(b, b, a * a)) : fabsf(a) + fabsf(b) + fabsf(d));
       }
     }
+#endif
   }
 #pragma unroll
   for (int q = 0; q < kScanCands; ++q) {
