@@ -68,3 +68,33 @@ def test_property_dses_matches_oracle(seed, n, m, kind, k_rot, k_trans):
     assert res.best_inliers == ref["best_inliers"]
     assert res.candidates_evaluated == ref["candidates_evaluated"]
     assert res.candidates_refined == ref["candidates_refined"]
+
+
+PROPERTY_EXAMPLES = int(__import__("os").environ.get("DSES_PROPERTY_EXAMPLES", "25"))
+
+
+@settings(max_examples=PROPERTY_EXAMPLES, deadline=None, derandomize=True,
+          suppress_health_check=list(HealthCheck))
+@given(seed=st.integers(0, 2**31 - 1), clusters=st.integers(2, 70), per=st.integers(1, 14),
+       spread=st.floats(0.05, 1.5), n=st.integers(1, 200), b=st.floats(0.02, 0.2),
+       k_trans=st.integers(1, 12))
+def test_property_dense_dedup_votes_match_oracle(seed, clusters, per, spread, n, b, k_trans):
+    """Dedup-heavy lattices: clusters of up to 14 reference points within
+    about a bin of each other (many dedup partners per lane, full 32-lane
+    groups whose unused partner slots need a safe lane, components beyond a
+    warp's reach -> far lanes), arbitrary windows; every rotation's (count,
+    bin, ties) equals the pinned oracle's."""
+    from oracle import oracle as O
+    from paper_2502_00115_b200 import _native
+    rng = np.random.default_rng(seed)
+    centres = rng.normal(size=(clusters, 3)) * 0.4
+    y = np.repeat(centres, per, axis=0) + rng.uniform(-spread, spread, (clusters * per, 3)) * b
+    x = rng.normal(size=(n, 3)) * 0.4
+    ilo = np.full(3, -k_trans, dtype=np.int64)
+    dims = np.full(3, 2 * k_trans + 1, dtype=np.int64)
+    k = 3
+    rots = O.rotation_grid(k, math.radians(20) / k)[rng.choice((2 * k + 1) ** 3, 12)]
+    with _native.Plan(x, y, b, ilo, dims) as plan:
+        c, l, t = plan.mode_batch(rots)
+    oc, ol, ot = O.mode_batch(x, y, b, ilo, dims, rots=rots)
+    assert np.array_equal(c, oc) and np.array_equal(l, ol) and np.array_equal(t, ot)
