@@ -50,6 +50,9 @@
 #ifndef DSES_STAGE_SRC
 #define DSES_STAGE_SRC 1  // a unit's surviving sources staged per warp (no per-slot bit scans)
 #endif
+#ifndef DSES_POP_DENSE
+#define DSES_POP_DENSE 1  // units per claim when the round's overlap is dense
+#endif
 #ifndef DSES_CHUNKBOX
 #define DSES_CHUNKBOX 1
 #endif
@@ -493,7 +496,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       // sparse overlap (< 1/4 of the round's (group, unit) pairs) means light
       // units: claim DSES_POP at a time to amortise the claim; dense overlap
       // (heavy units) claims one at a time to keep the round's tail balanced
-      const int kpop = (4 * nunits < (b1 - b0) * p.nxt) ? DSES_POP : 1;
+      const int kpop = (4 * nunits < (b1 - b0) * p.nxt) ? DSES_POP : DSES_POP_DENSE;
       for (int u = nunits, uend = nunits;; ++u) {
         if (u >= uend) {  // claim the next kpop units
           if (lane == 0) u = atomicAdd(s_next, kpop);
