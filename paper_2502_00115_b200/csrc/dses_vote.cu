@@ -53,6 +53,9 @@
 #ifndef DSES_POP_DENSE
 #define DSES_POP_DENSE 1  // units per claim when the round's overlap is dense
 #endif
+#ifndef DSES_B1_MASKS
+#define DSES_B1_MASKS 1  // per-group chunk masks computed one thread per group
+#endif
 #ifndef DSES_CHUNKBOX
 #define DSES_CHUNKBOX 1
 #endif
@@ -417,7 +420,14 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   unsigned long long st_pairs = 0, st_votes = 0;
   const bool exact_mode = (p.F == 0);
   // reference groups per round so that the round's units fit `units`
+#if DSES_B1_MASKS
+  // reference groups per round so that the round's units AND one chunk mask
+  // per group (stored at the tail of `units`) fit
+  const int tiles_per_round = max(1, p.unit_cap / max(1, p.nxt + 1));
+  const bool masks = DSES_CHUNKBOX && !exact_mode && nxc > 1 && nxc <= 32;
+#else
   const int tiles_per_round = max(1, p.unit_cap / max(1, p.nxt));
+#endif
 
   // rotations: the first one static, the rest from a global queue (the cost
   // of a rotation varies with its angle; dynamic claims balance the tail)
@@ -472,9 +482,38 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     for (int b0 = 0; b0 < p.nyt; b0 += tiles_per_round) {
       const int b1 = min(p.nyt, b0 + tiles_per_round);
       if (tid == 0) { *s_nunits = 0; *s_next = 0; }
+#if DSES_B1_MASKS
+      // which 32-unit chunks each group can reach: one thread per group
+      // (instead of a warp-uniform test per (group, chunk))
+      unsigned* gmask = reinterpret_cast<unsigned*>(units) + (p.unit_cap - tiles_per_round);
+      if (masks)
+        for (int k = tid; k < b1 - b0; k += nthreads) {
+          const YTile yg = load_ytile(p.yt, b0 + k);
+          unsigned mk = 0;
+          for (int c = 0; c < nxc; ++c)
+            if (boxes_meet(p, yg, CB[2 * c], CB[2 * c + 1])) mk |= 1u << c;
+          gmask[k] = mk;
+        }
+#endif
       __syncthreads();
       for (int b = b0 + warp; b < b1; b += nwarps) {
         const YTile yt = load_ytile(p.yt, b);
+#if DSES_B1_MASKS
+        if (masks) {
+          for (unsigned mk = gmask[b - b0]; mk; mk &= mk - 1) {
+            const int a = 32 * (__ffs(mk) - 1) + lane;
+            const bool ov = a < p.nxt && boxes_meet(p, yt, XB[2 * a], XB[2 * a + 1]);
+            const unsigned m = __ballot_sync(0xffffffffu, ov);
+            if (m) {
+              int slot = 0;
+              if (lane == 0) slot = atomicAdd(s_nunits, __popc(m));
+              slot = __shfl_sync(0xffffffffu, slot, 0);
+              if (ov) units[slot + __popc(m & lanemask_lt)] = (b << 16) | a;
+            }
+          }
+          continue;
+        }
+#endif
         for (int a0 = 0; a0 < p.nxt; a0 += 32) {
           // whole chunk outside the group's reach: one warp-uniform test
           if (DSES_CHUNKBOX && nxc > 1 && !exact_mode &&
