@@ -34,6 +34,7 @@ cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, i
                         cudaStream_t stream);
 int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int threads);
 size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads);
+size_t vote_static_smem();
 // dses_sparse.cu
 size_t sparse_scratch_bytes(int64_t n, int64_t m);
 cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t r_count,
@@ -910,7 +911,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.unit_cap = kUnitCapMin;
   const size_t fixed = vote_smem_bytes(v, false, false, P->vote_threads);
   const size_t hb = (size_t)v.hist_words * 4, pb = (size_t)v.n_pad * 16;
-  const size_t lim = P->smem_optin - 256;  // static shared memory of the vote kernel
+  static const size_t static_smem = (vote_static_smem() + 127) & ~size_t(127);
+  const size_t lim = P->smem_optin - std::max<size_t>(static_smem, 256);  // minus the kernel's static shared memory
   P->hsmem = v.count16 && fixed + hb <= lim;
   if (!P->hsmem) {  // global-memory histograms always use 32-bit counts
     v.count16 = 0;

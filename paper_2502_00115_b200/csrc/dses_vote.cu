@@ -758,6 +758,18 @@ cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, i
   return cudaGetLastError();
 }
 
+// Static shared memory of the vote kernel (kc[], exact-path pointers, ...):
+// the dynamic part is sized against opt-in limit minus this.
+size_t vote_static_smem() {
+  cudaFuncAttributes a{};
+  size_t m = 0;
+  if (cudaFuncGetAttributes(&a, vote_kernel<true, true>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<true, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<false, true>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<false, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  return m;
+}
+
 int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int threads) {
   const size_t smem = vote_smem_bytes(p, hsmem, psmem, threads);
   int n = 0;
