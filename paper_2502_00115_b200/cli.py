@@ -6,6 +6,14 @@ harness.register_files harness.py:285-322) on the B200: same flags
 --trans-range/--trans-bin; --metric trunc-l1|l2|l1|inliers, --trunc, --q;
 --center-pose JSON; --exhaustive; --out; --json), same report keys and exit
 codes (0 ok, 1 engine error, 2 input / I/O error).  --device picks the GPU.
+
+``benchmark --instances PREFIX... --search FILE`` is the reference's
+``gridreg benchmark`` (cli.py:64-79, 176-197: harness.run_batch, CSV / JSON
+reports, summary lines) over instance files (``<prefix>_source.xyz``,
+``<prefix>_reference.xyz``, ``<prefix>_gt.json`` as written by the
+reference's ``gridreg generate`` / ``benchgen.save_instance``) instead of
+the in-process scenario generator (benchgen is out of scope): trial k is
+the k-th prefix, its seed and shape come from the sidecar's config.
 """
 from __future__ import annotations
 
@@ -40,6 +48,17 @@ def _parser():
     p.add_argument("--exhaustive", action="store_true")
     p.add_argument("--out", metavar="FILE")
     p.add_argument("--json", action="store_true")
+    p = sub.add_parser("benchmark", help="run a batch of registration trials on instance files")
+    p.add_argument("--instances", required=True, nargs="+", metavar="PREFIX",
+                   help="instance prefixes (PREFIX_source.xyz, PREFIX_reference.xyz, PREFIX_gt.json)")
+    p.add_argument("--search", required=True, metavar="FILE", help="search config JSON")
+    p.add_argument("--csv", metavar="FILE", help="write per-trial rows here")
+    p.add_argument("--json", metavar="FILE", dest="json_out",
+                   help="write full report (incl. timings) here")
+    p.add_argument("--rot-tol-deg", type=float, default=1.0,
+                   help="recall threshold on mean Euler error (default 1)")
+    p.add_argument("--trans-tol", type=float, default=0.1,
+                   help="recall threshold on mean translation error (default 0.1)")
     return ap
 
 
@@ -130,10 +149,34 @@ def _register(args) -> int:
     return 0
 
 
+def _benchmark(args) -> int:
+    from .harness import register_batch, search_from_json, write_batch_csv, write_batch_json
+    from .pcio import load_instance
+
+    search = search_from_json(args.search)
+    insts = [load_instance(p) for p in args.instances]
+    summary, records = register_batch(
+        [i.source for i in insts], [i.reference for i in insts], [i.gt_aligner for i in insts],
+        search, rot_tol_deg=args.rot_tol_deg, trans_tol=args.trans_tol, device=args.device,
+        seeds=[int(i.config.get("rng_seed", k)) for k, i in enumerate(insts)],
+        shapes=[str(i.config.get("shape", "file")) for i in insts])
+    if args.csv:
+        write_batch_csv(args.csv, records)
+    if args.json_out:
+        write_batch_json(args.json_out, insts[0].config, search, summary, records)
+    print(f"trials: {summary.n_trials}  failed: {summary.n_failed}")
+    print(f"recall: {summary.recall:.3f}")
+    if summary.mean_mie_r is not None:
+        print(f"mean rotation error (deg): {summary.mean_mie_r:.4f}")
+        print(f"mean translation error (m): {summary.mean_mie_t:.5f}")
+        print(f"median time (ms): {summary.median_total_ms:.1f}")
+    return 0
+
+
 def main(argv=None) -> int:
     args = _parser().parse_args(argv)
     try:
-        return _register(args)
+        return _benchmark(args) if args.command == "benchmark" else _register(args)
     except (FileNotFoundError, IsADirectoryError, PermissionError, PointCloudIOError,
             InvalidInputError, json.JSONDecodeError) as exc:
         print(f"error: {exc}", file=sys.stderr)

@@ -11,15 +11,22 @@ Same formats, results and exceptions as the reference's gridreg/pcio.py
   before it are skipped when their record size is fixed, list properties in
   or before the vertex element are rejected.
 * ``write_xyz``: 9 significant digits per coordinate.
+* Registration instances (benchgen.py:370-411): ``<prefix>_source.xyz``,
+  ``<prefix>_reference.xyz`` and the JSON sidecar ``<prefix>_gt.json`` with
+  the ground-truth source transform, its inverse (the aligner a registration
+  should recover) and the scenario config, byte-identical to the reference's
+  ``save_instance``; ``load_instance`` reads files written by either.
 """
 from __future__ import annotations
 
+import json
 import os
+from dataclasses import dataclass
 
 import numpy as np
 
 from .errors import PointCloudIOError
-from .geometry import as_point_cloud
+from .geometry import RigidTransform, as_point_cloud
 
 # PLY scalar type -> numpy little-endian dtype
 _TYPES = {}
@@ -150,3 +157,63 @@ def read_ply(path) -> np.ndarray:
 def read_point_cloud(path) -> np.ndarray:
     """By extension: .ply -> read_ply, anything else -> read_xyz."""
     return read_ply(path) if str(path).lower().endswith(".ply") else read_xyz(path)
+
+
+@dataclass(frozen=True)
+class Instance:
+    """One registration problem (benchgen.ScenarioInstance, benchgen.py:108-119):
+    `source` is the reference cloud moved by `source_transform` (plus noise
+    and crop); `config` is the scenario config as a dict (the generator itself
+    is out of scope)."""
+    source: np.ndarray
+    reference: np.ndarray
+    source_transform: RigidTransform
+    config: dict
+
+    @property
+    def gt_aligner(self) -> RigidTransform:
+        """The transform mapping the source back onto the reference frame."""
+        return self.source_transform.inverse()
+
+
+def _pose_json(tf: RigidTransform) -> dict:
+    return {"rotation": [[float(v) for v in row] for row in tf.rotation],
+            "translation": [float(v) for v in tf.translation]}
+
+
+def save_instance(instance: Instance, prefix) -> dict:
+    """benchgen.save_instance (benchgen.py:370-394): the two clouds as XYZ and
+    the sidecar (indent 2, sorted keys, trailing newline).  Returns the
+    written paths under the keys "source", "reference", "sidecar"."""
+    paths = {"source": f"{prefix}_source.xyz", "reference": f"{prefix}_reference.xyz",
+             "sidecar": f"{prefix}_gt.json"}
+    write_xyz(paths["source"], instance.source)
+    write_xyz(paths["reference"], instance.reference)
+    side = {"source_transform": _pose_json(instance.source_transform),
+            "gt_aligner": _pose_json(instance.gt_aligner),
+            "config": dict(instance.config)}
+    with open(paths["sidecar"], "w", encoding="utf-8") as fh:
+        json.dump(side, fh, indent=2, sort_keys=True)
+        fh.write("\n")
+    return paths
+
+
+def load_instance(prefix) -> Instance:
+    """benchgen.load_instance (benchgen.py:397-411): the source transform is
+    read from the sidecar (the aligner is recomputed as its inverse, as the
+    reference does); a pose that is not a rigid transform raises
+    InvalidInputError as in the reference, a sidecar missing its keys
+    PointCloudIOError."""
+    path = f"{prefix}_gt.json"
+    with open(path, "r", encoding="utf-8") as fh:
+        side = json.load(fh)
+    try:
+        st = side["source_transform"]
+        tf = RigidTransform(np.array(st["rotation"], dtype=np.float64),
+                            np.array(st["translation"], dtype=np.float64))
+        cfg = dict(side["config"])
+    except (KeyError, TypeError) as exc:  # the reference lets these escape
+        raise PointCloudIOError(f"{path}: malformed instance sidecar ({exc!r})") from exc
+    return Instance(source=read_xyz(f"{prefix}_source.xyz"),
+                    reference=read_xyz(f"{prefix}_reference.xyz"),
+                    source_transform=tf, config=cfg)

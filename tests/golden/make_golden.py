@@ -434,10 +434,44 @@ def make_histo():
                 [np.nan if c.refined_error is None else c.refined_error for c in out])
     save("histo", rec)
 
+def make_instances():
+    """benchgen.save_instance files of three small instances (byte-exact
+    sidecar / XYZ fixtures) and the reference's batch CSV for them:
+    harness._run_one on benchgen.load_instance of the written files, then
+    harness.write_batch_csv (what `gridreg benchmark` writes)."""
+    import json
+    import tempfile
+    from dataclasses import replace
+    from gridreg import harness
+    search = SearchConfig(k_rot=3, rot_step=math.radians(5.0), k_trans=16, trans_bin=0.03)
+    base = benchgen.ScenarioConfig(shape="blob", points_pool=600, points_reference=300,
+                                   points_source=260, rot_range_deg=12.0, trans_range=0.3,
+                                   rng_seed=40)
+    files, recs = [], []
+    with tempfile.TemporaryDirectory() as tmp:
+        for k in range(3):
+            inst = benchgen.make_instance(replace(base, rng_seed=40 + k,
+                                                  shape=("blob", "box", "torus")[k]))
+            prefix = os.path.join(tmp, f"i{k}")
+            benchgen.save_instance(inst, prefix)
+            files.append({suffix: open(f"{prefix}_{suffix}", encoding="utf-8").read()
+                          for suffix in ("source.xyz", "reference.xyz", "gt.json")})
+            loaded = benchgen.load_instance(prefix)
+            recs.append(harness._run_one(loaded, search, k, loaded.config.rng_seed, 1.0, 0.1))
+            print(f"  i{k}: {recs[-1].status} {recs[-1].eval}")
+        harness.write_batch_csv(os.path.join(tmp, "b.csv"), recs)
+        csv_text = open(os.path.join(tmp, "b.csv"), encoding="utf-8").read()
+        with open(os.path.join(tmp, "s.json"), "w", encoding="utf-8") as fh:
+            json.dump(harness.search_to_dict(search), fh)
+        search_text = open(os.path.join(tmp, "s.json"), encoding="utf-8").read()
+    out = {"files": files, "csv": csv_text, "search": search_text,
+           "summary": harness.asdict(harness._summarize(recs))}
+    save("instances", {"instances": np.array(json.dumps(out, sort_keys=True))})
+
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "exh", "harness", "batchio",
-                             "histo"]
+                             "histo", "instances"]
     for w in which:
         print(w)
         globals()[f"make_{w}"]()

@@ -125,3 +125,95 @@ def test_cli_register_json(tmp_path):
     assert rep["best_inliers"] == res.best_inliers
     assert rep["chamfer_after_m"] <= rep["chamfer_before_m"] or not rep["chamfer_improved"]
     assert read_xyz(out).shape == x.shape
+
+
+# ---- registration instances (benchgen.py:370-411) and the benchmark CLI ----
+
+def _instance_files(golden, tmp_path):
+    """The reference's save_instance output for three instances, written to
+    tmp_path (tests/golden/instances.npz); returns (prefixes, golden dict)."""
+    g = json.loads(str(golden("instances")["instances"]))
+    prefixes = []
+    for k, files in enumerate(g["files"]):
+        prefix = tmp_path / f"i{k}"
+        for suffix, text in files.items():
+            (tmp_path / f"i{k}_{suffix}").write_text(text, encoding="utf-8")
+        prefixes.append(str(prefix))
+    return prefixes, g
+
+
+def test_instance_round_trip_byte_exact(golden, tmp_path):
+    """load_instance of the reference's files, then save_instance: the XYZ
+    files and the sidecar come out byte-identical; the aligner is the exact
+    inverse the reference wrote."""
+    from paper_2502_00115_b200.pcio import load_instance, save_instance
+    prefixes, g = _instance_files(golden, tmp_path)
+    out = tmp_path / "out"
+    out.mkdir()
+    for k, prefix in enumerate(prefixes):
+        inst = load_instance(prefix)
+        side = json.loads(g["files"][k]["gt.json"])
+        assert inst.gt_aligner.rotation.tolist() == side["gt_aligner"]["rotation"]
+        assert inst.gt_aligner.translation.tolist() == side["gt_aligner"]["translation"]
+        assert inst.config["rng_seed"] == 40 + k
+        paths = save_instance(inst, str(out / f"i{k}"))
+        assert set(paths) == {"source", "reference", "sidecar"}
+        for suffix, text in g["files"][k].items():
+            assert (out / f"i{k}_{suffix}").read_text(encoding="utf-8") == text, suffix
+
+
+def test_instance_errors(golden, tmp_path):
+    from paper_2502_00115_b200.errors import InvalidInputError, PointCloudIOError
+    from paper_2502_00115_b200.pcio import load_instance
+    prefixes, g = _instance_files(golden, tmp_path)
+    side = json.loads(g["files"][0]["gt.json"])
+    del side["source_transform"]
+    (tmp_path / "i0_gt.json").write_text(json.dumps(side))
+    with pytest.raises(PointCloudIOError):
+        load_instance(prefixes[0])
+    side = json.loads(g["files"][1]["gt.json"])
+    side["source_transform"]["rotation"][0][0] = 2.0  # not a rotation
+    (tmp_path / "i1_gt.json").write_text(json.dumps(side))
+    with pytest.raises(InvalidInputError):
+        load_instance(prefixes[1])
+    with pytest.raises(FileNotFoundError):
+        load_instance(str(tmp_path / "missing"))
+    # the CLI maps input errors to exit code 2 before touching the GPU
+    (tmp_path / "s.json").write_text(g["search"])
+    r = _cli("benchmark", "--instances", prefixes[0], "--search", str(tmp_path / "s.json"))
+    assert r.returncode == 2 and "error" in r.stderr
+    r = _cli("benchmark", "--instances", prefixes[2], "--search", str(tmp_path / "nope.json"))
+    assert r.returncode == 2
+
+
+@pytest.mark.gpu
+def test_cli_benchmark_matches_reference(golden, tmp_path):
+    """`benchmark` over the reference's instance files against the reference's
+    harness._run_one + write_batch_csv on the same files: identical rows
+    (status, seed, shape, recall hit, inliers, refined) and floats within
+    1e-9 relative (the moved cloud is a BLAS matmul, geometry.py:209-211)."""
+    import csv
+    import io
+    prefixes, g = _instance_files(golden, tmp_path)
+    (tmp_path / "s.json").write_text(g["search"])
+    out_csv, out_json = tmp_path / "b.csv", tmp_path / "b.json"
+    r = _cli("benchmark", "--instances", *prefixes, "--search", str(tmp_path / "s.json"),
+             "--csv", str(out_csv), "--json", str(out_json))
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.splitlines()[0] == "trials: 3  failed: 0"
+    s = g["summary"]
+    assert r.stdout.splitlines()[1] == f"recall: {s['recall']:.3f}"
+    got_text, ref_text = out_csv.read_text(), g["csv"]
+    assert got_text.splitlines()[:2] == ref_text.splitlines()[:2]  # schema + header
+    rows = list(csv.DictReader(io.StringIO("\n".join(got_text.splitlines()[1:]))))
+    refs = list(csv.DictReader(io.StringIO("\n".join(ref_text.splitlines()[1:]))))
+    assert len(rows) == len(refs) == 3
+    for a, b in zip(rows, refs):
+        for key in b:
+            if key in ("mie_r_deg", "mie_t_m", "mae_r_deg", "mae_t_m", "chamfer_m") and b[key]:
+                assert abs(float(a[key]) - float(b[key])) <= 1e-9 * abs(float(b[key])) + 1e-12
+            else:
+                assert a[key] == b[key], key
+    rep = json.loads(out_json.read_text())
+    assert rep["schema"] == "gridreg-batch-json v1" and rep["scenario"]["rng_seed"] == 40
+    assert rep["summary"]["n_trials"] == 3
