@@ -190,6 +190,18 @@ int dses_stage_stats(dses_plan* plan, int64_t* pairs, int64_t* votes, int64_t* r
 int dses_plan_traffic(dses_plan* plan, int64_t* h2d_bytes, int64_t* d2h_bytes, int64_t* launches,
                       int reset);
 
+/* ---- verification --------------------------------------------------------- */
+/* Dense translation sweep of the mode-optimality check; replaces
+ * _kernels.sweep_inlier_best (_kernels.py:384-410), called by
+ * harness.run_oracle_checks (harness.py:438-440).  cands: (n*m, 3) binary64
+ * differences y_j - R x_i, row-major by source i; t0/t1/t2: the lattice axes.
+ * *best = max over lattice translations t of the number of sources i with
+ * some j such that |cands[i*m+j] - t|_inf < half (bit-identical counts).
+ * Host pointers; synchronous. */
+int dses_sweep_inlier_best(int device, const double* cands, int64_t n, int64_t m, double half,
+                           const double* t0, int64_t n0, const double* t1, int64_t n1,
+                           const double* t2, int64_t n2, int64_t* best);
+
 /* ---- measurement ---------------------------------------------------------- */
 /* FP32 FFMA throughput of `device` measured live (independent FFMA chains on
  * every SM, CUDA events): the roofline denominator bench.py reports against. */

@@ -289,3 +289,22 @@ def translation_histogram(x, y, rot, bin_size, ilo=None, ihi=None, dedup=True):
     return {tuple(int(v) for v in key): int(c) for key, c in zip(uniq, cnt)}
 
 
+
+
+def sweep_inlier_best(cands, n, m, half, t0vals, t1vals, t2vals):
+    """_kernels.sweep_inlier_best (_kernels.py:384-410) in numpy, one t0 plane
+    at a time: max over the lattice of the number of sources i with some
+    j such that |cands[i*m+j] - t|_inf < half (strict, binary64)."""
+    c = np.asarray(cands, dtype=np.float64).reshape(n, m, 3)
+    t1 = np.asarray(t1vals, dtype=np.float64)
+    t2 = np.asarray(t2vals, dtype=np.float64)
+    if n == 0 or m == 0 or min(len(t0vals), t1.size, t2.size) == 0:
+        return 0
+    in1 = np.abs(c[:, :, 1, None] - t1[None, None, :]) < half   # (n, m, n1)
+    in2 = np.abs(c[:, :, 2, None] - t2[None, None, :]) < half   # (n, m, n2)
+    best = 0
+    for a in np.asarray(t0vals, dtype=np.float64):
+        in0 = np.abs(c[:, :, 0] - a) < half                       # (n, m)
+        hit = (in0[:, :, None, None] & in1[:, :, :, None] & in2[:, :, None, :]).any(axis=1)
+        best = max(best, int(hit.sum(axis=0).max()))
+    return best

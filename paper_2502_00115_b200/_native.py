@@ -96,6 +96,8 @@ _SIGS = [
                                        ctypes.c_double, _dp, _vp]),
     ("dses_stage_stats", ctypes.c_int, [_vp, _ip, _ip, _ip]),
     ("dses_plan_traffic", ctypes.c_int, [_vp, _ip, _ip, _ip, ctypes.c_int]),
+    ("dses_sweep_inlier_best", ctypes.c_int, [ctypes.c_int, _dp, _i64, _i64, ctypes.c_double,
+                                              _dp, _i64, _dp, _i64, _dp, _i64, _ip]),
     ("dses_probe_fp32_peak", ctypes.c_int, [ctypes.c_int, _dp, _dp]),
 ]
 EXPORTED = tuple(name for name, _, _ in _SIGS)
@@ -155,6 +157,20 @@ def probe_fp32_peak(device: int = 0):
     check(load().dses_probe_fp32_peak(int(device), ctypes.byref(f), ctypes.byref(ms)),
           "dses_probe_fp32_peak")
     return f.value, ms.value
+
+
+def sweep_inlier_best(cands, n: int, m: int, half: float, t0, t1, t2, device: int = 0) -> int:
+    """dses_sweep_inlier_best: maximum inlier count over the lattice t0 x t1 x t2."""
+    c = np.ascontiguousarray(cands, dtype=np.float64).reshape(-1, 3)
+    if c.shape[0] != n * m:
+        raise ValueError("cands must hold n*m difference vectors")
+    axes = [np.ascontiguousarray(t, dtype=np.float64).ravel() for t in (t0, t1, t2)]
+    best = ctypes.c_int64()
+    check(load().dses_sweep_inlier_best(int(device), dptr(c), int(n), int(m), float(half),
+                                        dptr(axes[0]), axes[0].size, dptr(axes[1]), axes[1].size,
+                                        dptr(axes[2]), axes[2].size, ctypes.byref(best)),
+          "dses_sweep_inlier_best")
+    return int(best.value)
 
 
 def dptr(a: np.ndarray):

@@ -15,7 +15,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libdses_b200.so")
-SOURCES = ["dses_vote.cu", "dses_score.cu", "dses_sparse.cu", "dses_capi.cu", "dses_probe.cu"]
+SOURCES = ["dses_vote.cu", "dses_score.cu", "dses_sparse.cu", "dses_capi.cu", "dses_probe.cu",
+           "dses_sweep.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -14,6 +14,10 @@ reports, summary lines) over instance files (``<prefix>_source.xyz``,
 reference's ``gridreg generate`` / ``benchgen.save_instance``) instead of
 the in-process scenario generator (benchgen is out of scope): trial k is
 the k-th prefix, its seed and shape come from the sidecar's config.
+
+``oracle-check --trials N --seed S`` is ``gridreg oracle-check``
+(cli.py:88-93, 212-226; harness.run_oracle_checks): same instances for the
+same seed, same report lines, exit 1 when a suite finds a violation.
 """
 from __future__ import annotations
 
@@ -59,6 +63,11 @@ def _parser():
                    help="recall threshold on mean Euler error (default 1)")
     p.add_argument("--trans-tol", type=float, default=0.1,
                    help="recall threshold on mean translation error (default 0.1)")
+    p = sub.add_parser("oracle-check",
+                       help="verify mode optimality and engine equality on small instances")
+    p.add_argument("--trials", type=int, default=20, metavar="N",
+                   help="trials per suite (default 20)")
+    p.add_argument("--seed", type=int, default=0, metavar="S")
     return ap
 
 
@@ -173,10 +182,31 @@ def _benchmark(args) -> int:
     return 0
 
 
+def _oracle_check(args) -> int:
+    """cli.py:212-226: both suites, the reference's report lines, exit 1 on a
+    violation."""
+    from .harness import run_oracle_checks
+
+    report = run_oracle_checks(n_lemma=args.trials, n_theorem=args.trials, seed=args.seed,
+                               device=args.device)
+    print(f"mode-optimality sweep: {report.lemma_trials - report.lemma_violations}"
+          f"/{report.lemma_trials} ok")
+    print(f"engine inlier equality: {report.theorem_trials - report.theorem_violations}"
+          f"/{report.theorem_trials} ok")
+    for line in report.details:
+        print(f"  {line}")
+    if not report.ok:
+        raise GridregError("oracle checks found violations")
+    return 0
+
+
+_COMMANDS = {"register": "_register", "benchmark": "_benchmark", "oracle-check": "_oracle_check"}
+
+
 def main(argv=None) -> int:
     args = _parser().parse_args(argv)
     try:
-        return _benchmark(args) if args.command == "benchmark" else _register(args)
+        return globals()[_COMMANDS[args.command]](args)
     except (FileNotFoundError, IsADirectoryError, PermissionError, PointCloudIOError,
             InvalidInputError, json.JSONDecodeError) as exc:
         print(f"error: {exc}", file=sys.stderr)

@@ -17,6 +17,14 @@ keys (search_to_dict / search_from_json, harness.py:545-616).
 
 The reference's synthetic instance generator (benchgen) is out of scope: the
 caller passes the pairs (e.g. paper_2502_00115_b200.synth.make_pair).
+
+run_oracle_checks is the reference's verification suite (harness.py:329-462,
+`gridreg oracle-check`): planted-consensus instances where the histogram mode
+must maximise the inlier count over a dense translation sweep (the sweep is
+the GPU kernel dses_sweep_inlier_best), and small on-grid instances where
+dses and exhaustive_search must agree on the inlier count.  The instance
+generators make the reference's numpy RNG calls in the reference's order, so
+the same seed yields the same instances.
 """
 from __future__ import annotations
 
@@ -29,10 +37,11 @@ from dataclasses import asdict, dataclass, is_dataclass
 
 import numpy as np
 
-from .engines import SearchConfig, dses, dses_batch
+from .engines import SearchConfig, dses, dses_batch, exhaustive_search
 from .errors import GridregError, InvalidInputError
-from .geometry import RigidTransform
-from .metrics import ErrorMetric, EvalReport, chamfer_distance, evaluate_pose
+from .geometry import RigidTransform, random_rotation, rotation_from_euler
+from .metrics import ErrorMetric, EvalReport, chamfer_distance, count_inliers, evaluate_pose
+from .mode_search import bin_center, mode_translation
 
 CSV_SCHEMA = "gridreg-batch-csv v1"
 JSON_SCHEMA = "gridreg-batch-json v1"
@@ -268,3 +277,128 @@ def search_from_dict(raw: dict) -> SearchConfig:
 def search_from_json(path) -> SearchConfig:
     with open(path, "r", encoding="utf-8") as fh:
         return search_from_dict(json.load(fh))
+
+
+# ---- verification suite (harness.py:329-462) ----
+
+def _sample_separated(rng, n, sep, lo, hi):
+    """harness.py:329-335: n points uniform in [lo, hi)^3, pairwise Chebyshev
+    separation > sep, by rejection (same RNG draws as the reference)."""
+    pts = []
+    while len(pts) < n:
+        p = rng.uniform(lo, hi, 3)
+        if all(np.max(np.abs(p - q)) > sep for q in pts):
+            pts.append(p)
+    return np.array(pts)
+
+
+def make_lemma_instance(rng: np.random.Generator, bin_size: float):
+    """harness.py:338-372: planted-consensus instance (a cluster of m sources
+    matched exactly at one translation, every other candidate difference at
+    least 2.5 bins away, the true translation off bin boundaries), under which
+    the histogram mode provably maximises the inlier count over ALL
+    translations.  Returns (X, Y, R, m)."""
+    b = bin_size
+    for _ in range(500):
+        n = int(rng.integers(4, 10))
+        m_total = int(rng.integers(4, 10))
+        m = int(rng.integers(2, min(n, m_total) + 1))
+        x = _sample_separated(rng, n, 3 * b, -0.6, 0.6)
+        rot = random_rotation(rng)
+        t_true = rng.uniform(-0.4, 0.4, 3)
+        ys = list(x[:m] @ rot.T + t_true)
+        while len(ys) < m_total:
+            p = rng.uniform(-0.6, 0.6, 3)
+            if all(np.max(np.abs(p - q)) > 3 * b for q in ys):
+                ys.append(p)
+        y = np.array(ys)
+        cand = (y[None, :, :] - (x @ rot.T)[:, None, :]).reshape(-1, 3)
+        d = np.max(np.abs(cand[:, None, :] - cand[None, :, :]), axis=2)
+        seps = d[np.triu_indices(cand.shape[0], 1)]
+        if np.any((seps > 1e-9) & (seps <= 2.5 * b)):
+            continue
+        qf = t_true / b
+        if np.any(np.abs(np.abs(qf - np.round(qf)) - 0.5) < 0.05):
+            continue
+        return x, y, rot, m
+    raise GridregError("lemma-instance rejection sampling did not converge")
+
+
+def make_theorem_instance(rng: np.random.Generator):
+    """harness.py:375-402: small random instance with an on-grid planted pose;
+    returns (X, Y, SearchConfig with the saturated-L0 metric at the bin)."""
+    k_rot, k_trans, rot_step, bin_size = int(rng.integers(0, 2)), 2, 0.3, 0.1
+    n = int(rng.integers(5, 13))
+    m_total = int(rng.integers(5, 13))
+    m = int(rng.integers(2, min(n, m_total) + 1))
+    x = rng.uniform(-0.5, 0.5, (n, 3))
+    idx_r = rng.integers(-k_rot, k_rot + 1, 3)
+    idx_t = rng.integers(-k_trans, k_trans + 1, 3)
+    node = RigidTransform(rotation_from_euler(idx_r.astype(np.float64) * rot_step),
+                          bin_center(idx_t, bin_size))
+    ys = list(node.apply(x[:m]))
+    while len(ys) < m_total:
+        ys.append(rng.uniform(-0.8, 0.8, 3))
+    cfg = SearchConfig(k_rot=k_rot, rot_step=rot_step, k_trans=k_trans, trans_bin=bin_size,
+                       q=0.5, metric=ErrorMetric.saturated_l0(bin_size))
+    return x, np.array(ys), cfg
+
+
+def sweep_inlier_best(cands, n: int, m: int, half: float, t0vals, t1vals, t2vals,
+                      device: int = 0) -> int:
+    """_kernels.sweep_inlier_best (_kernels.py:384-410) on the GPU: the maximum
+    over the lattice t0 x t1 x t2 of the number of sources with some
+    difference (row i*m + j of `cands`) inside the open Chebyshev ball of
+    radius `half` around t.  Bit-identical counts (binary64 compares)."""
+    from . import _native
+    return _native.sweep_inlier_best(cands, n, m, half, t0vals, t1vals, t2vals, device)
+
+
+@dataclass(frozen=True)
+class OracleReport:
+    """harness.py:405-415."""
+    lemma_trials: int
+    lemma_violations: int
+    theorem_trials: int
+    theorem_violations: int
+    details: list
+
+    @property
+    def ok(self) -> bool:
+        return self.lemma_violations == 0 and self.theorem_violations == 0
+
+
+def run_oracle_checks(n_lemma: int = 25, n_theorem: int = 10, seed: int = 0,
+                      device: int = 0) -> OracleReport:
+    """harness.py:418-462: the mode-optimality sweep check (n_lemma planted
+    instances: the inlier count at mode_translation's t* must not be beaten by
+    a sweep at bin/4 spacing) and the engine inlier-equality check (n_theorem
+    instances: dses and exhaustive_search report the same best_inliers)."""
+    details = []
+    rng = np.random.default_rng(np.random.SeedSequence([0x0AC1E, seed]))
+    bin_size = 0.05
+    lemma_bad = 0
+    for k in range(n_lemma):
+        x, y, rot, m = make_lemma_instance(rng, bin_size)
+        mode = mode_translation(x, y, rot, bin_size, device=device)
+        c_star = count_inliers(x, y, RigidTransform(rot, mode.t_star), bin_size, device=device)
+        cand = np.ascontiguousarray((y[None, :, :] - (x @ rot.T)[:, None, :]).reshape(-1, 3))
+        step = bin_size / 4.0
+        axes = [np.arange(cand[:, a].min(), cand[:, a].max() + step, step) for a in range(3)]
+        best = sweep_inlier_best(cand, x.shape[0], y.shape[0], bin_size / 2.0, *axes, device=device)
+        if best > c_star:
+            lemma_bad += 1
+            details.append(f"lemma trial {k}: sweep found {best} inliers vs mode {c_star}")
+        elif c_star != m:
+            details.append(f"lemma trial {k}: inliers at mode = {c_star}, planted {m}")
+    theorem_bad = 0
+    for k in range(n_theorem):
+        x, y, cfg = make_theorem_instance(rng)
+        semi = dses(x, y, cfg, device)
+        full = exhaustive_search(x, y, cfg, device)
+        if semi.best_inliers != full.best_inliers:
+            theorem_bad += 1
+            details.append(f"theorem trial {k}: semi-exhaustive {semi.best_inliers} vs "
+                           f"exhaustive {full.best_inliers} inliers")
+    return OracleReport(lemma_trials=n_lemma, lemma_violations=lemma_bad,
+                        theorem_trials=n_theorem, theorem_violations=theorem_bad, details=details)

@@ -469,9 +469,60 @@ def make_instances():
     save("instances", {"instances": np.array(json.dumps(out, sort_keys=True))})
 
 
+def make_oracle():
+    """harness.run_oracle_checks pieces: the lemma / theorem instances the
+    reference draws for seed 0 (make_lemma_instance / make_theorem_instance
+    with the run's RNG), the mode inlier count, the dense-sweep maximum
+    (_kernels.sweep_inlier_best) and the two engines' inlier counts; the
+    report of run_oracle_checks(4, 4, 0); plus two standalone sweep cases
+    (random, and differences exactly on the ball boundary: strict <)."""
+    from gridreg import _kernels, harness, metrics
+    from gridreg.mode_search import mode_translation
+    rec = {}
+    rng = np.random.default_rng(np.random.SeedSequence([0x0AC1E, 0]))
+    b = 0.05
+    nl = nt = 4
+    for k in range(nl):
+        x, y, rot, m = harness.make_lemma_instance(rng, b)
+        mode = mode_translation(x, y, rot, b)
+        c_star = metrics.count_inliers(x, y, geometry.RigidTransform(rot, mode.t_star), b)
+        cand = np.ascontiguousarray((y[None, :, :] - (x @ rot.T)[:, None, :]).reshape(-1, 3))
+        step = b / 4.0
+        axes = [np.arange(cand[:, a].min(), cand[:, a].max() + step, step) for a in range(3)]
+        best = int(_kernels.sweep_inlier_best(cand, x.shape[0], y.shape[0], b / 2.0, *axes))
+        p = f"l{k}"
+        rec[f"{p}_x"], rec[f"{p}_y"], rec[f"{p}_rot"] = x, y, rot
+        rec[f"{p}_m"], rec[f"{p}_cstar"], rec[f"{p}_best"] = np.int64(m), np.int64(c_star), np.int64(best)
+        rec[f"{p}_tstar"] = np.asarray(mode.t_star)
+        print(f"  lemma {k}: n={x.shape[0]} m={y.shape[0]} planted {m} mode {c_star} sweep {best}")
+    for k in range(nt):
+        x, y, cfg = harness.make_theorem_instance(rng)
+        semi, full = engines.dses(x, y, cfg), engines.exhaustive_search(x, y, cfg)
+        p = f"t{k}"
+        rec[f"{p}_x"], rec[f"{p}_y"] = x, y
+        rec[f"{p}_krot"] = np.int64(cfg.k_rot)
+        rec[f"{p}_semi"], rec[f"{p}_full"] = np.int64(semi.best_inliers), np.int64(full.best_inliers)
+        print(f"  theorem {k}: k_rot={cfg.k_rot} semi {semi.best_inliers} full {full.best_inliers}")
+    rep = harness.run_oracle_checks(n_lemma=nl, n_theorem=nt, seed=0)
+    rec["report"] = np.array([rep.lemma_trials, rep.lemma_violations, rep.theorem_trials,
+                              rep.theorem_violations], dtype=np.int64)
+    rec["report_details"] = np.array("\n".join(rep.details))
+    r2 = np.random.default_rng(7)
+    cand = r2.uniform(-0.3, 0.3, (7 * 5, 3))
+    axes = [np.linspace(-0.35, 0.35, 29) for _ in range(3)]
+    rec["s0_cands"], rec["s0_axes"] = cand, np.stack(axes)
+    rec["s0_best"] = np.int64(_kernels.sweep_inlier_best(cand, 7, 5, 0.04, *axes))
+    cand = r2.integers(-2, 3, (6 * 6, 3)).astype(np.float64) * 0.25
+    axes = [np.arange(-1.0, 1.0 + 0.125, 0.125) for _ in range(3)]
+    rec["s1_cands"], rec["s1_axes"] = cand, np.stack(axes)
+    rec["s1_best"] = np.int64(_kernels.sweep_inlier_best(cand, 6, 6, 0.25, *axes))
+    print(f"  sweeps: {int(rec['s0_best'])} {int(rec['s1_best'])}")
+    save("oracle", rec)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "c1", "c2", "c3", "c4", "exh", "harness", "batchio",
-                             "histo", "instances"]
+                             "histo", "instances", "oracle"]
     for w in which:
         print(w)
         globals()[f"make_{w}"]()
