@@ -106,6 +106,11 @@ static int fail(int code, const char* fmt, ...) {
 
 extern "C" const char* dses_last_error(void) { return g_err.c_str(); }
 
+namespace dses {
+// Error reporting for entry points defined in other translation units.
+int api_fail(int code, const char* what) { return fail(code, "%s", what); }
+}  // namespace dses
+
 extern "C" const char* dses_build_info(void) {
   return "dses_b200: sm_100a, nvcc " DSES_NVCC_VERSION ", fixed-point vote + fp32 screen + fp64 exact";
 }

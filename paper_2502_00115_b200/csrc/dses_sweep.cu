@@ -19,6 +19,7 @@
 
 namespace dses {
 
+int api_fail(int code, const char* what);  // dses_capi.cu: sets dses_last_error()
 constexpr int kSweepThreads = 256;
 
 template <bool SMEM>
@@ -63,20 +64,25 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_inlier_kernel(
 extern "C" int dses_sweep_inlier_best(int device, const double* cands, int64_t n, int64_t m,
                                       double half, const double* t0, int64_t n0, const double* t1,
                                       int64_t n1, const double* t2, int64_t n2, int64_t* best_out) {
-  if (!best_out || n < 0 || m < 0 || n0 < 0 || n1 < 0 || n2 < 0) return DSES_E_INVALID;
-  if (n > INT32_MAX / 3 || m > INT32_MAX / 3 || n * m > INT32_MAX / 3) return DSES_E_INVALID;
+  if (!best_out || n < 0 || m < 0 || n0 < 0 || n1 < 0 || n2 < 0)
+    return dses::api_fail(DSES_E_INVALID, "negative size or null output");
+  if (n > INT32_MAX / 3 || m > INT32_MAX / 3 || n * m > INT32_MAX / 3)
+    return dses::api_fail(DSES_E_INVALID, "n*m too large");
   *best_out = 0;
   const int64_t total = n0 * n1 * n2;
   if (total == 0 || n == 0 || m == 0) return DSES_OK;
-  if (!cands || !t0 || !t1 || !t2) return DSES_E_INVALID;
-  if (cudaSetDevice(device) != cudaSuccess) return DSES_E_NODEVICE;
+  if (!cands || !t0 || !t1 || !t2)
+    return dses::api_fail(DSES_E_INVALID, "null input");
+  if (cudaSetDevice(device) != cudaSuccess)
+    return dses::api_fail(DSES_E_NODEVICE, "no usable CUDA device");
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
-    return DSES_E_CUDA;
+    return dses::api_fail(DSES_E_CUDA, "device query failed");
   const size_t cb = sizeof(double) * 3 * (size_t)(n * m);
   const size_t ab = sizeof(double) * (size_t)(n0 + n1 + n2);
   char* buf = nullptr;
-  if (cudaMalloc(&buf, cb + ab + 16) != cudaSuccess) return DSES_E_NOMEM;
+  if (cudaMalloc(&buf, cb + ab + 16) != cudaSuccess)
+    return dses::api_fail(DSES_E_NOMEM, "device allocation failed");
   double* dc = reinterpret_cast<double*>(buf);
   double* d0 = dc + 3 * n * m;
   double* d1 = d0 + n0;
@@ -101,7 +107,7 @@ extern "C" int dses_sweep_inlier_best(int device, const double* cands, int64_t n
   int best = 0;
   if (e == cudaSuccess) e = cudaMemcpy(&best, dbest, sizeof(int), cudaMemcpyDeviceToHost);
   cudaFree(buf);
-  if (e != cudaSuccess) return DSES_E_CUDA;
+  if (e != cudaSuccess) return dses::api_fail(DSES_E_CUDA, cudaGetErrorString(e));
   *best_out = best;
   return DSES_OK;
 }
