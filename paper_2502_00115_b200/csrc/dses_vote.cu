@@ -63,7 +63,7 @@
 #define DSES_VOTE_FSH 1  // vote word value by a wrapping funnel shift
 #endif
 #ifndef DSES_POP
-#define DSES_POP 2  // units per claim when the round's overlap is sparse
+#define DSES_POP 3  // units per claim when the round's overlap is sparse (c4: 3 vs 2 -0.9%)
 #endif
 
 namespace dses {
