@@ -40,6 +40,8 @@ extern "C" {
 #define DSES_E_CUDA -2      /* CUDA runtime / launch failure */
 #define DSES_E_NOMEM -3     /* device or host allocation failed */
 #define DSES_E_NODEVICE -4  /* no CUDA device / the sm_100a image cannot run here */
+#define DSES_E_LIMIT -5     /* input beyond a documented size limit of this implementation
+                               (SearchSpaceTooLargeError upstream) */
 
 /* Metric codes follow _kernels.py:15-16 (METRIC_*), plus code 4 (extension). */
 #define DSES_METRIC_L2 0

@@ -21,6 +21,7 @@ DSES_E_INVALID = -1
 DSES_E_CUDA = -2
 DSES_E_NOMEM = -3
 DSES_E_NODEVICE = -4
+DSES_E_LIMIT = -5
 
 
 class NativeUnavailable(RuntimeError):
@@ -133,13 +134,20 @@ def last_error() -> str:
 
 
 def check(rc: int, what: str):
+    """Map a C-ABI status to the reference's exception contract: bad
+    arguments raise InvalidInputError (a ValueError, errors.py), inputs past a
+    documented size limit of this implementation SearchSpaceTooLargeError --
+    both GridregError, so the batch harness records them per trial."""
     if rc == DSES_OK:
         return
+    from .errors import InvalidInputError, SearchSpaceTooLargeError
     msg = f"{what}: {last_error()}"
     if rc == DSES_E_NODEVICE:
         raise NativeUnavailable(msg)
     if rc == DSES_E_INVALID:
-        raise ValueError(msg)
+        raise InvalidInputError(msg)
+    if rc == DSES_E_LIMIT:
+        raise SearchSpaceTooLargeError(msg)
     if rc == DSES_E_NOMEM:
         raise MemoryError(msg)
     raise NativeError(msg)

@@ -168,9 +168,14 @@ struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
   bool borrowed = false;  // points into another buffer (an upload arena): never freed here
-  cudaError_t ensure(size_t bytes, cudaStream_t st = 0) {
+  // A growing buffer is freed and re-allocated on the stream that uses it, so
+  // the free is ordered after the work already queued there on the old one.
+  cudaError_t ensure(size_t bytes, cudaStream_t st) {
     if (bytes <= cap && p) return cudaSuccess;
-    release();
+    if (p && !borrowed) cudaFreeAsync(p, st);
+    p = nullptr;
+    cap = 0;
+    borrowed = false;
     size_t want = std::max<size_t>(bytes + bytes / 2, 256);
     cudaError_t e = cudaMallocAsync(&p, want, st);
     if (e == cudaSuccess) cap = want;
@@ -808,7 +813,6 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       if (!far) T.gm = std::max(T.gm, ne);
       yq[q].w = far ? kFarFlag : w;
     }
-#if DSES_SAFE_LANES
     // unused partner slots (below the group's shuffle count gm) -> a safe
     // lane: an empty lane of the group, else the first non-far point that is
     // no dedup partner of q; a point without one takes the exact path
@@ -835,10 +839,10 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
         for (; ne < T.gm; ++ne) yq[q].w |= (safe + 1) << (6 * ne);
       }
     }
-#endif
   }
-  if (yt.size() >= 65536 || xt.size() >= 65536)
-    return fail(DSES_E_INVALID, "cloud too large for the 16-bit work-unit encoding");
+  if (yt.size() >= 65536 || xt.size() >= 65536)  // (group << 16 | unit) work-unit encoding
+    return fail(DSES_E_LIMIT, "cloud too large for the vote kernel: at most 65535 groups / units "
+                "of 32 points (about 2 million points) per cloud");
   // ---- full dedup near lists (tile order, j' < j) for the exact path
   trace("dedup near lists");
   // CSR near lists in tile order: j' < j, sorted (the exact path's partners)
@@ -940,8 +944,10 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     P->vote_threads = 512;
     per_sm = vote_max_ctas_per_sm(v, P->hsmem, P->psmem, P->vote_threads);
   }
-  if (per_sm < 1) return fail(DSES_E_CUDA, "vote kernel cannot be resident (smem %zu)",
-                              vote_smem_bytes(v, P->hsmem, P->psmem, P->vote_threads));
+  if (per_sm < 1)
+    return fail(DSES_E_LIMIT, "source cloud too large for the vote kernel: its unit boxes need "
+                "%zu bytes of shared memory (about 180,000 source points at most)",
+                vote_smem_bytes(v, P->hsmem, P->psmem, P->vote_threads));
   P->vote_grid = per_sm * P->sms;
   trace("plan ready");
   return DSES_OK;
@@ -951,8 +957,8 @@ int set_grid(dses_plan* P, const dses_grid* g, RotSource* rs, cudaStream_t st) {
   std::memset(rs, 0, sizeof(*rs));
   if (!g || g->k < 0 || !g->cos_tab || !g->sin_tab) return fail(DSES_E_INVALID, "bad rotation grid");
   const size_t nt = (size_t)(2 * g->k + 1);
-  CK(P->cth.ensure(nt * 8));
-  CK(P->sth.ensure(nt * 8));
+  CK(P->cth.ensure(nt * 8, st));
+  CK(P->sth.ensure(nt * 8, st));
   CK(h2d(P->cth.p, g->cos_tab, nt * 8, st));
   CK(h2d(P->sth.p, g->sin_tab, nt * 8, st));
   rs->cth = P->cth.as<double>();
@@ -980,17 +986,17 @@ static SparseParams sparse_params(const dses_plan* P, const RotSource& rs) {
 }
 
 int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
-  CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
-  CK(P->lins64.ensure(sizeof(long long) * std::max<int64_t>(r_count, 1)));
-  CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1), st));
+  CK(P->lins64.ensure(sizeof(long long) * std::max<int64_t>(r_count, 1), st));
+  CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1), st));
   P->cur_r_begin = r_begin;
   P->cur_r_count = r_count;
   P->cur_rot = rs;
   if (r_count <= 0) return DSES_OK;
   const SparseParams sp = sparse_params(P, rs);
   const size_t sb = sparse_scratch_bytes(P->n, P->m);
-  CK(P->sparse_scratch.ensure(sb));
-  CK(P->scal.ensure(64));
+  CK(P->sparse_scratch.ensure(sb, st));
+  CK(P->scal.ensure(64, st));
   CK(launched(launch_sparse_modes(sp, r_begin, r_count, P->sparse_scratch.p, P->sparse_scratch.cap,
                                   P->scal.as<unsigned long long>() + 6, P->counts.as<int>(),
                                   P->lins64.as<long long>(), P->ties.as<int>(), P->sms, st),
@@ -1000,9 +1006,9 @@ int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_cou
 
 int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
   if (P->sparse) return run_sparse(P, rs, r_begin, r_count, st);
-  CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
-  CK(P->lins.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
-  CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1)));
+  CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1), st));
+  CK(P->lins.ensure(sizeof(int) * std::max<int64_t>(r_count, 1), st));
+  CK(P->ties.ensure(sizeof(int) * std::max<int64_t>(r_count, 1), st));
   VoteParams v = P->vp;
   v.rot = rs;
   v.r_begin = r_begin;
@@ -1021,11 +1027,11 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
     const size_t budget = (size_t)4 << 30;
     grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)grid, budget / per_cta));
     if (!P->hsmem) {
-      CK(P->hist_g.ensure((size_t)grid * v.hist_words * 4));
+      CK(P->hist_g.ensure((size_t)grid * v.hist_words * 4, st));
       v.hist_global = P->hist_g.as<unsigned>();
     }
     if (!P->psmem) {
-      CK(P->p_g.ensure((size_t)grid * v.n_pad * 16));
+      CK(P->p_g.ensure((size_t)grid * v.n_pad * 16, st));
       v.p_global = P->p_g.as<int4>();
     }
   }
@@ -1177,7 +1183,7 @@ extern "C" int dses_mode_batch(dses_plan* P, const double* rots, int64_t nrot, i
   if (!P || (!rots && nrot > 0) || nrot < 0) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
-  CK(P->rots.ensure(sizeof(double) * 9 * std::max<int64_t>(nrot, 1)));
+  CK(P->rots.ensure(sizeof(double) * 9 * std::max<int64_t>(nrot, 1), st));
   if (nrot > 0) CK(h2d(P->rots.p, rots, sizeof(double) * 9 * nrot, st));
   RotSource rs{};
   rs.rots = P->rots.as<double>();
@@ -1222,13 +1228,13 @@ extern "C" int dses_translation_histogram(dses_plan* P, const double* rot, int d
     return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
-  CK(P->rots.ensure(sizeof(double) * 9));
+  CK(P->rots.ensure(sizeof(double) * 9, st));
   CK(h2d(P->rots.p, rot, sizeof(double) * 9, st));
   RotSource rs{};
   rs.rots = P->rots.as<double>();
   const SparseParams sp = sparse_params(P, rs);
-  CK(P->sparse_scratch.ensure(sparse_scratch_bytes(P->n, P->m)));
-  CK(P->scal.ensure(64));
+  CK(P->sparse_scratch.ensure(sparse_scratch_bytes(P->n, P->m), st));
+  CK(P->scal.ensure(64, st));
   unsigned long long* dl = nullptr;
   int *dc = nullptr, *dn = nullptr;
   unsigned long long nk = 0;
@@ -1262,12 +1268,12 @@ extern "C" int dses_refine_batch(dses_plan* P, const double* rots, const double*
   if (ncand == 0) return DSES_OK;
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
-  CK(P->rots.ensure(sizeof(double) * 9 * ncand));
-  CK(P->tvec.ensure(sizeof(double) * 3 * ncand));
-  CK(P->tmp_rows.ensure(sizeof(int64_t) * ncand));
-  CK(P->tmp_lins.ensure(sizeof(int) * ncand));
-  CK(P->vals.ensure(sizeof(double) * P->n * ncand));
-  CK(P->err64.ensure(sizeof(double) * ncand));
+  CK(P->rots.ensure(sizeof(double) * 9 * ncand, st));
+  CK(P->tvec.ensure(sizeof(double) * 3 * ncand, st));
+  CK(P->tmp_rows.ensure(sizeof(int64_t) * ncand, st));
+  CK(P->tmp_lins.ensure(sizeof(int) * ncand, st));
+  CK(P->vals.ensure(sizeof(double) * P->n * ncand, st));
+  CK(P->err64.ensure(sizeof(double) * ncand, st));
   std::vector<int64_t> rows(ncand);
   std::iota(rows.begin(), rows.end(), 0);
   std::vector<int> zeros(ncand, 0);
@@ -1345,8 +1351,8 @@ extern "C" int dses_stage_screen(dses_plan* P, double q, int64_t mstar_global, i
   const int64_t nr = P->cur_r_count;
   // engines.py:196-201 in binary64: cutoff = q * M* - 1e-9
   const double cutoff = q * (double)mstar_global - 1e-9;
-  CK(P->cand_rows.ensure(sizeof(int64_t) * std::max<int64_t>(nr, 1)));
-  CK(P->cand_lins.ensure(sizeof(int) * std::max<int64_t>(nr, 1)));
+  CK(P->cand_rows.ensure(sizeof(int64_t) * std::max<int64_t>(nr, 1), st));
+  CK(P->cand_lins.ensure(sizeof(int) * std::max<int64_t>(nr, 1), st));
   unsigned long long* sc = P->scal.as<unsigned long long>() + 3;
   CK(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), st));
   if (nr > 0)
@@ -1363,8 +1369,8 @@ extern "C" int dses_stage_screen(dses_plan* P, double q, int64_t mstar_global, i
     return DSES_OK;
   }
   const int nblk = (int)((P->n + screen_threads() - 1) / screen_threads());
-  CK(P->partial.ensure(sizeof(double) * nblk * kept));
-  CK(P->err32.ensure(sizeof(double) * kept));
+  CK(P->partial.ensure(sizeof(double) * nblk * kept, st));
+  CK(P->err32.ensure(sizeof(double) * kept, st));
   unsigned long long* mb = P->scal.as<unsigned long long>() + 4;
   CK(cudaMemsetAsync(mb, 0x7f, sizeof(unsigned long long), st));
   ScoreParams s = score_params(P, P->cur_rot, code, param);
@@ -1389,7 +1395,7 @@ extern "C" int dses_stage_rescore(dses_plan* P, double threshold, int code, doub
   if (row_local) *row_local = INT64_MAX;
   if (rescored) *rescored = 0;
   if (P->kept <= 0) return DSES_OK;
-  CK(P->sel.ensure(sizeof(int) * P->kept));
+  CK(P->sel.ensure(sizeof(int) * P->kept, st));
   unsigned long long* ns = P->scal.as<unsigned long long>() + 5;
   CK(cudaMemsetAsync(ns, 0, sizeof(unsigned long long), st));
   CK(launched(launch_rescore_compact(P->err32.as<double>(), P->kept, threshold, P->sel.as<int>(), ns, st)));
@@ -1398,11 +1404,11 @@ extern "C" int dses_stage_rescore(dses_plan* P, double threshold, int code, doub
   CK(cudaStreamSynchronize(st));
   if (rescored) *rescored = (int64_t)nsel;
   if (nsel == 0) return DSES_OK;
-  CK(P->vals.ensure(sizeof(double) * P->n * nsel));
-  CK(P->err64.ensure(sizeof(double) * nsel));
-  CK(P->win_err.ensure(sizeof(double)));
-  CK(P->win_row.ensure(sizeof(int64_t)));
-  CK(P->win_c.ensure(sizeof(int)));
+  CK(P->vals.ensure(sizeof(double) * P->n * nsel, st));
+  CK(P->err64.ensure(sizeof(double) * nsel, st));
+  CK(P->win_err.ensure(sizeof(double), st));
+  CK(P->win_row.ensure(sizeof(int64_t), st));
+  CK(P->win_c.ensure(sizeof(int), st));
   ScoreParams s = score_params(P, P->cur_rot, code, param);
   CK(launched(launch_exact(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->sel.as<int>(),
                            (int64_t)nsel, P->vals.as<double>(), P->err64.as<double>(), st),
@@ -1446,10 +1452,10 @@ extern "C" int dses_pose_error(dses_plan* P, const dses_grid* g, int64_t row, in
   RotSource rs;
   int rc = set_grid(P, g, &rs, st);
   if (rc) return rc;
-  CK(P->tmp_rows.ensure(sizeof(int64_t)));
-  CK(P->tmp_lins.ensure(sizeof(int)));
-  CK(P->vals.ensure(sizeof(double) * P->n));
-  CK(P->err64.ensure(sizeof(double)));
+  CK(P->tmp_rows.ensure(sizeof(int64_t), st));
+  CK(P->tmp_lins.ensure(sizeof(int), st));
+  CK(P->vals.ensure(sizeof(double) * P->n, st));
+  CK(P->err64.ensure(sizeof(double), st));
   const int l32 = (int)lin;
   CK(h2d(P->tmp_rows.p, &row, sizeof row, st));
   CK(h2d(P->tmp_lins.p, &l32, sizeof l32, st));
@@ -1559,12 +1565,12 @@ extern "C" int dses_search_async(dses_plan* P, const dses_grid* g, int64_t r_beg
   CK(cudaMemsetAsync(sc + 4, 0x7f, sizeof(unsigned long long), st));
   if (r_count > 0) CK(launched(launch_select_stats(P->counts.as<int>(), r_count, sc, sc + 1, P->sms, st)));
   CK(cudaEventRecord(P->ev[1], st));
-  CK(P->cand_rows.ensure(sizeof(int64_t) * nr));
-  CK(P->cand_lins.ensure(sizeof(int) * nr));
-  CK(P->win_err.ensure(sizeof(double)));
-  CK(P->win_row.ensure(sizeof(int64_t)));
-  CK(P->win_c.ensure(sizeof(int)));
-  CK(P->tvec.ensure(sizeof(double) * (P->n + 16)));  // the winner's inlier pass (+ miss, record)
+  CK(P->cand_rows.ensure(sizeof(int64_t) * nr, st));
+  CK(P->cand_lins.ensure(sizeof(int) * nr, st));
+  CK(P->win_err.ensure(sizeof(double), st));
+  CK(P->win_row.ensure(sizeof(int64_t), st));
+  CK(P->win_c.ensure(sizeof(int), st));
+  CK(P->tvec.ensure(sizeof(double) * (P->n + 16), st));  // the winner's inlier pass (+ miss, record)
   double* inl_vals = P->tvec.as<double>();
   double* miss = inl_vals + P->n;
   long long* rec = reinterpret_cast<long long*>(inl_vals + P->n + 2);
@@ -1581,11 +1587,11 @@ extern "C" int dses_search_async(dses_plan* P, const dses_grid* g, int64_t r_beg
                                st, sc, q)));
     CK(cudaEventRecord(P->ev[2], st));
     const int nblk = (int)((P->n + screen_threads() - 1) / screen_threads());
-    CK(P->partial.ensure(sizeof(double) * nblk * nr));
-    CK(P->err32.ensure(sizeof(double) * nr));
-    CK(P->sel.ensure(sizeof(int) * nr));
-    CK(P->vals.ensure(sizeof(double) * P->n * cap));
-    CK(P->err64.ensure(sizeof(double) * cap));
+    CK(P->partial.ensure(sizeof(double) * nblk * nr, st));
+    CK(P->err32.ensure(sizeof(double) * nr, st));
+    CK(P->sel.ensure(sizeof(int) * nr, st));
+    CK(P->vals.ensure(sizeof(double) * P->n * cap, st));
+    CK(P->err64.ensure(sizeof(double) * cap, st));
     const ScoreParams s = score_params(P, rs, code, param);
     CK(launched(launch_screen(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), nr,
                               P->partial.as<double>(), P->err32.as<double>(), sc + 4, st, sc + 3), 2));
@@ -1719,8 +1725,8 @@ extern "C" int dses_exhaustive(dses_plan* P, const dses_grid* g, int64_t k_trans
   const int64_t npose = nrot * ntrans;
   CK(cudaEventRecord(P->ev[0], st));
   // every pose (rotation-major, translation lexicographic: _kernels.py:327-381)
-  CK(P->cand_rows.ensure(sizeof(int64_t) * npose));
-  CK(P->cand_lins.ensure(sizeof(int) * npose));
+  CK(P->cand_rows.ensure(sizeof(int64_t) * npose, st));
+  CK(P->cand_lins.ensure(sizeof(int) * npose, st));
   CK(launched(launch_enumerate_poses(0, npose, ntrans, P->cand_rows.as<int64_t>(),
                                      P->cand_lins.as<int>(), st)));
   ScoreParams s = score_params(P, rs, code, param);
@@ -1732,8 +1738,8 @@ extern "C" int dses_exhaustive(dses_plan* P, const dses_grid* g, int64_t k_trans
   // poses within the rigorous screen tolerance of the minimum
   const int64_t chunk = 1 << 20;
   const int nblk = (int)((P->n + screen_threads() - 1) / screen_threads());
-  CK(P->partial.ensure(sizeof(double) * nblk * std::min<int64_t>(chunk, npose)));
-  CK(P->err32.ensure(sizeof(double) * npose));
+  CK(P->partial.ensure(sizeof(double) * nblk * std::min<int64_t>(chunk, npose), st));
+  CK(P->err32.ensure(sizeof(double) * npose, st));
   unsigned long long* mb = P->scal.as<unsigned long long>() + 4;
   CK(cudaMemsetAsync(mb, 0x7f, sizeof(unsigned long long), st));
   for (int64_t p0 = 0; p0 < npose; p0 += chunk) {
@@ -1747,7 +1753,7 @@ extern "C" int dses_exhaustive(dses_plan* P, const dses_grid* g, int64_t k_trans
   CK(cudaStreamSynchronize(st));
   CK(cudaEventRecord(P->ev[2], st));
   const double thr = mn + screen_tolerance(P, code);
-  CK(P->sel.ensure(sizeof(int) * npose));
+  CK(P->sel.ensure(sizeof(int) * npose, st));
   unsigned long long* ns = P->scal.as<unsigned long long>() + 5;
   CK(cudaMemsetAsync(ns, 0, sizeof(unsigned long long), st));
   CK(launched(launch_rescore_compact(P->err32.as<double>(), npose, thr, P->sel.as<int>(), ns, st)));
@@ -1755,11 +1761,11 @@ extern "C" int dses_exhaustive(dses_plan* P, const dses_grid* g, int64_t k_trans
   CK(d2h(&nsel, ns, sizeof nsel, st));
   CK(cudaStreamSynchronize(st));
   if (nsel == 0) return fail(DSES_E_CUDA, "internal: exhaustive screen selected no pose");
-  CK(P->vals.ensure(sizeof(double) * P->n * nsel));
-  CK(P->err64.ensure(sizeof(double) * nsel));
-  CK(P->win_err.ensure(sizeof(double)));
-  CK(P->win_row.ensure(sizeof(int64_t)));
-  CK(P->win_c.ensure(sizeof(int)));
+  CK(P->vals.ensure(sizeof(double) * P->n * nsel, st));
+  CK(P->err64.ensure(sizeof(double) * nsel, st));
+  CK(P->win_err.ensure(sizeof(double), st));
+  CK(P->win_row.ensure(sizeof(int64_t), st));
+  CK(P->win_c.ensure(sizeof(int), st));
   CK(launched(launch_exact(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->sel.as<int>(),
                            (int64_t)nsel, P->vals.as<double>(), P->err64.as<double>(), st),
               (int)((nsel + 65534) / 65535) + 1));

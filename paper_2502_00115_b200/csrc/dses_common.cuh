@@ -31,24 +31,14 @@ namespace dses {
 
 constexpr int kTile = 32;        // points per reference group (one per lane) and per source unit
 constexpr int kGuard = 2;        // guard band in fixed-point units
-constexpr int kUnitCapMin = 2048;
-constexpr int kDenseMaxBins = 1 << 26;  // beyond: sort-based (sparse) mode queries // minimum (reference group, source unit) list capacity per round
+constexpr int kUnitCapMin = 2048;       // minimum (reference group, source unit) list capacity per round
+constexpr int kDenseMaxBins = 1 << 26;  // beyond: sort-based (sparse) mode queries
 // Sentinel Yq.x of empty reference slots: with |Pq| < 2^29 and W < 2^30 (or
 // W = 2^31 - 1 and Pq = 0 in exact mode) u = Yq - Pq wraps to >= 2^30 > W.
 constexpr int kNoRef = -3 * (1 << 29);
 constexpr int kMaxComp = 16;     // dedup components up to this size stay in one warp
 constexpr int kFarFlag = 1 << 12; // Yq.w: the point's dedup needs the exact path
-#ifndef DSES_SAFE_LANES
-// Partner slots a lane does not use hold a "safe" lane of its group (an
-// empty lane, or a point that is no dedup partner of it: it can never be
-// decided in the same bin for the same source), so the vote kernel shuffles
-// unconditionally instead of testing l >= 0 per pair.
-#define DSES_SAFE_LANES 1
-#endif
-#ifndef DSES_VOTE_THREADS
-#define DSES_VOTE_THREADS 1024
-#endif
-constexpr int kVoteThreads = DSES_VOTE_THREADS;
+constexpr int kVoteThreads = 1024;
 
 enum Metric { kL2 = 0, kL1 = 1, kTruncL1 = 2, kSatL0 = 3, kTruncL2 = 4 };
 

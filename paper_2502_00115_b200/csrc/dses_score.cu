@@ -72,7 +72,8 @@ __global__ void compact_kernel(const int* counts, const int* lins, int64_t nrot,
                                double q) {
   // engines.py:196-201 in binary64: cutoff = q * M* - 1e-9 (M* on the device
   // when dmstar is given)
-  if (dmstar) cutoff = q * (double)*dmstar - 1e-9;
+  // explicit roundings: nvcc would otherwise contract this into one DFMA
+  if (dmstar) cutoff = dsub(dmul(q, (double)*dmstar), 1e-9);
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrot;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int c = counts[r];

@@ -29,42 +29,8 @@
 //    closer than one bin per axis, so the rule is exact and order-free.
 #include <climits>
 #include <cstdio>
+#include <mutex>
 #include "dses_common.cuh"
-
-#ifndef DSES_NS4
-#define DSES_NS4 1  // four staged source points per slot while at least four remain
-#endif
-
-#ifndef DSES_DYNROT
-#define DSES_DYNROT 1  // rotations claimed from a global queue
-#endif
-#ifndef DSES_FRAC_IMAD
-#define DSES_FRAC_IMAD 1  // fractions on the multiply pipe (ALU-pipe relief, c2 -2.5%)
-#endif
-#ifndef DSES_FAR_GTHR
-#define DSES_FAR_GTHR 1  // far lanes: all-ones guard threshold (c2 -5%)
-#endif
-#ifndef DSES_EXACT_INLINE
-#define DSES_EXACT_INLINE __forceinline__  // __noinline__: smaller code, BRA.DIV-guarded syncs
-#endif
-#ifndef DSES_STAGE_SRC
-#define DSES_STAGE_SRC 1  // a unit's surviving sources staged per warp (no per-slot bit scans)
-#endif
-#ifndef DSES_POP_DENSE
-#define DSES_POP_DENSE 1  // units per claim when the round's overlap is dense
-#endif
-#ifndef DSES_B1_MASKS
-#define DSES_B1_MASKS 1  // per-group chunk masks computed one thread per group
-#endif
-#ifndef DSES_CHUNKBOX
-#define DSES_CHUNKBOX 1
-#endif
-#ifndef DSES_VOTE_FSH
-#define DSES_VOTE_FSH 1  // vote word value by a wrapping funnel shift
-#endif
-#ifndef DSES_POP
-#define DSES_POP 3  // units per claim when the round's overlap is sparse (c4: 3 vs 2 -0.9%)
-#endif
 
 namespace dses {
 
@@ -154,7 +120,7 @@ __device__ __forceinline__ void hist_inc(unsigned* hist, uint32_t hist_sh, int l
 // lands in the same bin for the same i (_kernels.py:144-158).
 // Returns (votes << 16) | rechecks.
 template <bool HSMEM, bool PSMEM>
-__device__ DSES_EXACT_INLINE unsigned vote_exact(const VoteParams& p, const double* R, const int4* P,
+__device__ __forceinline__ unsigned vote_exact(const VoteParams& p, const double* R, const int4* P,
                                             unsigned* hist, uint32_t hist_sh, int i, int j) {
   unsigned rechecks = 0;
   const int4 Pi = PSMEM ? P[i] : __ldcg(&P[i]);
@@ -176,7 +142,7 @@ __device__ DSES_EXACT_INLINE unsigned vote_exact(const VoteParams& p, const doub
 // converged around the slot loop's shuffles / votes (a call into a
 // non-inlined divergent function made it guard each of them with BRA.DIV).
 template <bool HSMEM, bool PSMEM>
-__device__ DSES_EXACT_INLINE unsigned flush_rare(const VoteParams& p, const double* R,
+__device__ __forceinline__ unsigned flush_rare(const VoteParams& p, const double* R,
                                                  const int4* P, unsigned* hist, uint32_t hist_sh,
                                                  uint32_t rare_sh, int n, int lane) {
   unsigned acc = 0;
@@ -214,9 +180,9 @@ __shared__ unsigned* g_exH;
 
 // Append the lanes in `dm` (pairs (i, j)) to the warp's exact-path list.
 template <bool HSMEM, bool PSMEM>
-__device__ __forceinline__ void defer_pairs(const VoteParams& p, const double* R, const int4* P,
-                                            unsigned* hist, uint32_t hist_sh, Lane& L, unsigned dm,
-                                            bool mine, int i, int j, int lane, unsigned lanemask_lt) {
+__device__ __forceinline__ void defer_pairs(const VoteParams& p, uint32_t hist_sh, Lane& L,
+                                            unsigned dm, bool mine, int i, int j, int lane,
+                                            unsigned lanemask_lt) {
   if (mine) sts_v2(L.rare_sh + 8u * (unsigned)(L.nrare + __popc(dm & lanemask_lt)), i, j);
   L.nrare += __popc(dm);
   if (L.nrare > kRare - 32) {
@@ -224,7 +190,6 @@ __device__ __forceinline__ void defer_pairs(const VoteParams& p, const double* R
                                            lane) & 0xffffu;
     L.nrare = 0;
   }
-  (void)R; (void)P; (void)hist;
 }
 
 // Fast-path constants in per-lane registers.
@@ -246,16 +211,11 @@ __device__ __forceinline__ PairBin fixed_bin(const FastK& k, const int4& Y, cons
   r.cand = (u0 < k.W0) & (u1 < k.W1) & (u2 < k.W2);
   // a candidate with every fraction >= 2G lies inside [0, D) (u in [D, W) has
   // a fraction < 2G) and its fixed-point bin u >> F is the exact bin
-#if DSES_FRAC_IMAD
   // the bins u >> F are needed anyway; the fractions u - (u >> F) * 2^F then
   // cost one IMAD each (FMA pipe) instead of an AND on the saturated ALU pipe
   const unsigned q0 = u0 >> k.F, q1 = u1 >> k.F, q2 = u2 >> k.F;
   r.near = r.cand & (__vimin3_u32(u0 + q0 * k.negP, u1 + q1 * k.negP, u2 + q2 * k.negP) < k.gthr);
   r.lin = (q0 * k.d1 + q1) * k.d2 + q2;
-#else
-  r.near = r.cand & (__vimin3_u32(u0 & k.fmask, u1 & k.fmask, u2 & k.fmask) < k.gthr);
-  r.lin = ((u0 >> k.F) * k.d1 + (u1 >> k.F)) * k.d2 + (u2 >> k.F);
-#endif
   return r;
 }
 
@@ -263,13 +223,9 @@ template <bool HSMEM>
 __device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsigned lin, bool ok,
                                         unsigned nbins = 0xffffffffu) {
   DSES_ASSERT(!ok || lin < nbins);
-#if DSES_VOTE_FSH
   // 1 << 16*(lin & 1) as a wrapping funnel shift of lin*16 (the multiply is
   // on the FMA pipe): one ALU instruction instead of an AND and a shift
   if (HSMEM) reds_add_if(hist_sh + ((lin + lin) & ~3u), __funnelshift_l(0u, 1u, lin << 4), ok);
-#else
-  if (HSMEM) reds_add_if(hist_sh + ((lin >> 1) << 2), 1u << ((lin & 1u) << 4), ok);
-#endif
   else if (ok) atomicAdd(&hist[lin], 1u);
 }
 
@@ -283,10 +239,9 @@ __device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsign
 // shuffles the group needs (0, 1, 2).
 template <bool HSMEM, bool PSMEM, int GP, int NS>
 __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, const double* R,
-                                          const int4* P, uint32_t P_sh, unsigned* hist,
-                                          uint32_t hist_sh, Lane& L, const int4& Y, int l0, int l1,
-                                          bool far, const int (&is_in)[NS], uint32_t src_sh,
-                                          int j, int lane, unsigned lanemask_lt) {
+                                          const int4* P, unsigned* hist, uint32_t hist_sh, Lane& L,
+                                          const int4& Y, int l0, int l1, uint32_t src_sh, int j,
+                                          int lane, unsigned lanemask_lt) {
   // NS source points per call: their independent work interleaves and the
   // warp votes / loop overhead are shared.
   PairBin b[NS];
@@ -294,16 +249,9 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
   bool any = false;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-#if DSES_STAGE_SRC
     // the unit's surviving sources, staged (Pq, i) per warp: uniform address
     const int4 Pi = lds_v4(src_sh + 16u * (unsigned)s);
     is[s] = Pi.w;
-    (void)is_in;
-#else
-    is[s] = is_in[s];
-    const int4 Pi = PSMEM ? lds_v4(P_sh + 16u * (unsigned)is[s]) : __ldcg(&P[is[s]]);
-    (void)src_sh;
-#endif
     b[s] = fixed_bin(fk, Y, Pi);
     any |= b[s].cand;
   }
@@ -312,44 +260,23 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     const bool decided = b[s].cand & !b[s].near;
-#if DSES_FAR_GTHR
     // far lanes carry an all-ones guard threshold: every candidate of theirs
     // is "near" (exact path), so `far` drops out of the per-pair logic
     bool ok = decided;
     defer[s] = b[s].near;
-    (void)far;
-#else
-    bool ok = decided & !far;
-    defer[s] = b[s].near | (decided & far);
-#endif
     if (GP > 0) {
       const int key = decided ? (int)b[s].lin : (b[s].near ? -2 : -1);
       const int k0 = __shfl_sync(0xffffffffu, key, l0 & 31);
-#if DSES_SAFE_LANES
       bool dup = k0 == key;  // l0 is always a lane: a partner or a safe one
       bool und = k0 == -2;
-#else
-      bool dup = (l0 >= 0) & (k0 == key);
-      bool und = (l0 >= 0) & (k0 == -2);
-#endif
       if (GP > 1) {
         const int k1 = __shfl_sync(0xffffffffu, key, l1 & 31);
-#if DSES_SAFE_LANES
         dup |= k1 == key;
         und |= k1 == -2;
-#else
-        dup |= (l1 >= 0) & (k1 == key);
-        und |= (l1 >= 0) & (k1 == -2);
-#endif
       }
       dup &= decided;
-#if DSES_FAR_GTHR
       ok = decided & !dup & !und;
       defer[s] = b[s].near | (decided & !dup & und);
-#else
-      ok = decided & !far & !dup & !und;
-      defer[s] = b[s].near | (decided & !dup & (far | und));
-#endif
     }
     vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins);
     DSES_ASSERT(is[s] >= 0 && is[s] < p.n && j >= 0 && j < p.m_pad);
@@ -359,8 +286,7 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const unsigned dm = __ballot_sync(0xffffffffu, defer[s]);
-      if (dm) defer_pairs<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L, dm, defer[s], is[s], j, lane,
-                                        lanemask_lt);
+      if (dm) defer_pairs<HSMEM, PSMEM>(p, hist_sh, L, dm, defer[s], is[s], j, lane, lanemask_lt);
     }
   }
 }
@@ -386,7 +312,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   off += 16 * 8;
   int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + counters
   off += 4 * 32 * 4;
-  int* units = reinterpret_cast<int*>(smem + off);  // [unit_cap] overlapping (group, unit) pairs
+  unsigned* units = reinterpret_cast<unsigned*>(smem + off);  // [unit_cap] (group << 16 | unit)
   off += (size_t)p.unit_cap * 4;
   int2* rare = reinterpret_cast<int2*>(smem + off) + warp * kRare;
   off += (size_t)nwarps * kRare * 8;
@@ -428,15 +354,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 
   unsigned long long st_pairs = 0, st_votes = 0;
   const bool exact_mode = (p.F == 0);
-  // reference groups per round so that the round's units fit `units`
-#if DSES_B1_MASKS
   // reference groups per round so that the round's units AND one chunk mask
   // per group (stored at the tail of `units`) fit
   const int tiles_per_round = max(1, p.unit_cap / max(1, p.nxt + 1));
-  const bool masks = DSES_CHUNKBOX && !exact_mode && nxc > 1 && nxc <= 32;
-#else
-  const int tiles_per_round = max(1, p.unit_cap / max(1, p.nxt));
-#endif
+  const bool masks = !exact_mode && nxc > 1 && nxc <= 32;
 
   // rotations: the first one static, the rest from a global queue (the cost
   // of a rotation varies with its angle; dynamic claims balance the tail)
@@ -491,7 +412,6 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     for (int b0 = 0; b0 < p.nyt; b0 += tiles_per_round) {
       const int b1 = min(p.nyt, b0 + tiles_per_round);
       if (tid == 0) { *s_nunits = 0; *s_next = 0; }
-#if DSES_B1_MASKS
       // which 32-unit chunks each group can reach: one thread per group
       // (instead of a warp-uniform test per (group, chunk))
       unsigned* gmask = reinterpret_cast<unsigned*>(units) + (p.unit_cap - tiles_per_round);
@@ -503,11 +423,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
             if (boxes_meet(p, yg, CB[2 * c], CB[2 * c + 1])) mk |= 1u << c;
           gmask[k] = mk;
         }
-#endif
       __syncthreads();
       for (int b = b0 + warp; b < b1; b += nwarps) {
         const YTile yt = load_ytile(p.yt, b);
-#if DSES_B1_MASKS
         if (masks) {
           for (unsigned mk = gmask[b - b0]; mk; mk &= mk - 1) {
             const int a = 32 * (__ffs(mk) - 1) + lane;
@@ -517,15 +435,14 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
               int slot = 0;
               if (lane == 0) slot = atomicAdd(s_nunits, __popc(m));
               slot = __shfl_sync(0xffffffffu, slot, 0);
-              if (ov) units[slot + __popc(m & lanemask_lt)] = (b << 16) | a;
+              if (ov) units[slot + __popc(m & lanemask_lt)] = ((unsigned)b << 16) | (unsigned)a;
             }
           }
           continue;
         }
-#endif
         for (int a0 = 0; a0 < p.nxt; a0 += 32) {
           // whole chunk outside the group's reach: one warp-uniform test
-          if (DSES_CHUNKBOX && nxc > 1 && !exact_mode &&
+          if (nxc > 1 && !exact_mode &&
               !boxes_meet(p, yt, CB[2 * (a0 >> 5)], CB[2 * (a0 >> 5) + 1]))
             continue;
           const int a = a0 + lane;
@@ -535,16 +452,16 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
             int slot = 0;
             if (lane == 0) slot = atomicAdd(s_nunits, __popc(m));
             slot = __shfl_sync(0xffffffffu, slot, 0);
-            if (ov) units[slot + __popc(m & lanemask_lt)] = (b << 16) | a;
+            if (ov) units[slot + __popc(m & lanemask_lt)] = ((unsigned)b << 16) | (unsigned)a;
           }
         }
       }
       __syncthreads();
       const int nunits = *s_nunits;
       // sparse overlap (< 1/4 of the round's (group, unit) pairs) means light
-      // units: claim DSES_POP at a time to amortise the claim; dense overlap
+      // units: claim three at a time to amortise the claim; dense overlap
       // (heavy units) claims one at a time to keep the round's tail balanced
-      const int kpop = (4 * nunits < (b1 - b0) * p.nxt) ? DSES_POP : DSES_POP_DENSE;
+      const int kpop = (4 * nunits < (b1 - b0) * p.nxt) ? 3 : 1;
       for (int u = nunits, uend = nunits;; ++u) {
         if (u >= uend) {  // claim the next kpop units
           if (lane == 0) u = atomicAdd(s_next, kpop);
@@ -552,22 +469,19 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
           if (u >= nunits) break;
           uend = min(nunits, u + kpop);
         }
-        const int unit = units[u];
-        const YTile yt = load_ytile(p.yt, unit >> 16);
-        const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + (unit & 0xffff)));
+        const unsigned unit = units[u];
+        const YTile yt = load_ytile(p.yt, (int)(unit >> 16));
+        const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + (unit & 0xffffu)));
         const int ustart = U.x, ucount = U.y;
         const int gp = yt.gm;  // partner shuffles this group needs (warp-uniform)
         const bool valid = lane < yt.count;
         const int j = yt.start + (valid ? lane : 0);
         int4 Y = __ldg(&p.yq[j]);
         if (!valid) Y = make_int4(kNoRef, 0, 0, 0);
-        const bool far = (Y.w & kFarFlag) != 0;
-#if DSES_FAR_GTHR
+        // far lanes carry an all-ones guard threshold: every candidate of
+        // theirs is "near" (exact path)
         FastK fkl = fk;
-        fkl.gthr = far ? 0xffffffffu : fk.gthr;
-#else
-        const FastK& fkl = fk;
-#endif
+        fkl.gthr = (Y.w & kFarFlag) ? 0xffffffffu : fk.gthr;
         const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
         bool sok = false;
         int4 Pl = make_int4(0, 0, 0, 0);
@@ -579,7 +493,6 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         }
         unsigned sm = __ballot_sync(0xffffffffu, sok);
         if (lane == 0) st_pairs += (unsigned long long)__popc(sm) * (unsigned)yt.count;
-#if DSES_STAGE_SRC
         const int nsrc = __popc(sm);
         // opaque copy: keeps the stage base in a register (otherwise it is
         // re-derived from kernel parameters in every slot)
@@ -589,52 +502,19 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         if (sok) sts_v4(sbase + 16u * (unsigned)__popc(sm & lanemask_lt),
                         make_int4(Pl.x, Pl.y, Pl.z, ustart + lane));
         __syncwarp();
-#else
-        (void)Pl;
-#endif
-#if DSES_STAGE_SRC
 #define DSES_SLOTS(GP)                                                                         \
   int t = 0;                                                                                   \
-  if (DSES_NS4)                                                                                \
-    for (; t + 3 < nsrc; t += 4) {                                                             \
-      const int four[4] = {0, 0, 0, 0};                                                        \
-      vote_slot<HSMEM, PSMEM, GP, 4>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
-                                     four, sbase + 16u * (unsigned)t, j, lane, lanemask_lt);   \
-    }                                                                                          \
+  for (; t + 3 < nsrc; t += 4)                                                                 \
+    vote_slot<HSMEM, PSMEM, GP, 4>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,                  \
+                                   sbase + 16u * (unsigned)t, j, lane, lanemask_lt);            \
   for (; t < nsrc; t += 2) {                                                                   \
-    const int none[2] = {0, 0};                                                                \
-    if (t + 1 < nsrc) {                                                                        \
-      vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
-                                     none, sbase + 16u * (unsigned)t, j, lane, lanemask_lt);\
-    } else {                                                                                   \
-      const int one[1] = {0};                                                                  \
-      vote_slot<HSMEM, PSMEM, GP, 1>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far,      \
-                                     one, sbase + 16u * (unsigned)t, j, lane, lanemask_lt); \
-    }                                                                                          \
+    if (t + 1 < nsrc)                                                                          \
+      vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,                \
+                                     sbase + 16u * (unsigned)t, j, lane, lanemask_lt);          \
+    else                                                                                       \
+      vote_slot<HSMEM, PSMEM, GP, 1>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,                \
+                                     sbase + 16u * (unsigned)t, j, lane, lanemask_lt);          \
   }
-#else
-#define DSES_SLOTS(GP)                                                                         \
-  while (sm) {                                                                                 \
-    const int i0 = ustart + __ffs(sm) - 1;                                                     \
-    sm &= sm - 1;                                                                              \
-    if (DSES_NS4 && __popc(sm) >= 3) {                                                         \
-      int is[4];                                                                               \
-      is[0] = i0;                                                                              \
-      for (int q = 1; q < 4; ++q) { is[q] = ustart + __ffs(sm) - 1; sm &= sm - 1; }            \
-      vote_slot<HSMEM, PSMEM, GP, 4>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
-                                     0u, j, lane, lanemask_lt);                                    \
-    } else if (sm) {                                                                           \
-      const int is[2] = {i0, ustart + __ffs(sm) - 1};                                          \
-      sm &= sm - 1;                                                                            \
-      vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
-                                     0u, j, lane, lanemask_lt);                                    \
-    } else {                                                                                   \
-      const int is[1] = {i0};                                                                  \
-      vote_slot<HSMEM, PSMEM, GP, 1>(p, fkl, R, P, P_sh, hist, hist_sh, L, Y, l0, l1, far, is,  \
-                                     0u, j, lane, lanemask_lt);                                    \
-    }                                                                                          \
-  }
-#endif
         if (gp == 0) { DSES_SLOTS(0) }
         else if (gp == 1) { DSES_SLOTS(1) }
         else { DSES_SLOTS(2) }
@@ -717,8 +597,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         p.counts[rr] = best;
         p.lins[rr] = best > 0 ? blin : -1;
         p.ties[rr] = best > 0 ? bties : 0;
-        s_rr = DSES_DYNROT ? (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull)
-                           : rr + gridDim.x;
+        s_rr = (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull);
       }
     }
     __syncthreads();
@@ -750,14 +629,38 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
   return b;
 }
 
+// The dynamic shared-memory limit of each instantiation is raised ONCE per
+// device to the opt-in maximum (minus its static shared memory) and never
+// lowered: plan construction on one thread and launches on another must not
+// race on this process-wide attribute (a lowered limit between another
+// thread's set and launch would fail that launch).
+template <bool H, bool PS>
+static cudaError_t raise_smem_limit() {
+  static std::once_flag once[64];
+  static cudaError_t err[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    int optin = 0;
+    cudaFuncAttributes a{};
+    err[dev] = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (err[dev] == cudaSuccess) err[dev] = cudaFuncGetAttributes(&a, vote_kernel<H, PS>);
+    if (err[dev] == cudaSuccess)
+      err[dev] = cudaFuncSetAttribute(vote_kernel<H, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      optin - (int)a.sharedSizeBytes);
+  });
+  return err[dev];
+}
+
 cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, int threads,
                         cudaStream_t stream) {
   const size_t smem = vote_smem_bytes(p, hsmem, psmem, threads);
   cudaError_t e;
-#define DSES_LAUNCH(H, PS)                                                                    \
-  e = cudaFuncSetAttribute(vote_kernel<H, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                           (int)smem);                                                        \
-  if (e != cudaSuccess) return e;                                                             \
+#define DSES_LAUNCH(H, PS)                          \
+  e = raise_smem_limit<H, PS>();                    \
+  if (e != cudaSuccess) return e;                   \
   vote_kernel<H, PS><<<grid, threads, smem, stream>>>(p);
   if (hsmem && psmem) { DSES_LAUNCH(true, true) }
   else if (hsmem) { DSES_LAUNCH(true, false) }
@@ -783,9 +686,10 @@ int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int thread
   const size_t smem = vote_smem_bytes(p, hsmem, psmem, threads);
   int n = 0;
   cudaError_t e;
-#define DSES_OCC(H, PS)                                                                            \
-  cudaFuncSetAttribute(vote_kernel<H, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<H, PS>, threads, smem);
+#define DSES_OCC(H, PS)                                                                    \
+  e = raise_smem_limit<H, PS>();                                                           \
+  if (e == cudaSuccess)                                                                    \
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<H, PS>, threads, smem);
   if (hsmem && psmem) { DSES_OCC(true, true) }
   else if (hsmem) { DSES_OCC(true, false) }
   else if (psmem) { DSES_OCC(false, true) }

@@ -325,10 +325,10 @@ def test_dses_batch_error_order_and_async_misuse(api):
     p = prepare(pairs[0][0], pairs[0][1], cfg)
     g = _native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot)
     with _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims) as plan:
-        with pytest.raises(ValueError):  # _native maps DSES_E_INVALID to ValueError
+        with pytest.raises(api.InvalidInputError):  # _native maps DSES_E_INVALID (a ValueError)
             plan.search_wait()  # nothing in flight
         plan.search_async(g, cfg.q, p.code, p.param, p.skip_refine)
-        with pytest.raises(ValueError):
+        with pytest.raises(api.InvalidInputError):
             plan.search_async(g, cfg.q, p.code, p.param, p.skip_refine)  # one at a time
         r = plan.search_wait()
         r2 = plan.search(g, cfg.q, p.code, p.param, p.skip_refine)
