@@ -62,22 +62,6 @@ __device__ __forceinline__ bool pair_bin(const VoteParams& p, const double* R, c
 
 constexpr int kRare = 64;       // per-warp list of deferred (i, j) pairs
 
-// Rotated sphere (centre +- radius, a rotation preserves |x - c|) of a source
-// tile as a fixed-point box; .w carries the tile's point range.
-__device__ __forceinline__ void tile_box(const VoteParams& p, const double* R, const XTile& t,
-                                         bool exact_mode, int4& lo, int4& hi) {
-  if (exact_mode) {
-    lo = make_int4(INT_MIN / 4, INT_MIN / 4, INT_MIN / 4, t.start);
-    hi = make_int4(INT_MAX / 4, INT_MAX / 4, INT_MAX / 4, t.start + t.count);
-    return;
-  }
-  const int c0 = __double2int_rn(rot_row(R, 0, t.c[0], t.c[1], t.c[2]) * p.inv_s);
-  const int c1 = __double2int_rn(rot_row(R, 1, t.c[0], t.c[1], t.c[2]) * p.inv_s);
-  const int c2 = __double2int_rn(rot_row(R, 2, t.c[0], t.c[1], t.c[2]) * p.inv_s);
-  lo = make_int4(c0 - t.rad, c1 - t.rad, c2 - t.rad, t.start);
-  hi = make_int4(c0 + t.rad, c1 + t.rad, c2 + t.rad, t.start + t.count);
-}
-
 // Can a source box [lo, hi] and the reference tile bbox produce u = Yq - Pq in [0, W)?
 __device__ __forceinline__ bool boxes_meet(const VoteParams& p, const YTile& yt, const int4& lo,
                                            const int4& hi) {
@@ -256,12 +240,28 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
     any |= b[s].cand;
   }
   if (!__any_sync(0xffffffffu, any)) return;
+  bool anynear = false;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) anynear |= b[s].near;
+  if (!__any_sync(0xffffffffu, anynear)) {
+    // common case: no candidate of the slot is near a bin edge, so every
+    // candidate is decided and a partner's key is its exact bin or -1
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      bool ok = b[s].cand;
+      if (GP > 0) {
+        const int key = b[s].cand ? (int)b[s].lin : -1;
+        ok &= __shfl_sync(0xffffffffu, key, l0 & 31) != key;
+        if (GP > 1) ok &= __shfl_sync(0xffffffffu, key, l1 & 31) != key;
+      }
+      vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins);
+    }
+    return;
+  }
   bool defer[NS], anydef = false;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     const bool decided = b[s].cand & !b[s].near;
-    // far lanes carry an all-ones guard threshold: every candidate of theirs
-    // is "near" (exact path), so `far` drops out of the per-pair logic
     bool ok = decided;
     defer[s] = b[s].near;
     if (GP > 0) {
@@ -325,21 +325,21 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   const uint32_t P_sh = PSMEM ? (uint32_t)__cvta_generic_to_shared(P) : 0u;
   // fast-path constants through shared memory: loaded into regular registers
   // once, instead of being re-loaded into uniform registers in the hot loop
-  __shared__ unsigned kc[10];
+  __shared__ __align__(16) unsigned kc[12];
+  __shared__ unsigned long long s_pairs[kVoteThreads / 32];  // per-warp evaluated-pair counts
   if (tid == 0) {
     kc[0] = p.W0; kc[1] = p.W1; kc[2] = p.W2; kc[3] = p.fmask; kc[4] = p.gthr;
     kc[5] = (unsigned)p.d1; kc[6] = (unsigned)p.d2; kc[7] = (unsigned)p.F;
     kc[8] = HSMEM ? (uint32_t)__cvta_generic_to_shared(hist) : 0u;
     kc[9] = 0u - (1u << p.F);
+    kc[10] = kc[11] = 0u;
     g_exR = R;
     g_exP = P;
     g_exH = hist;
   }
   __syncthreads();
-  FastK fk;
-  fk.W0 = kc[0]; fk.W1 = kc[1]; fk.W2 = kc[2]; fk.fmask = kc[3]; fk.gthr = kc[4];
-  fk.d1 = kc[5]; fk.d2 = kc[6]; fk.F = (int)kc[7]; fk.negP = kc[9];
   const uint32_t hist_sh = kc[8];
+  if (lane == 0) s_pairs[warp] = 0;
   Lane L;
   // opaque copy: a register, not re-derived from kernel parameters per slot
   asm volatile("mov.u32 %0, %1;" : "=r"(L.rare_sh) : "r"((uint32_t)__cvta_generic_to_shared(rare)));
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     if (HSMEM) hist4[w] = make_uint4(0, 0, 0, 0); else __stcg(&hist4[w], make_uint4(0, 0, 0, 0));
   }
 
-  unsigned long long st_pairs = 0, st_votes = 0;
+  unsigned long long st_votes = 0;
   const bool exact_mode = (p.F == 0);
   // reference groups per round so that the round's units AND one chunk mask
   // per group (stored at the tail of `units`) fit
@@ -368,34 +368,48 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     __syncthreads();
 
     // ---- A: rotated source points in fixed point (binary64 in the reference's
-    //      operation order, then one rounding) and rotated unit boxes
-    for (int i = tid; i < p.n; i += nthreads) {
-      const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
+    //      operation order, then one rounding); warp = source unit, lane =
+    //      point, and the unit's exact rotated bounding box (fixed point, the
+    //      same values the per-source test sees) by warp min/max reductions --
+    //      much tighter than a rotated bounding sphere for flat units
+    for (int a = warp; a < p.nxt; a += nwarps) {
+      const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + a));  // start, count
+      const bool valid = lane < U.y;
+      const int i = U.x + (valid ? lane : 0);
       int4 v = make_int4(0, 0, 0, 0);
-      if (!exact_mode) {
+      if (valid && !exact_mode) {
+        const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
         v.x = __double2int_rn(dmul(rot_row(R, 0, x0, x1, x2), p.inv_s));
         v.y = __double2int_rn(dmul(rot_row(R, 1, x0, x1, x2), p.inv_s));
         v.z = __double2int_rn(dmul(rot_row(R, 2, x0, x1, x2), p.inv_s));
       }
-      if (PSMEM) P[i] = v; else __stcg(&P[i], v);
+      if (valid) { if (PSMEM) P[i] = v; else __stcg(&P[i], v); }
+      int4 lo, hi;
+      if (exact_mode) {
+        lo = make_int4(INT_MIN / 4, INT_MIN / 4, INT_MIN / 4, U.x);
+        hi = make_int4(INT_MAX / 4, INT_MAX / 4, INT_MAX / 4, U.x + U.y);
+      } else {
+        lo = make_int4(__reduce_min_sync(0xffffffffu, valid ? v.x : INT_MAX),
+                       __reduce_min_sync(0xffffffffu, valid ? v.y : INT_MAX),
+                       __reduce_min_sync(0xffffffffu, valid ? v.z : INT_MAX), U.x);
+        hi = make_int4(__reduce_max_sync(0xffffffffu, valid ? v.x : INT_MIN),
+                       __reduce_max_sync(0xffffffffu, valid ? v.y : INT_MIN),
+                       __reduce_max_sync(0xffffffffu, valid ? v.z : INT_MIN), U.x + U.y);
+      }
+      if (lane == 0) { XB[2 * a] = lo; XB[2 * a + 1] = hi; }
     }
-    for (int c = warp; c < nxc; c += nwarps) {  // warp = chunk, lane = unit
+    __syncthreads();
+    for (int c = warp; c < nxc; c += nwarps) {  // warp = chunk, lane = unit: chunk union boxes
       const int t = 32 * c + lane;
-      int4 lo = make_int4(INT_MAX, INT_MAX, INT_MAX, 0), hi = make_int4(INT_MIN, INT_MIN, INT_MIN, 0);
-      if (t < p.nxt) {
-        tile_box(p, R, p.xt[t], exact_mode, lo, hi);
-        XB[2 * t] = lo;
-        XB[2 * t + 1] = hi;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo.x = min(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
-        lo.y = min(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, o));
-        lo.z = min(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, o));
-        hi.x = max(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, o));
-        hi.y = max(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, o));
-        hi.z = max(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, o));
-      }
+      const bool valid = t < p.nxt;
+      int4 lo = valid ? XB[2 * t] : make_int4(INT_MAX, INT_MAX, INT_MAX, 0);
+      int4 hi = valid ? XB[2 * t + 1] : make_int4(INT_MIN, INT_MIN, INT_MIN, 0);
+      lo.x = __reduce_min_sync(0xffffffffu, lo.x);
+      lo.y = __reduce_min_sync(0xffffffffu, lo.y);
+      lo.z = __reduce_min_sync(0xffffffffu, lo.z);
+      hi.x = __reduce_max_sync(0xffffffffu, hi.x);
+      hi.y = __reduce_max_sync(0xffffffffu, hi.y);
+      hi.z = __reduce_max_sync(0xffffffffu, hi.z);
       if (lane == 0) { CB[2 * c] = lo; CB[2 * c + 1] = hi; }
     }
     __syncthreads();
@@ -480,8 +494,16 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         if (!valid) Y = make_int4(kNoRef, 0, 0, 0);
         // far lanes carry an all-ones guard threshold: every candidate of
         // theirs is "near" (exact path)
-        FastK fkl = fk;
-        fkl.gthr = (Y.w & kFarFlag) ? 0xffffffffu : fk.gthr;
+        // the fast-path constants come from shared memory per unit (nothing of
+        // them stays live in registers outside the slot loop)
+        FastK fkl;
+        {
+          const uint4 k0 = *reinterpret_cast<const uint4*>(kc);
+          const uint4 k1 = *reinterpret_cast<const uint4*>(kc + 4);
+          fkl.W0 = k0.x; fkl.W1 = k0.y; fkl.W2 = k0.z; fkl.fmask = k0.w;
+          fkl.gthr = (Y.w & kFarFlag) ? 0xffffffffu : k1.x;
+          fkl.d1 = k1.y; fkl.d2 = k1.z; fkl.F = (int)k1.w; fkl.negP = kc[9];
+        }
         const int l0 = (Y.w & 63) - 1, l1 = ((Y.w >> 6) & 63) - 1;
         bool sok = false;
         int4 Pl = make_int4(0, 0, 0, 0);
@@ -492,7 +514,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
                                (yt.hi[2] - Pl.z >= 0) & (yt.lo[2] - Pl.z < (int)p.W2));
         }
         unsigned sm = __ballot_sync(0xffffffffu, sok);
-        if (lane == 0) st_pairs += (unsigned long long)__popc(sm) * (unsigned)yt.count;
+        if (lane == 0) s_pairs[warp] += (unsigned long long)__popc(sm) * (unsigned)yt.count;
         const int nsrc = __popc(sm);
         // opaque copy: keeps the stage base in a register (otherwise it is
         // re-derived from kernel parameters in every slot)
@@ -605,7 +627,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   }
 
   // kernel statistics
-  unsigned long long st_rechecks = L.rechecks;
+  unsigned long long st_rechecks = L.rechecks, st_pairs = lane == 0 ? s_pairs[warp] : 0ull;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     st_pairs += __shfl_xor_sync(0xffffffffu, st_pairs, o);
