@@ -40,6 +40,7 @@ size_t sparse_scratch_bytes(int64_t n, int64_t m);
 cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t r_count,
                                 void* scratch, size_t scratch_bytes, unsigned long long* counters,
                                 int* counts, long long* lins, int* ties, int sms, cudaStream_t st);
+cudaError_t launch_narrow_lins(const long long* in, int* out, int64_t n, int sms, cudaStream_t st);
 cudaError_t launch_sparse_histogram(const SparseParams& s, bool dedup, void* scratch,
                                     size_t scratch_bytes, unsigned long long* counter,
                                     unsigned long long** out_lins, int** out_counts, int** out_n,
@@ -970,6 +971,11 @@ int set_grid(dses_plan* P, const dses_grid* g, RotSource* rs, cudaStream_t st) {
   return DSES_OK;
 }
 
+// Flat bins of the lattice fit the search's int32 candidate arrays.
+static bool lattice_fits_int32(const dses_plan* P) {
+  return (double)P->dims[0] * (double)P->dims[1] * (double)P->dims[2] < 2147483647.0;
+}
+
 static SparseParams sparse_params(const dses_plan* P, const RotSource& rs) {
   SparseParams sp{};
   sp.n = (int)P->n;
@@ -985,6 +991,11 @@ static SparseParams sparse_params(const dses_plan* P, const RotSource& rs) {
   return sp;
 }
 
+// Sort-based mode batch (the reference's mode_sparse_batch, _kernels.py:196-294)
+// for lattices beyond kDenseMaxBins.  When the lattice has < 2^31 bins the
+// flat bins are also narrowed to the int32 array the search's select / score
+// stages read, so dses() runs on such lattices like the reference
+// (mode_search.py:158-163 dispatches them to its sparse kernel).
 int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
   CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1), st));
   CK(P->lins64.ensure(sizeof(long long) * std::max<int64_t>(r_count, 1), st));
@@ -1001,6 +1012,10 @@ int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_cou
                                   P->scal.as<unsigned long long>() + 6, P->counts.as<int>(),
                                   P->lins64.as<long long>(), P->ties.as<int>(), P->sms, st),
               (int)(5 * r_count)));
+  if (lattice_fits_int32(P)) {
+    CK(P->lins.ensure(sizeof(int) * std::max<int64_t>(r_count, 1), st));
+    CK(launched(launch_narrow_lins(P->lins64.as<long long>(), P->lins.as<int>(), r_count, P->sms, st)));
+  }
   return DSES_OK;
 }
 
@@ -1298,10 +1313,10 @@ extern "C" int dses_stage_vote(dses_plan* P, const dses_grid* g, int64_t r_begin
                                int64_t* mstar_local, int64_t* valid_local, void* stream) {
   TrafficScope ts_(P);
   if (!P || !g) return fail(DSES_E_INVALID, "bad arguments");
-  if (P->sparse)
-    return fail(DSES_E_INVALID, "translation window of %.3g bins is beyond the search's dense "
-                "limit (%d bins); mode queries (dses_mode_*) support it",
-                (double)P->dims[0] * P->dims[1] * P->dims[2], kDenseMaxBins);
+  if (!lattice_fits_int32(P))
+    return fail(DSES_E_LIMIT, "translation window of %.3g bins: the search supports lattices "
+                "below 2^31 bins (mode queries, dses_mode_*, support any size)",
+                (double)P->dims[0] * P->dims[1] * P->dims[2]);
   CK(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t total = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);
@@ -1520,7 +1535,6 @@ static int reserve_search(dses_plan* P, int64_t nr, cudaStream_t st = 0) {
 extern "C" int dses_plan_reserve(dses_plan* P, int64_t r_count) {
   if (!P || r_count < 0) return fail(DSES_E_INVALID, "bad arguments");
   CK(cudaSetDevice(P->device));
-  if (P->sparse) return DSES_OK;
   cudaStream_t st = upload_stream(P->device);
   const int rc = reserve_search(P, r_count, st);
   if (rc) return rc;
@@ -1543,9 +1557,10 @@ extern "C" int dses_search_async(dses_plan* P, const dses_grid* g, int64_t r_beg
   const int64_t total = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);
   if (r_count < 0) r_count = total - r_begin;
   if (r_begin < 0 || r_begin + r_count > total) return fail(DSES_E_INVALID, "rotation range beyond the grid");
-  if (P->sparse)
-    return fail(DSES_E_INVALID, "translation window of %.3g bins is beyond the search's dense "
-                "limit (%d bins)", (double)P->dims[0] * P->dims[1] * P->dims[2], kDenseMaxBins);
+  if (!lattice_fits_int32(P))
+    return fail(DSES_E_LIMIT, "translation window of %.3g bins: the search supports lattices "
+                "below 2^31 bins (mode queries, dses_mode_*, support any size)",
+                (double)P->dims[0] * P->dims[1] * P->dims[2]);
   {
     const int rr = reserve_search(P, r_count);
     if (rr) return rr;

@@ -192,6 +192,20 @@ cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t 
   return cudaSuccess;
 }
 
+// Flat bins of a sort-based mode batch narrowed to the int32 the search's
+// select / score stages read (the lattice is < 2^31 bins there).
+__global__ void narrow_lins_kernel(const long long* __restrict__ in, int* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int)in[i];
+}
+
+cudaError_t launch_narrow_lins(const long long* in, int* out, int64_t n, int sms, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 4, (n + 255) / 256));
+  narrow_lins_kernel<<<blocks, 256, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+
 // The full vote map of one rotation (mode_search.translation_histogram,
 // mode_search.py:205-235): keys of rotation 0 of `s.rot` sorted, deduplicated
 // per (bin, source) when `dedup`, run-length encoded by bin.  Outputs live in

@@ -129,11 +129,9 @@ def prepare(source, reference, cfg: SearchConfig) -> Prepared:
     dims = np.full(3, 2 * cfg.k_trans + 1, dtype=np.int64)
     nbins = int(dims[0]) ** 3
     check_key_space(nbins, x.shape[0])
-    if nbins > DENSE_MAX_BINS:
-        # the search needs the dense vote (mode queries, mode_translation, take
-        # larger lattices through the sort-based path)
-        raise InvalidInputError(
-            f"translation window of {nbins} bins exceeds the GPU search limit of {DENSE_MAX_BINS}")
+    # windows beyond DENSE_MAX_BINS run the sort-based vote (the reference's
+    # mode_sparse_batch, mode_search.py:158-163); beyond 2^31 bins the native
+    # search raises SearchSpaceTooLargeError
     code, param = cfg.metric._code_param()
     skip = cfg.metric.kind == "sat_l0" and cfg.metric.param == cfg.trans_bin  # engines.py:265
     return Prepared(x, y, cos_tab, sin_tab, center_rot, ilo, dims, code, param, skip)

@@ -291,6 +291,49 @@ def test_sparse_window_matches_dict_histogram():
         assert O.decode_flat(lins[r], ilo, dims) == idx
 
 
+@pytest.mark.parametrize("kind,param", [("trunc_l1", None), ("sat_l0", 0.004)])
+def test_dses_sparse_window_matches_oracle(api, kind, param):
+    """dses with k_trans = 210 (421^3 = 74.6 M bins > 2^26): the search runs
+    the sort-based vote, as the reference dispatches such windows to
+    mode_sparse_batch (mode_search.py:158-163, _kernels.py:196-294); per-rotation
+    votes, winner, refine counts and errors against the oracle."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-0.3, 0.3, (160, 3))
+    rot = api.rotation_from_euler((0.02, -0.03, 0.04))
+    y = np.concatenate([x[:120] @ rot.T + np.array([0.11, -0.07, 0.05]) +
+                        rng.normal(0, 0.001, (120, 3)), rng.uniform(-0.4, 0.4, (60, 3))])
+    cfg = api.SearchConfig(k_rot=1, rot_step=0.03, k_trans=210, trans_bin=0.004,
+                           metric=None if param is None else api.ErrorMetric(kind, param))
+    res = api.dses(x, y, cfg)
+    ref = O.dses(x, y, k_rot=cfg.k_rot, rot_step=cfg.rot_step, k_trans=cfg.k_trans,
+                 trans_bin=cfg.trans_bin, q=cfg.q, metric=(kind, param), return_votes=True,
+                 nthreads=2)  # 600 MB of oracle scratch per thread at this lattice
+    assert tuple(res.best.grid_coords) == tuple(ref["grid_coords"])
+    assert np.array_equal(res.best.translation, ref["translation"])
+    assert math.isclose(res.best_error, ref["best_error"], rel_tol=1e-9, abs_tol=1e-12)
+    assert res.best_inliers == ref["best_inliers"]
+    assert res.candidates_evaluated == ref["candidates_evaluated"]
+    assert res.candidates_refined == ref["candidates_refined"]
+    from paper_2502_00115_b200 import _native
+    from paper_2502_00115_b200.engines import prepare
+    p = prepare(x, y, cfg)
+    g = _native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot)
+    with _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims) as plan:
+        counts, lins, ties = plan.mode_grid(g, 0, cfg.rotation_count)
+    assert np.array_equal(counts, ref["counts"]) and np.array_equal(lins, ref["lins"])
+    assert np.array_equal(ties, ref["ties"])
+
+
+def test_dses_window_beyond_int32_lattice_raises(api):
+    """Beyond 2^31 bins the search raises the reference's SearchSpaceTooLargeError
+    (a documented limit: the candidate arrays hold 32-bit flat bins)."""
+    x = np.random.default_rng(2).uniform(-0.1, 0.1, (8, 3))
+    cfg = api.SearchConfig(k_rot=0, rot_step=0.1, k_trans=700, trans_bin=0.001)
+    with pytest.raises(api.SearchSpaceTooLargeError):
+        api.dses(x, x, cfg)
+
+
 def test_dses_batch_equals_single_calls(api):
     from paper_2502_00115_b200.synth import CONFIGS, make_pair
     pairs = [make_pair(CONFIGS["c1"]["spec"], s) for s in range(4)]
