@@ -186,6 +186,30 @@ int dses_stage_row_info(dses_plan* plan, int64_t row, int64_t* lin, int64_t* cou
 int dses_pose_error(dses_plan* plan, const dses_grid* grid, int64_t row, int64_t lin,
                     int metric_code, double metric_param, double* err, void* stream);
 /* Kernel statistics accumulated since the last call (pairs, votes, rechecks). */
+/* ---- device-resident sharded search --------------------
+ * engines.dses with the rotation grid split over ranks, exchange values kept
+ * in DEVICE memory: `xchg` is an int64[7] device buffer of the caller that it
+ * reduces with NCCL between the calls (all on `stream`, no host round trip):
+ *   dses_shard_vote    vote over the rank's slice; x[0] = local M*, x[3] =
+ *                      rotations with a vote               -> all_reduce x[0] MAX
+ *   dses_shard_select  cutoff from the GLOBAL M* in x[0], fp32 screen, exact
+ *                      re-score, local winner: x[1] = binary64 bits of its
+ *                      error, x[2] = row << 32 | flat bin, x[4] = kept,
+ *                      x[6] = overflow (fall back to dses_stage_*)
+ *                                                          -> all_reduce x[1] MIN
+ *   dses_shard_key     x[2] = all-ones unless this rank holds the minimum error
+ *                                                          -> all_reduce x[2] MIN
+ *   dses_shard_miss    x[5] = the winner's sat_l0 miss bits on its rank, else 0
+ *                                                          -> all_reduce x[3..6] SUM
+ * Replaces engines.py:254-301 (M*, the q*M* cutoff, min-error / lexicographic
+ * winner, candidates_evaluated / _refined, best_inliers) across ranks. */
+int dses_shard_vote(dses_plan* plan, const dses_grid* grid, int64_t r_begin, int64_t r_count,
+                    int64_t* xchg, void* stream);
+int dses_shard_select(dses_plan* plan, double q, int metric_code, double metric_param,
+                      int skip_refine, int64_t* xchg, void* stream);
+int dses_shard_key(dses_plan* plan, int64_t* xchg, void* stream);
+int dses_shard_miss(dses_plan* plan, int64_t* xchg, void* stream);
+
 int dses_stage_stats(dses_plan* plan, int64_t* pairs, int64_t* votes, int64_t* rechecks);
 /* Host<->device bytes and kernel launches attributed to this plan (plan
  * creation included); reset != 0 zeroes the counters after reading. */

@@ -96,6 +96,11 @@ _SIGS = [
     ("dses_pose_error", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, ctypes.c_int,
                                        ctypes.c_double, _dp, _vp]),
     ("dses_stage_stats", ctypes.c_int, [_vp, _ip, _ip, _ip]),
+    ("dses_shard_vote", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, _vp, _vp]),
+    ("dses_shard_select", ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                         ctypes.c_int, _vp, _vp]),
+    ("dses_shard_key", ctypes.c_int, [_vp, _vp, _vp]),
+    ("dses_shard_miss", ctypes.c_int, [_vp, _vp, _vp]),
     ("dses_plan_traffic", ctypes.c_int, [_vp, _ip, _ip, _ip, ctypes.c_int]),
     ("dses_sweep_inlier_best", ctypes.c_int, [ctypes.c_int, _dp, _i64, _i64, ctypes.c_double,
                                               _dp, _i64, _dp, _i64, _dp, _i64, _ip]),
@@ -369,6 +374,22 @@ class Plan:
         check(self._L.dses_stage_row_info(self._h, int(row), ctypes.byref(lin), ctypes.byref(cnt),
                                           stream), "dses_stage_row_info")
         return lin.value, cnt.value
+
+    # ---- device-resident sharded search (xchg: int64[7] device pointer) ----
+    def shard_vote(self, grid: Grid, r_begin, r_count, xchg_ptr, stream=None):
+        check(self._L.dses_shard_vote(self._h, ctypes.byref(grid), int(r_begin), int(r_count),
+                                      xchg_ptr, stream), "dses_shard_vote")
+
+    def shard_select(self, q, code, param, skip_refine, xchg_ptr, stream=None):
+        check(self._L.dses_shard_select(self._h, float(q), int(code), float(param),
+                                        int(bool(skip_refine)), xchg_ptr, stream),
+              "dses_shard_select")
+
+    def shard_key(self, xchg_ptr, stream=None):
+        check(self._L.dses_shard_key(self._h, xchg_ptr, stream), "dses_shard_key")
+
+    def shard_miss(self, xchg_ptr, stream=None):
+        check(self._L.dses_shard_miss(self._h, xchg_ptr, stream), "dses_shard_miss")
 
     def pose_error(self, grid: Grid, row, lin, code, param, stream=None):
         e = ctypes.c_double()

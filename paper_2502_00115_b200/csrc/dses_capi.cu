@@ -885,7 +885,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   CK(pack.commit(P->arena, st));
   CK(P->stats.ensure(4 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(P->stats.p, 0, 4 * sizeof(unsigned long long), st));
-  CK(P->scal.ensure(64, st));
+  CK(P->scal.ensure(128, st));  // [0..5] search counters, [6] sparse, [8..10] shard locals
   CK(cudaStreamSynchronize(st));  // this thread's upload stream only
 
   // ---- vote kernel parameters
@@ -1810,6 +1810,156 @@ extern "C" int dses_exhaustive(dses_plan* P, const dses_grid* g, int64_t k_trans
   out->launches = P->traffic.launches;
   out->h2d_bytes = P->traffic.h2d;
   out->d2h_bytes = P->traffic.d2h;
+  return DSES_OK;
+}
+
+// ---- device-resident sharded search ----------------------
+// The exchange record x[7] (int64, DEVICE memory of the caller, e.g. a torch
+// tensor reduced with NCCL between the calls):
+//   x[0] M*          (local, then all_reduce MAX)
+//   x[1] error bits  (binary64 bits of the local winner's exact error; the
+//                     order of non-negative doubles is their int64 order; MIN)
+//   x[2] key         (row << 32 | flat bin of the local winner; MIN after
+//                     dses_shard_key masks ranks whose error is not the minimum)
+//   x[3] rotations with a vote, x[4] kept candidates, x[5] the winner's
+//        sat_l0 miss (binary64 bits, only on the winner's rank),
+//   x[6] overflow flag (more near-minimum candidates than the fused tail
+//        re-scores: the caller falls back to the staged protocol)  -- SUM
+// Local values the later steps compare against stay in the plan's scalars.
+namespace {
+__global__ void shard_put_vote(const unsigned long long* sc, long long* x) {
+  x[0] = (long long)sc[0];
+  x[3] = (long long)sc[1];
+}
+__global__ void shard_get_mstar(unsigned long long* sc, const long long* x) { sc[0] = (unsigned long long)x[0]; }
+// sc[8] local error bits, sc[9] local key, sc[10] local miss bits
+__global__ void shard_put_select(unsigned long long* sc, const double* win_err, const int* win_c,
+                                 const int64_t* cand_rows, const int* cand_lins, const double* miss,
+                                 int64_t cap, int skip, long long* x) {
+  const int c = *win_c;
+  long long eb = LLONG_MAX, key = LLONG_MAX, mb = 0;
+  if (c >= 0) {
+    const double e = skip ? 0.0 : *win_err;
+    eb = __double_as_longlong(e);
+    key = (long long)((unsigned long long)cand_rows[c] << 32) | (long long)(unsigned)cand_lins[c];
+    mb = __double_as_longlong(*miss);
+  }
+  sc[8] = (unsigned long long)eb;
+  sc[9] = (unsigned long long)key;
+  sc[10] = (unsigned long long)mb;
+  x[1] = eb;
+  x[2] = key;
+  x[4] = skip ? 0 : (long long)sc[3];
+  x[5] = 0;
+  x[6] = (!skip && (long long)sc[5] > cap) ? 1 : 0;
+}
+__global__ void shard_mask_key(const unsigned long long* sc, long long* x) {
+  if ((long long)sc[8] != x[1]) x[2] = LLONG_MAX;
+}
+__global__ void shard_put_miss(const unsigned long long* sc, long long* x) {
+  x[5] = ((long long)sc[9] == x[2]) ? (long long)sc[10] : 0;
+}
+}  // namespace
+
+extern "C" int dses_shard_vote(dses_plan* P, const dses_grid* g, int64_t r_begin, int64_t r_count,
+                               int64_t* xchg, void* stream) {
+  TrafficScope ts_(P);
+  if (!P || !g || !xchg) return fail(DSES_E_INVALID, "bad arguments");
+  if (P->pend.active) return fail(DSES_E_INVALID, "plan has a search in flight");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t total = (2 * g->k + 1) * (2 * g->k + 1) * (2 * g->k + 1);
+  if (r_begin < 0 || r_count < 0 || r_begin + r_count > total)
+    return fail(DSES_E_INVALID, "rotation range beyond the grid");
+  if (!lattice_fits_int32(P))
+    return fail(DSES_E_LIMIT, "translation window of %.3g bins: the search supports lattices "
+                "below 2^31 bins", (double)P->dims[0] * P->dims[1] * P->dims[2]);
+  int rc = reserve_search(P, std::max<int64_t>(r_count, 1), st);
+  if (rc) return rc;
+  RotSource rs;
+  rc = set_grid(P, g, &rs, st);
+  if (rc) return rc;
+  P->cur_k = g->k;
+  rc = run_vote(P, rs, r_begin, r_count, st);
+  if (rc) return rc;
+  unsigned long long* sc = P->scal.as<unsigned long long>();
+  CK(cudaMemsetAsync(sc, 0, 6 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(sc + 2, 0xff, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(sc + 4, 0x7f, sizeof(unsigned long long), st));
+  if (r_count > 0) CK(launched(launch_select_stats(P->counts.as<int>(), r_count, sc, sc + 1, P->sms, st)));
+  shard_put_vote<<<1, 1, 0, st>>>(sc, reinterpret_cast<long long*>(xchg));
+  CK(launched(cudaGetLastError()));
+  return DSES_OK;
+}
+
+extern "C" int dses_shard_select(dses_plan* P, double q, int code, double param, int skip_refine,
+                                 int64_t* xchg, void* stream) {
+  TrafficScope ts_(P);
+  if (!P || !xchg || code < 0 || code > 4) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  long long* x = reinterpret_cast<long long*>(xchg);
+  const int64_t r_begin = P->cur_r_begin, r_count = P->cur_r_count;
+  const int64_t nr = std::max<int64_t>(r_count, 1);
+  unsigned long long* sc = P->scal.as<unsigned long long>();
+  shard_get_mstar<<<1, 1, 0, st>>>(sc, x);  // the GLOBAL M*
+  CK(launched(cudaGetLastError()));
+  double* inl_vals = P->tvec.as<double>();
+  double* miss = inl_vals + P->n;
+  const int64_t cap = std::min<int64_t>(nr, kFusedRescoreCap);
+  CK(cudaMemsetAsync(P->win_c.p, 0xff, sizeof(int), st));  // no local winner yet
+  if (r_count > 0) {
+    const RotSource& rs = P->cur_rot;
+    if (skip_refine) {
+      CK(cudaMemsetAsync(sc + 2, 0xff, sizeof(unsigned long long), st));
+      CK(launched(launch_argmax(P->counts.as<int>(), r_count, r_begin, 0, sc + 2, P->sms, st, sc)));
+      CK(launched(launch_pick_argmax(sc + 2, P->lins.as<int>(), r_begin, P->cand_rows.as<int64_t>(),
+                                     P->cand_lins.as<int>(), P->win_c.as<int>(), st)));
+    } else {
+      CK(cudaMemsetAsync(sc + 3, 0, sizeof(unsigned long long), st));
+      CK(cudaMemsetAsync(sc + 4, 0x7f, sizeof(unsigned long long), st));
+      CK(cudaMemsetAsync(sc + 5, 0, sizeof(unsigned long long), st));
+      CK(launched(launch_compact(P->counts.as<int>(), P->lins.as<int>(), r_count, r_begin, 0.0,
+                                 P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), sc + 3, P->sms,
+                                 st, sc, q)));
+      const ScoreParams s = score_params(P, rs, code, param);
+      CK(launched(launch_screen(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), nr,
+                                P->partial.as<double>(), P->err32.as<double>(), sc + 4, st, sc + 3), 2));
+      CK(launched(launch_rescore_compact(P->err32.as<double>(), nr, 0.0, P->sel.as<int>(), sc + 5, st,
+                                         sc + 3, sc + 4, screen_tolerance(P, code))));
+      CK(launched(launch_exact(s, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->sel.as<int>(),
+                               cap, P->vals.as<double>(), P->err64.as<double>(), st, sc + 5), 2));
+      CK(launched(launch_winner(P->err64.as<double>(), P->sel.as<int>(), P->cand_rows.as<int64_t>(),
+                                cap, P->win_err.as<double>(), P->win_row.as<int64_t>(),
+                                P->win_c.as<int>(), st, nullptr, sc + 5)));
+    }
+    // the local winner's inlier count: exact sat_l0 at the bin size (metrics.py:143-150)
+    const ScoreParams si = score_params(P, rs, kSatL0, P->bin);
+    CK(launched(launch_exact(si, P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), P->win_c.as<int>(),
+                             1, inl_vals, miss, st), 2));
+  }
+  shard_put_select<<<1, 1, 0, st>>>(sc, P->win_err.as<double>(), P->win_c.as<int>(),
+                                    P->cand_rows.as<int64_t>(), P->cand_lins.as<int>(), miss, cap,
+                                    skip_refine, x);
+  CK(launched(cudaGetLastError()));
+  return DSES_OK;
+}
+
+extern "C" int dses_shard_key(dses_plan* P, int64_t* xchg, void* stream) {
+  if (!P || !xchg) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  shard_mask_key<<<1, 1, 0, (cudaStream_t)stream>>>(P->scal.as<unsigned long long>(),
+                                                    reinterpret_cast<long long*>(xchg));
+  CK(cudaGetLastError());
+  return DSES_OK;
+}
+
+extern "C" int dses_shard_miss(dses_plan* P, int64_t* xchg, void* stream) {
+  if (!P || !xchg) return fail(DSES_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(P->device));
+  shard_put_miss<<<1, 1, 0, (cudaStream_t)stream>>>(P->scal.as<unsigned long long>(),
+                                                    reinterpret_cast<long long*>(xchg));
+  CK(cudaGetLastError());
   return DSES_OK;
 }
 

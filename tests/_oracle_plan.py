@@ -65,3 +65,38 @@ class OraclePlan:
     def pose_error(self, grid, row, lin, code, param):
         return float(O.refine_batch(self._rots([row]), self._ts([lin]), self.x, self.y, code,
                                     param)[0])
+
+    # ---- the device-resident sharded protocol's stages (dses_shard_*), on a
+    #      CPU int64[7] torch tensor instead of device memory ---------------
+    def shard_vote(self, grid, r_begin, r_count, x, stream=None):
+        mstar, valid = self.stage_vote(grid, r_begin, r_count)
+        x[0], x[3] = mstar, valid
+
+    def shard_select(self, q, code, param, skip, x, stream=None):
+        mstar = int(x[0])
+        eb = key = INT64_MAX
+        miss = 0.0
+        kept = 0
+        if skip:
+            row = self.stage_argmax(mstar)
+            if row != INT64_MAX:
+                eb = 0
+        else:
+            kept, mn, tol = self.stage_screen(q, mstar, code, param)
+            _, row, _ = self.stage_rescore(mn + tol, code, param)
+            if kept > 0 and row != INT64_MAX:
+                e = self.stage_rescore(mn + tol, code, param)[0]
+                eb = int(np.float64(e).view(np.int64))
+        if eb != INT64_MAX:
+            lin = int(self.lins[row - self.r0])
+            key = (row << 32) | lin
+            miss = self.pose_error(grid=None, row=row, lin=lin, code=3, param=self.bin)
+        self._eb, self._key, self._miss = eb, key, int(np.float64(miss).view(np.int64))
+        x[1], x[2], x[4], x[5], x[6] = eb, key, kept, 0, 0
+
+    def shard_key(self, x, stream=None):
+        if self._eb != int(x[1]):
+            x[2] = INT64_MAX
+
+    def shard_miss(self, x, stream=None):
+        x[5] = self._miss if self._key == int(x[2]) else 0
