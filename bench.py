@@ -12,14 +12,17 @@ Inputs (--inputs benchgen, the default): the reference generator's own clouds
 for seeds 0..15 (SURVEY.md 8(d)), committed as bench_data/benchgen_<cfg>.npz;
 --inputs synth uses the independent generator paper_2502_00115_b200/synth.py.
 
-Under torchrun every rank registers its own pairs (replicas, weak scaling, no
-data-path collective); the timed region is bracketed by a
-barrier + synchronize, timed with CUDA events on the launching stream, and the
-max over ranks is reported.  Rank 0 prints ONE JSON line.  Its
-"rotation_sharded" object is the other multi-GPU mode: one c3 registration
-(753,571 rotations) with the rotation grid split over ALL ranks
-(distributed.dses_sharded, two NCCL all_gathers per registration), strong
-scaling (skip with --no-sharded).
+`--gpus N` launches N ranks itself (torch.distributed.run, one process per
+GPU) when not already under torchrun, and checks WORLD_SIZE == N.  Every rank
+registers its own pairs (replicas, weak scaling, no data-path collective;
+SURVEY.md 8(e)); the timed region is bracketed by a barrier + synchronize,
+timed with CUDA events on the launching stream, and the max over ranks is
+reported.  Rank 0 prints ONE JSON line.  Its "rotation_sharded" list is the
+other multi-GPU mode, measured first-class (value, ms_per_step, steps per
+entry): one registration's rotation grid split over ALL ranks
+(distributed.ShardedSearch: M* and the min-loc winner reduced in device
+memory by NCCL all_reduces), strong scaling, for c3 (753,571 rotations) and the
+c5 sweep points >= 10^6 rotations (skip with --no-sharded).
 
 `--impl reference` times the reference's own CPU implementation on the box's
 host cores, on rank 0 only: the unmodified `gridreg` package (pure Python +
@@ -332,7 +335,8 @@ def run_reference(args):
         "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": bench_pairs(args.config, 1, 0, args.inputs)[1],
         "config": {"workload": describe(args.config, c, cfg, x.shape[0], y.shape[0]),
-                   "metric": cfg.metric.kind, "l2_flush": "n/a (CPU)"},
+                   "metric": cfg.metric.kind, "rotations": cfg.rotation_count},
+        "l2_flush": "n/a (CPU)",
         "registrations_per_sec": value / total,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
                          "sample": f"each step: phase 1 over {sample} consecutive rotations of "
@@ -377,7 +381,8 @@ def run_reference_package(args, ref, c, cfg, x, y):
         "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": bench_pairs(args.config, 1, 0, args.inputs)[1],
         "config": {"workload": describe(args.config, c, cfg, x.shape[0], y.shape[0]),
-                   "metric": cfg.metric.kind, "l2_flush": "n/a (CPU)"},
+                   "metric": cfg.metric.kind, "rotations": cfg.rotation_count},
+        "l2_flush": "n/a (CPU)",
         "registrations_per_sec": value / total,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": what + " (unmodified gridreg 0.1.0 from baseline/_ref, "
@@ -387,62 +392,103 @@ def run_reference_package(args, ref, c, cfg, x, y):
     print(json.dumps(line), flush=True)
 
 
-def sharded_registration(args, rank, world, local, steps=3):
-    """One c3 registration (753,571 rotations, L1, noisy + 20% outliers: the
-    north star's "fine rotation grid sharded across the GPUs") split over ALL
-    ranks by distributed.dses_sharded -- every rank votes a contiguous slice
-    of the rotation grid, two all_gathers (NCCL) pick M* and the min-loc
-    winner.  Strong scaling: the work per step is fixed.  Device time (CUDA
-    events around the whole call, max over ranks), after one warm-up."""
+SHARDED = (  # (name, workload, pair config, k_rot override, steps): SURVEY.md 8(d) c3 and c5 >= 10^6
+    ("c3", "c3", "c3", None, 3),
+    ("c5_K50", "c2", "c2", 50, 3),
+    ("c5_K108", "c2", "c2", 108, 2),
+)
+
+
+def sharded_measurements(args, rank, world, local):
+    """The rotation-grid-sharded mode, first-class: one registration's grid
+    split over ALL ranks (distributed.ShardedSearch: every rank votes a
+    contiguous slice; M* and the min-loc (error, rotation) key are reduced
+    in device memory by four NCCL all_reduces; one host read per
+    registration).  Strong scaling -- the work per step is fixed: c3 (753,571
+    rotations, noisy + 20% outliers, L1) and the c5 sweep points >= 10^6
+    rotations (K = 50: 1,030,301; K = 108: 10,218,313) on the c2 pair.  Plans
+    are built before timing; one warm-up registration; CUDA events around the
+    timed registrations (each ends with its host read), max over ranks."""
     import torch
     import torch.distributed as dist
-    from paper_2502_00115_b200.distributed import dses_sharded
-    try:
-        c = workload("c3")
-        cfg = search_config(c)
-        (x, y, _), = bench_pairs("c3", 1, 0, args.inputs)[0]
-        dses_sharded(x, y, cfg, device=local)  # warm
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record()
-        for _ in range(steps):
-            res = dses_sharded(x, y, cfg, device=local)
-        t1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda")
-        w = torch.tensor(list(res.best.grid_coords), dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            lo, hi = w.clone(), w.clone()
-            dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-            dist.all_reduce(hi, op=dist.ReduceOp.MAX)
-            same = bool(torch.equal(lo, hi))
-        else:
+    from dataclasses import replace
+    from paper_2502_00115_b200.distributed import ShardedSearch
+    out = []
+    for name, wl, pair_cfg, K, steps in SHARDED:
+        try:
+            cfg = search_config(workload(wl))
+            if K is not None:
+                cfg = replace(cfg, k_rot=K, rot_step=math.radians(45.0 / K))
+            (x, y, _), = bench_pairs(pair_cfg, 1, 0, args.inputs)[0]
+            with ShardedSearch(x, y, cfg, device=local) as s:
+                s.run()  # warm
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record()
+                for _ in range(steps):
+                    res = s.run()
+                t1.record()
+                torch.cuda.synchronize()
+            t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda")
+            w = torch.tensor(list(res.best.grid_coords), dtype=torch.float64, device="cuda")
             same = True
-        ms = float(t.item()) / steps
-        R = cfg.rotation_count
-        return {"value": R / (ms * 1e-3), "unit": UNIT, "scaling": "strong", "n_gpus": world,
-                "ms_per_registration": ms, "steps": steps, "rotations": R,
-                "config": "c3: 717-pt noisy partial (+20% outliers) vs 1024-pt cloud, k_rot=45 @ 1 deg, "
-                          "k_trans=20 @ 25 mm, metric l1, pair 0 of --inputs",
-                "collectives": "2 all_gathers per registration (global M*; min (error, row))",
+            if world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                lo, hi = w.clone(), w.clone()
+                dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+                dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+                same = bool(torch.equal(lo, hi))
+            ms = float(t.item()) / steps
+            R = cfg.rotation_count
+            out.append({
+                "name": name, "metric": METRIC, "value": R / (ms * 1e-3), "unit": UNIT,
+                "ms_per_step": ms, "steps": steps, "n_gpus": world, "scaling": "strong",
+                "registrations_per_sec": 1e3 / ms, "rotations": R,
+                "config": {"workload": describe(name, workload(wl), cfg, x.shape[0], y.shape[0]),
+                           "metric": cfg.metric.kind, "rotations": R},
+                "parallelism": f"rotation grid split over {world} rank(s)",
+                "collectives": "per registration: all_reduce MAX (M*), MIN (error bits), "
+                               "MIN (row<<32|bin), SUM (valid, kept, miss, overflow) on a "
+                               "device-resident int64[7] record",
                 "winner_grid": list(res.best.grid_coords), "winner_identical_on_all_ranks": same,
-                "candidates_refined": int(res.candidates_refined)}
-    except Exception as exc:  # reported, never fatal for the headline line
-        return {"error": f"{type(exc).__name__}: {exc}"}
+                "candidates_refined": int(res.candidates_refined),
+                "protocol": res.elapsed.get("protocol")})
+        except Exception as exc:  # reported, never fatal for the headline line
+            out.append({"name": name, "error": f"{type(exc).__name__}: {exc}"})
+    return out
+
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args):
+    """`--gpus N` without a torchrun environment: re-launch this command under
+    torch.distributed.run with N local ranks (one process per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execvp(sys.executable, cmd)
 
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args)  # does not return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         run_reference(args)
         return
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # BENCH_SHARE_DEVICE=1: code-path check of the N-rank protocol on a 1-GPU
@@ -562,7 +608,7 @@ def main():
     assert all(tuple(a.best.grid_coords) == tuple(b.best.grid_coords) for a, b in
                zip(bres, [dses(p[0], p[1], cfg, device=local) for p in e2e_pairs[:2]]))
 
-    sharded = None if args.no_sharded else sharded_registration(args, rank, world, local)
+    sharded = None if args.no_sharded else sharded_measurements(args, rank, world, local)
 
     if rank == 0:
         ffma_s, _ = _native.probe_fp32_peak(local)
@@ -585,9 +631,9 @@ def main():
             "dtype": "i32 fixed-point vote / f32 screen / f64 exact",
             "data": data_desc,
             "config": {"workload": describe(args.config, c, cfg, n_src, preps[0].y.shape[0]),
-                       "metric": cfg.metric.kind, "rotations": R,
-                       "parallelism": f"replicas x{world} (registrations sharded, no collective)",
-                       "l2_flush": "512 MiB buffer zeroed between timed steps"},
+                       "metric": cfg.metric.kind, "rotations": R},
+            "parallelism": f"replicas x{world} (registrations sharded over ranks, no collective)",
+            "l2_flush": "512 MiB buffer zeroed between timed steps",
             "registrations_per_sec": args.steps * world / (ms_max * 1e-3),
             "e2e": {"value": b_value, "unit": UNIT,
                     "registrations_per_sec": args.steps * world / (float(tb.item()) * 1e-3),
