@@ -161,6 +161,8 @@ struct Lane {          // per-warp deferred list state (warp-uniform)
 __shared__ const double* g_exR;
 __shared__ const int4* g_exP;
 __shared__ unsigned* g_exH;
+__shared__ unsigned g_dummy[32];   // per-lane sink of non-voting unconditional atomics
+#define g_dummy_sh ((uint32_t)__cvta_generic_to_shared(g_dummy))
 
 // Append the lanes in `dm` (pairs (i, j)) to the warp's exact-path list.
 template <bool HSMEM, bool PSMEM>
@@ -254,7 +256,14 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
         ok &= __shfl_sync(0xffffffffu, key, l0 & 31) != key;
         if (GP > 1) ok &= __shfl_sync(0xffffffffu, key, l1 & 31) != key;
       }
-      vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins);
+      if (HSMEM) {
+        // unconditional: a lane that does not vote adds to its own dummy word
+        // (conflict-free), so no branch / reconvergence around the atomic
+        const unsigned lin = b[s].lin;
+        const uint32_t a = ok ? hist_sh + ((lin + lin) & ~3u) : g_dummy_sh + 4u * (unsigned)lane;
+        reds_add(a, __funnelshift_l(0u, 1u, lin << 4));
+      } else
+        vote_if<HSMEM>(hist, hist_sh, b[s].lin, ok, (unsigned)p.nbins);
     }
     return;
   }
@@ -514,7 +523,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
                                (yt.hi[2] - Pl.z >= 0) & (yt.lo[2] - Pl.z < (int)p.W2));
         }
         unsigned sm = __ballot_sync(0xffffffffu, sok);
-        if (lane == 0) s_pairs[warp] += (unsigned long long)__popc(sm) * (unsigned)yt.count;
+        if (lane == 0) {  // evaluated-pair statistic: one 64-bit shared reduction
+          const unsigned long long np = (unsigned long long)__popc(sm) * (unsigned)yt.count;
+          asm volatile("red.shared.add.u64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(s_pairs + warp)),
+                       "l"(np) : "memory");
+        }
         const int nsrc = __popc(sm);
         // opaque copy: keeps the stage base in a register (otherwise it is
         // re-derived from kernel parameters in every slot)
