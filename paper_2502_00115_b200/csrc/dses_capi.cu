@@ -268,6 +268,7 @@ struct dses_plan {
   int vote_grid = 0, vote_threads = kVoteThreads;
   // device data
   DevBuf xs, ys, yq, near_off, near_idx, xt, yt;  // vote (tile order)
+  DevBuf risk;                                         // vote: guard-band risk bitmaps per group
   DevBuf x0, ys0, ys1, ys2, ysf;                      // scoring (original x, y sorted by axis 0)
   DevBuf gcell, gpts;                                  // scoring: uniform grid over y
   DevBuf arena;                                        // the inputs above live here (UploadPack)
@@ -841,6 +842,44 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       }
     }
   }
+  // ---- guard-band risk bitmaps: per group and axis, which fraction buckets of
+  // a source's rotated coordinate can put some point of the group within the
+  // guard band of a bin edge.  A pair is "near" iff frac(Yq - Pq) < 2G, i.e.
+  // Pq mod 2^F lies in {a, a-1, .., a-2G+1} for a = Yq mod 2^F; the buckets
+  // (2^kRiskBits per axis) of those values are marked.  A source whose three
+  // buckets are unmarked is "safe" for the group: none of its pairs with the
+  // group can be near, and the vote kernel skips the guard-band test for it.
+  // Groups with far points (every candidate exact) are never safe (flag in
+  // YTile.pad[0]).
+  // (only for small reference clouds: the bitmaps, 384 B per group, are read
+  // per (group, unit) and must stay L1-resident; with many groups and few
+  // survivors per unit -- c4 -- the lookups cost more than they save)
+  const bool risk_on = F >= kRiskBits + 2 && yt.size() <= 128;
+  std::vector<unsigned> risk;
+  if (risk_on) {
+    const int sh = F - kRiskBits;
+    const unsigned fm = (unsigned)((1u << F) - 1u);
+    risk.assign(yt.size() * kRiskWords, 0u);
+    for (size_t t = 0; t < yt.size(); ++t) {
+      YTile& T = yt[t];
+      T.pad[0] = 0;
+      unsigned* bm = risk.data() + t * kRiskWords;
+      for (int q = T.start; q < T.start + T.count; ++q) {
+        if (yq[q].w & kFarFlag) T.pad[0] = 1;
+        const int v[3] = {yq[q].x, yq[q].y, yq[q].z};
+        for (int k = 0; k < 3; ++k) {
+          const unsigned a = (unsigned)v[k] & fm;
+          for (unsigned d : {0u, 2u * kGuard - 1u}) {  // the window [a - 2G + 1, a] spans <= 2 buckets
+            const unsigned b = ((a - d) & fm) >> sh;
+            bm[k * (kRiskWords / 3) + (b >> 5)] |= 1u << (b & 31);
+          }
+        }
+      }
+    }
+  } else {
+    risk.assign(kRiskWords, 0u);
+    for (YTile& T : yt) T.pad[0] = 1;  // exact mode / few fraction bits: no source is safe
+  }
   if (yt.size() >= 65536 || xt.size() >= 65536)  // (group << 16 | unit) work-unit encoding
     return fail(DSES_E_LIMIT, "cloud too large for the vote kernel: at most 65535 groups / units "
                 "of 32 points (about 2 million points) per cloud");
@@ -875,6 +914,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   pack.add(P->near_idx, nidx);
   pack.add(P->xt, xt);
   pack.add(P->yt, yt);
+  pack.add(P->risk, risk);
   pack.add(P->x0, xv);
   pack.add(P->ys0, c0);
   pack.add(P->ys1, c1);
@@ -910,6 +950,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.xs = P->xs.as<double>(); v.ys = P->ys.as<double>(); v.yq = P->yq.as<int4>();
   v.near_off = P->near_off.as<int>(); v.near_idx = P->near_idx.as<int>();
   v.xt = P->xt.as<XTile>(); v.yt = P->yt.as<YTile>();
+  v.risk = P->risk.as<unsigned>();
+  v.risk_shift = risk_on ? F - kRiskBits : 0;
   v.gthr = F ? 2u * kGuard : 0xffffffffu;
   v.stats = P->stats.as<unsigned long long>();
   v.count16 = n < 65536 ? 1 : 0;
@@ -1149,7 +1191,7 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
 extern "C" int dses_plan_destroy(dses_plan* P) {
   if (!P) return DSES_OK;
   cudaSetDevice(P->device);
-  DevBuf* bufs[] = {&P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->yt,
+  DevBuf* bufs[] = {&P->risk, &P->xs, &P->ys, &P->yq, &P->near_off, &P->near_idx, &P->xt, &P->yt,
                     &P->x0, &P->ys0, &P->ys1, &P->ys2, &P->ysf, &P->gcell, &P->gpts, &P->arena, &P->yorig, &P->lins64, &P->sparse_scratch, &P->cth, &P->sth, &P->rots,
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,

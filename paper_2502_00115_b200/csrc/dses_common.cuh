@@ -38,6 +38,8 @@ constexpr int kDenseMaxBins = 1 << 26;  // beyond: sort-based (sparse) mode quer
 constexpr int kNoRef = -3 * (1 << 29);
 constexpr int kMaxComp = 16;     // dedup components up to this size stay in one warp
 constexpr int kFarFlag = 1 << 12; // Yq.w: the point's dedup needs the exact path
+constexpr int kRiskBits = 10;     // fraction buckets per axis of the guard-band risk bitmaps
+constexpr int kRiskWords = 3 * (1 << kRiskBits) / 32;  // words per group (3 axes)
 constexpr int kVoteThreads = 1024;
 
 enum Metric { kL2 = 0, kL1 = 1, kTruncL1 = 2, kSatL0 = 3, kTruncL2 = 4 };
@@ -56,7 +58,7 @@ struct __align__(16) YTile {  // spatial tile of the (sorted) reference cloud; 3
   int count;
   int gm;               // max earlier dedup partners (lanes) of a point in the group: 0, 1, 2
   int npts;             // real reference points in the group
-  int pad[2];
+  int pad[2];           // pad[0]: the group has far points (no source is guard-band safe)
 };
 static_assert(sizeof(YTile) == 48, "YTile is loaded as three int4");
 
@@ -67,7 +69,7 @@ __device__ __forceinline__ YTile load_ytile(const YTile* yt, int b) {
   YTile t;
   t.lo[0] = a.x; t.lo[1] = a.y; t.lo[2] = a.z; t.start = a.w;
   t.hi[0] = h.x; t.hi[1] = h.y; t.hi[2] = h.z; t.count = h.w;
-  t.gm = m.x; t.npts = m.y; t.pad[0] = t.pad[1] = 0;
+  t.gm = m.x; t.npts = m.y; t.pad[0] = m.z; t.pad[1] = 0;
   return t;
 }
 
@@ -102,6 +104,8 @@ struct VoteParams {
   const XTile* xt;       // source units of <= kTile points
   const YTile* yt;       // reference groups of <= kTile points
   unsigned gthr;         // a pair whose min fraction over the axes is < gthr is re-binned exactly
+  const unsigned* risk;  // per group kRiskWords: guard-band risk bitmaps (dses_capi.cu)
+  int risk_shift;        // F - kRiskBits (bucket of a fraction); 0 with every group unsafe
   RotSource rot;
   int64_t r_begin, r_count;
   // outputs (indexed r - r_begin)

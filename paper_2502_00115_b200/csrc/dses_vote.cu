@@ -205,6 +205,18 @@ __device__ __forceinline__ PairBin fixed_bin(const FastK& k, const int4& Y, cons
   return r;
 }
 
+// The same for a guard-band-safe (source, group) pair (risk bitmaps,
+// dses_capi.cu): no fraction can be near a bin edge, so the near test is
+// skipped; every candidate is decided.
+__device__ __forceinline__ PairBin fixed_bin_safe(const FastK& k, const int4& Y, const int4& Pi) {
+  PairBin r;
+  const unsigned u0 = (unsigned)(Y.x - Pi.x), u1 = (unsigned)(Y.y - Pi.y), u2 = (unsigned)(Y.z - Pi.z);
+  r.cand = (u0 < k.W0) & (u1 < k.W1) & (u2 < k.W2);
+  r.near = false;
+  r.lin = ((u0 >> k.F) * k.d1 + (u1 >> k.F)) * k.d2 + (u2 >> k.F);
+  return r;
+}
+
 template <bool HSMEM>
 __device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsigned lin, bool ok,
                                         unsigned nbins = 0xffffffffu) {
@@ -223,7 +235,7 @@ __device__ __forceinline__ void vote_if(unsigned* hist, uint32_t hist_sh, unsign
 // each source once).  Pairs in the guard band, pairs whose partner is in the
 // guard band, and "far" points take the exact path.  GP = number of partner
 // shuffles the group needs (0, 1, 2).
-template <bool HSMEM, bool PSMEM, int GP, int NS>
+template <bool HSMEM, bool PSMEM, int GP, int NS, bool SAFE>
 __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, const double* R,
                                           const int4* P, unsigned* hist, uint32_t hist_sh, Lane& L,
                                           const int4& Y, int l0, int l1, uint32_t src_sh, int j,
@@ -238,14 +250,14 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
     // the unit's surviving sources, staged (Pq, i) per warp: uniform address
     const int4 Pi = lds_v4(src_sh + 16u * (unsigned)s);
     is[s] = Pi.w;
-    b[s] = fixed_bin(fk, Y, Pi);
+    b[s] = SAFE ? fixed_bin_safe(fk, Y, Pi) : fixed_bin(fk, Y, Pi);
     any |= b[s].cand;
   }
   if (!__any_sync(0xffffffffu, any)) return;
   bool anynear = false;
 #pragma unroll
   for (int s = 0; s < NS; ++s) anynear |= b[s].near;
-  if (!__any_sync(0xffffffffu, anynear)) {
+  if (SAFE || !__any_sync(0xffffffffu, anynear)) {
     // common case: no candidate of the slot is near a bin edge, so every
     // candidate is decided and a partner's key is its exact bin or -1
 #pragma unroll
@@ -300,7 +312,8 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
   }
 }
 
-template <bool HSMEM, bool PSMEM>
+// RISK: guard-band risk bitmaps in use (small reference clouds; dses_capi.cu)
+template <bool HSMEM, bool PSMEM, bool RISK>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -522,33 +535,56 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
                                (yt.hi[1] - Pl.y >= 0) & (yt.lo[1] - Pl.y < (int)p.W1) &
                                (yt.hi[2] - Pl.z >= 0) & (yt.lo[2] - Pl.z < (int)p.W2));
         }
-        unsigned sm = __ballot_sync(0xffffffffu, sok);
+        // guard-band risk (dses_capi.cu): the source's fraction bucket on each
+        // axis against the group's bitmaps; safe sources skip the near test
+        bool safe = false;
+        if (RISK && sok && !yt.pad[0]) {
+          const unsigned* bm = p.risk + (size_t)(unit >> 16) * kRiskWords;
+          const int sh = p.risk_shift;
+          const unsigned w0 = __ldg(bm + (((unsigned)Pl.x >> (sh + 5)) & 31u));
+          const unsigned w1 = __ldg(bm + 32 + (((unsigned)Pl.y >> (sh + 5)) & 31u));
+          const unsigned w2 = __ldg(bm + 64 + (((unsigned)Pl.z >> (sh + 5)) & 31u));
+          safe = (((w0 >> (((unsigned)Pl.x >> sh) & 31u)) | (w1 >> (((unsigned)Pl.y >> sh) & 31u)) |
+                   (w2 >> (((unsigned)Pl.z >> sh) & 31u))) & 1u) == 0u;
+        }
+        const unsigned msafe = RISK ? __ballot_sync(0xffffffffu, safe) : 0u;
+        const unsigned sm = __ballot_sync(0xffffffffu, sok);
+        const unsigned mrisk = sm & ~msafe;
+        const int nsafe = RISK ? __popc(msafe) : 0;
         if (lane == 0) {  // evaluated-pair statistic: one 64-bit shared reduction
           const unsigned long long np = (unsigned long long)__popc(sm) * (unsigned)yt.count;
           asm volatile("red.shared.add.u64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(s_pairs + warp)),
                        "l"(np) : "memory");
         }
         const int nsrc = __popc(sm);
+        (void)nsafe;
         // opaque copy: keeps the stage base in a register (otherwise it is
         // re-derived from kernel parameters in every slot)
         uint32_t sbase;
         asm volatile("mov.u32 %0, %1;" : "=r"(sbase) : "r"(stage_sh));
         __syncwarp();  // the previous unit's slots have read the stage
-        if (sok) sts_v4(sbase + 16u * (unsigned)__popc(sm & lanemask_lt),
+        // safe sources first, then the rest
+        if (sok) sts_v4(sbase + 16u * (unsigned)(!RISK ? __popc(sm & lanemask_lt)
+                                                 : safe ? __popc(msafe & lanemask_lt)
+                                                        : nsafe + __popc(mrisk & lanemask_lt)),
                         make_int4(Pl.x, Pl.y, Pl.z, ustart + lane));
         __syncwarp();
 #define DSES_SLOTS(GP)                                                                         \
   int t = 0;                                                                                   \
+  if (RISK)                                                                                    \
+    for (; t + 3 < nsafe; t += 4)                                                              \
+      vote_slot<HSMEM, PSMEM, GP, 4, true>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,            \
+                                         sbase + 16u * (unsigned)t, j, lane, lanemask_lt);      \
   for (; t + 3 < nsrc; t += 4)                                                                 \
-    vote_slot<HSMEM, PSMEM, GP, 4>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,                  \
-                                   sbase + 16u * (unsigned)t, j, lane, lanemask_lt);            \
+    vote_slot<HSMEM, PSMEM, GP, 4, false>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,           \
+                                          sbase + 16u * (unsigned)t, j, lane, lanemask_lt);     \
   for (; t < nsrc; t += 2) {                                                                   \
     if (t + 1 < nsrc)                                                                          \
-      vote_slot<HSMEM, PSMEM, GP, 2>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,                \
-                                     sbase + 16u * (unsigned)t, j, lane, lanemask_lt);          \
+      vote_slot<HSMEM, PSMEM, GP, 2, false>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,         \
+                                            sbase + 16u * (unsigned)t, j, lane, lanemask_lt);   \
     else                                                                                       \
-      vote_slot<HSMEM, PSMEM, GP, 1>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,                \
-                                     sbase + 16u * (unsigned)t, j, lane, lanemask_lt);          \
+      vote_slot<HSMEM, PSMEM, GP, 1, false>(p, fkl, R, P, hist, hist_sh, L, Y, l0, l1,         \
+                                            sbase + 16u * (unsigned)t, j, lane, lanemask_lt);   \
   }
         if (gp == 0) { DSES_SLOTS(0) }
         else if (gp == 1) { DSES_SLOTS(1) }
@@ -669,7 +705,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
 // lowered: plan construction on one thread and launches on another must not
 // race on this process-wide attribute (a lowered limit between another
 // thread's set and launch would fail that launch).
-template <bool H, bool PS>
+template <bool H, bool PS, bool RK>
 static cudaError_t raise_smem_limit() {
   static std::once_flag once[64];
   static cudaError_t err[64];
@@ -681,9 +717,9 @@ static cudaError_t raise_smem_limit() {
     int optin = 0;
     cudaFuncAttributes a{};
     err[dev] = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (err[dev] == cudaSuccess) err[dev] = cudaFuncGetAttributes(&a, vote_kernel<H, PS>);
+    if (err[dev] == cudaSuccess) err[dev] = cudaFuncGetAttributes(&a, vote_kernel<H, PS, RK>);
     if (err[dev] == cudaSuccess)
-      err[dev] = cudaFuncSetAttribute(vote_kernel<H, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      err[dev] = cudaFuncSetAttribute(vote_kernel<H, PS, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       optin - (int)a.sharedSizeBytes);
   });
   return err[dev];
@@ -692,15 +728,16 @@ static cudaError_t raise_smem_limit() {
 cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, int threads,
                         cudaStream_t stream) {
   const size_t smem = vote_smem_bytes(p, hsmem, psmem, threads);
+  const bool risk = p.risk_shift != 0;
   cudaError_t e;
-#define DSES_LAUNCH(H, PS)                          \
-  e = raise_smem_limit<H, PS>();                    \
+#define DSES_LAUNCH(H, PS, RK)                      \
+  e = raise_smem_limit<H, PS, RK>();                \
   if (e != cudaSuccess) return e;                   \
-  vote_kernel<H, PS><<<grid, threads, smem, stream>>>(p);
-  if (hsmem && psmem) { DSES_LAUNCH(true, true) }
-  else if (hsmem) { DSES_LAUNCH(true, false) }
-  else if (psmem) { DSES_LAUNCH(false, true) }
-  else { DSES_LAUNCH(false, false) }
+  vote_kernel<H, PS, RK><<<grid, threads, smem, stream>>>(p);
+  if (hsmem && psmem) { if (risk) { DSES_LAUNCH(true, true, true) } else { DSES_LAUNCH(true, true, false) } }
+  else if (hsmem) { DSES_LAUNCH(true, false, false) }
+  else if (psmem) { DSES_LAUNCH(false, true, false) }
+  else { DSES_LAUNCH(false, false, false) }
 #undef DSES_LAUNCH
   return cudaGetLastError();
 }
@@ -710,25 +747,27 @@ cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, i
 size_t vote_static_smem() {
   cudaFuncAttributes a{};
   size_t m = 0;
-  if (cudaFuncGetAttributes(&a, vote_kernel<true, true>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
-  if (cudaFuncGetAttributes(&a, vote_kernel<true, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
-  if (cudaFuncGetAttributes(&a, vote_kernel<false, true>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
-  if (cudaFuncGetAttributes(&a, vote_kernel<false, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<true, true, true>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<true, true, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<true, false, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<false, true, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<false, false, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
   return m;
 }
 
 int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int threads) {
   const size_t smem = vote_smem_bytes(p, hsmem, psmem, threads);
+  const bool risk = p.risk_shift != 0;
   int n = 0;
   cudaError_t e;
-#define DSES_OCC(H, PS)                                                                    \
-  e = raise_smem_limit<H, PS>();                                                           \
+#define DSES_OCC(H, PS, RK)                                                                \
+  e = raise_smem_limit<H, PS, RK>();                                                       \
   if (e == cudaSuccess)                                                                    \
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<H, PS>, threads, smem);
-  if (hsmem && psmem) { DSES_OCC(true, true) }
-  else if (hsmem) { DSES_OCC(true, false) }
-  else if (psmem) { DSES_OCC(false, true) }
-  else { DSES_OCC(false, false) }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, vote_kernel<H, PS, RK>, threads, smem);
+  if (hsmem && psmem) { if (risk) { DSES_OCC(true, true, true) } else { DSES_OCC(true, true, false) } }
+  else if (hsmem) { DSES_OCC(true, false, false) }
+  else if (psmem) { DSES_OCC(false, true, false) }
+  else { DSES_OCC(false, false, false) }
 #undef DSES_OCC
   return e == cudaSuccess ? n : 0;
 }
