@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   // fast-path constants through shared memory: loaded into regular registers
   // once, instead of being re-loaded into uniform registers in the hot loop
   __shared__ __align__(16) unsigned kc[12];
-  __shared__ unsigned long long s_pairs[kVoteThreads / 32];  // per-warp evaluated-pair counts
+  __shared__ unsigned s_pairs[kVoteThreads / 32];  // per-warp evaluated pairs of this rotation
   if (tid == 0) {
     kc[0] = p.W0; kc[1] = p.W1; kc[2] = p.W2; kc[3] = p.fmask; kc[4] = p.gthr;
     kc[5] = (unsigned)p.d1; kc[6] = (unsigned)p.d2; kc[7] = (unsigned)p.F;
@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   __syncthreads();
   const uint32_t hist_sh = kc[8];
   if (lane == 0) s_pairs[warp] = 0;
+  unsigned long long st_pairs = 0;
   Lane L;
   // opaque copy: a register, not re-derived from kernel parameters per slot
   asm volatile("mov.u32 %0, %1;" : "=r"(L.rare_sh) : "r"((uint32_t)__cvta_generic_to_shared(rare)));
@@ -551,11 +552,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         const unsigned sm = __ballot_sync(0xffffffffu, sok);
         const unsigned mrisk = sm & ~msafe;
         const int nsafe = RISK ? __popc(msafe) : 0;
-        if (lane == 0) {  // evaluated-pair statistic: one 64-bit shared reduction
-          const unsigned long long np = (unsigned long long)__popc(sm) * (unsigned)yt.count;
-          asm volatile("red.shared.add.u64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(s_pairs + warp)),
-                       "l"(np) : "memory");
-        }
+        // evaluated-pair statistic: a 32-bit per-warp counter (a 64-bit shared
+        // add would be a CAS loop), folded into 64 bits once per rotation
+        if (lane == 0)
+          reds_add((uint32_t)__cvta_generic_to_shared(s_pairs) + 4u * (unsigned)warp,
+                   (unsigned)__popc(sm) * (unsigned)yt.count);
         const int nsrc = __popc(sm);
         (void)nsafe;
         // opaque copy: keeps the stage base in a register (otherwise it is
@@ -597,6 +598,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
       L.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L.rare_sh, L.nrare, lane) & 0xffffu;
       L.nrare = 0;
     }
+    if (lane == 0) { st_pairs += s_pairs[warp]; s_pairs[warp] = 0; }
     __syncthreads();
 
     // ---- mode, pass 1: block maximum M of the histogram (packed 16-bit max
@@ -676,7 +678,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   }
 
   // kernel statistics
-  unsigned long long st_rechecks = L.rechecks, st_pairs = lane == 0 ? s_pairs[warp] : 0ull;
+  unsigned long long st_rechecks = L.rechecks;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     st_pairs += __shfl_xor_sync(0xffffffffu, st_pairs, o);
