@@ -664,6 +664,12 @@ def main():
                                             f"bytes of one ncu --set full capture ({ncu_info['launch']})"
                                             if ncu_info else None),
                          "ncu_issue_active_pct": ncu_info.get("issue_active_pct") if ncu_info else None,
+                         "instructions_per_evaluated_pair": (
+                             32.0 * ncu_info["warp_instructions_per_evaluated_pair"]
+                             if ncu_info and "warp_instructions_per_evaluated_pair" in ncu_info else None),
+                         "instructions_per_evaluated_pair_note": "thread-level issue slots (32 x warp "
+                             "instructions) per evaluated pair, from the committed ncu capture",
+                         "votes_per_rotation": sum(r["votes"] for r in results) / (args.steps * R),
                          "ncu_alu_pipe_pct": ncu_info.get("alu_pipe_pct") if ncu_info else None,
                          "note": "integer/ALU-issue bound (no tensor-core or HBM bound applies: "
                                  "inputs are shared-memory resident, contraction dim 3)"},
