@@ -460,6 +460,102 @@ def sharded_measurements(args, rank, world, local):
     return out
 
 
+EXTRA_WORKLOADS = ("c1", "c4")  # BASELINE.json configs[0] and configs[3], beside the c2 headline
+
+
+def workload_line(name, args, rank, world, local, steps=10, warmup=3):
+    """One BASELINE config measured like the headline, first-class: device-
+    resident registrations (plans built before timing, L2 flushed between
+    steps, CUDA events, max over ranks), and end to end through the public
+    API from host numpy buffers -- dses_batch (plan construction of k+1
+    overlapped with the search of k) and single dses() calls."""
+    import torch
+    import torch.distributed as dist
+    from paper_2502_00115_b200 import _native, dses, dses_batch
+    from paper_2502_00115_b200.engines import prepare
+    try:
+        c = workload(name)
+        cfg = search_config(c)
+        nsteps = warmup + steps
+        pairs, _ = bench_pairs(name, nsteps, rank * nsteps, args.inputs)
+        preps = [prepare(x, y, cfg) for x, y, _ in pairs]
+        plans = [_native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims, local) for p in preps]
+        grids = [_native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot) for p in preps]
+        for pl in plans:
+            pl.reserve(cfg.rotation_count)
+        flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        stream = torch.cuda.current_stream().cuda_stream
+
+        def timed(fn):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(steps)]
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            out = []
+            for k in range(steps):
+                flush.zero_()
+                ev[k][0].record()
+                out.append(fn(k))
+                ev[k][1].record()
+            torch.cuda.synchronize()
+            t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64,
+                             device="cuda")
+            if world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item()), out
+
+        def dev(k):
+            p = preps[k]
+            return plans[k].search(grids[k], cfg.q, p.code, p.param, p.skip_refine, stream=stream)
+
+        for k in range(warmup):
+            dev(k)
+        ms, res = timed(lambda k: dev(warmup + k))
+        host = pairs[warmup:]
+        dses(host[0][0], host[0][1], cfg, device=local)
+        ms_single, _ = timed(lambda k: dses(host[k][0], host[k][1], cfg, device=local))
+        # a full untimed batch first (the stream-ordered memory pool grows to
+        # the batch's working set once), then the median of three
+        dses_batch([h[0] for h in host], [h[1] for h in host], cfg, device=local)
+        if world > 1:
+            dist.barrier()
+        bt = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.zero_()
+            b0.record()
+            dses_batch([h[0] for h in host], [h[1] for h in host], cfg, device=local)
+            b1.record()
+            torch.cuda.synchronize()
+            bt.append(b0.elapsed_time(b1))
+        tb = torch.tensor([sorted(bt)[1]], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        ms_batch = float(tb.item())
+        for pl in plans:
+            pl.close()
+        R = cfg.rotation_count
+        tot = steps * R * world
+        return {
+            "name": name, "metric": METRIC, "unit": UNIT, "value": tot / (ms * 1e-3),
+            "ms_per_step": ms / steps, "steps": steps, "warmup": warmup, "n_gpus": world,
+            "scaling": "weak", "registrations_per_sec": steps * world / (ms * 1e-3),
+            "config": {"workload": describe(name, c, cfg, preps[0].x.shape[0], preps[0].y.shape[0]),
+                       "metric": cfg.metric.kind, "rotations": R},
+            "vote_kernel_ms_per_step": sum(r["ms_vote_kernel"] for r in res) / steps,
+            "pairs_evaluated_per_rotation": sum(r["pairs_evaluated"] for r in res) / (steps * R),
+            "e2e": {"value": tot / (ms_batch * 1e-3), "unit": UNIT,
+                    "path": "dses_batch over the timed pairs (host numpy in, results out)",
+                    "single_call": {"value": tot / (ms_single * 1e-3), "unit": UNIT,
+                                    "ms_per_step": ms_single / steps,
+                                    "path": "one dses() call per step (plan construction exposed)"}},
+        }
+    except Exception as exc:  # reported, never fatal for the headline line
+        return {"name": name, "error": f"{type(exc).__name__}: {exc}"}
+
+
 def _free_port():
     import socket
     with socket.socket() as sk:
@@ -609,6 +705,8 @@ def main():
                zip(bres, [dses(p[0], p[1], cfg, device=local) for p in e2e_pairs[:2]]))
 
     sharded = None if args.no_sharded else sharded_measurements(args, rank, world, local)
+    extra = [] if args.no_sharded else [workload_line(w, args, rank, world, local)
+                                        for w in EXTRA_WORKLOADS if w != args.config]
 
     if rank == 0:
         ffma_s, _ = _native.probe_fp32_peak(local)
@@ -685,6 +783,8 @@ def main():
         }
         if sharded is not None:
             line["rotation_sharded"] = sharded
+        if extra:
+            line["workloads"] = extra
         if world == 1 and not args.no_cpu_baseline:
             x0, y0, _ = pairs[0]
 

@@ -4,11 +4,12 @@ sys.path.insert(0, '.')
 import torch
 import bench
 from paper_2502_00115_b200 import dses_batch
-c = bench.workload('c2'); cfg = bench.search_config(c)
-pairs, _ = bench.bench_pairs('c2', 10)
+name = sys.argv[1] if len(sys.argv) > 1 else 'c2'
+c = bench.workload(name); cfg = bench.search_config(c)
+pairs, _ = bench.bench_pairs(name, 10)
 xs, ys = [p[0] for p in pairs], [p[1] for p in pairs]
 dses_batch(xs[:2], ys[:2], cfg)
-for rep in range(8):
+for rep in range(4):
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter(); s.record()
