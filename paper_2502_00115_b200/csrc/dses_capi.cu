@@ -979,7 +979,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     v.unit_cap = (int)std::max<int64_t>(kUnitCapMin, std::min<int64_t>(kUnitCapMin + extra,
                                                                     std::max<int64_t>(all, kUnitCapMin)));
     // a round of one group must fit all its units plus its chunk mask
-    v.unit_cap = (int)std::max<int64_t>(v.unit_cap, (int64_t)v.nxt + 1);
+    v.unit_cap = (int)std::max<int64_t>(v.unit_cap, (int64_t)v.nxt + 2);
   }
   trace("occupancy");
   int per_sm = vote_max_ctas_per_sm(v, P->hsmem, P->psmem, P->vote_threads);

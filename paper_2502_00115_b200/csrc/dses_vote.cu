@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 
   int* s_nunits = red + 96;
   int* s_next = red + 97;
+  int* s_ovf = red + 98;
   const unsigned lanemask_lt = (1u << lane) - 1u;
   const uint32_t P_sh = PSMEM ? (uint32_t)__cvta_generic_to_shared(P) : 0u;
   // fast-path constants through shared memory: loaded into regular registers
@@ -377,9 +378,17 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 
   unsigned long long st_votes = 0;
   const bool exact_mode = (p.F == 0);
-  // reference groups per round so that the round's units AND one chunk mask
-  // per group (stored at the tail of `units`) fit
-  const int tiles_per_round = max(1, p.unit_cap / max(1, p.nxt + 1));
+  // Rounds: each tries up to `gmax` reference groups (their chunk masks live
+  // at the tail of `units`, the rest holds the round's surviving (group,
+  // unit) pairs); a round whose pairs overflow the list keeps the groups
+  // below the first one that overflowed and the next round restarts there
+  // (a one-group round when even the first group overflowed: its <= nxt
+  // units always fit).  With typical overlap a rotation is one round.
+  // (the RISK specialisation -- small reference clouds -- keeps worst-case
+  // sized rounds: no overflow bookkeeping on its hot path)
+  constexpr bool OVF = !RISK;
+  const int gmax = OVF ? max(1, min(min(p.nyt, p.unit_cap / 4), p.unit_cap - p.nxt - 1))
+                       : max(1, p.unit_cap / max(1, p.nxt + 1));
   const bool masks = !exact_mode && nxc > 1 && nxc <= 32;
 
   // rotations: the first one static, the rest from a global queue (the cost
@@ -446,12 +455,17 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     //      tests one source point of the unit against the group's box, then
     //      every surviving source i is broadcast from shared memory and voted
     //      in place (slot_single / slot_multi).
-    for (int b0 = 0; b0 < p.nyt; b0 += tiles_per_round) {
-      const int b1 = min(p.nyt, b0 + tiles_per_round);
-      if (tid == 0) { *s_nunits = 0; *s_next = 0; }
+    // Rounds of up to gmax groups.  OVF: a round whose (group, unit) pairs
+    // overflowed the list keeps the groups below its first overflowing group
+    // and the next round restarts there (a one-group round when that was its
+    // first group: its <= nxt units always fit).
+    for (int b0 = 0, gnext = gmax; b0 < p.nyt;) {
+      const int b1 = min(p.nyt, b0 + (OVF ? gnext : gmax));
+      if (tid == 0) { *s_nunits = 0; *s_next = 0; if (OVF) *s_ovf = b1; }
       // which 32-unit chunks each group can reach: one thread per group
       // (instead of a warp-uniform test per (group, chunk))
-      unsigned* gmask = reinterpret_cast<unsigned*>(units) + (p.unit_cap - tiles_per_round);
+      const int cap_u = p.unit_cap - gmax;  // unit-list capacity of the round
+      unsigned* gmask = reinterpret_cast<unsigned*>(units) + cap_u;
       if (masks)
         for (int k = tid; k < b1 - b0; k += nthreads) {
           const YTile yg = load_ytile(p.yt, b0 + k);
@@ -470,9 +484,17 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
             const unsigned m = __ballot_sync(0xffffffffu, ov);
             if (m) {
               int slot = 0;
-              if (lane == 0) slot = atomicAdd(s_nunits, __popc(m));
+              if (lane == 0) {
+                slot = atomicAdd(s_nunits, __popc(m));
+                if (OVF && slot + __popc(m) > cap_u) atomicMin(s_ovf, b);
+              }
               slot = __shfl_sync(0xffffffffu, slot, 0);
-              if (ov) units[slot + __popc(m & lanemask_lt)] = ((unsigned)b << 16) | (unsigned)a;
+              if (OVF) {
+                slot += __popc(m & lanemask_lt);
+                if (ov && slot < cap_u) units[slot] = ((unsigned)b << 16) | (unsigned)a;
+              } else if (ov) {
+                units[slot + __popc(m & lanemask_lt)] = ((unsigned)b << 16) | (unsigned)a;
+              }
             }
           }
           continue;
@@ -487,18 +509,27 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
           const unsigned m = __ballot_sync(0xffffffffu, ov);
           if (m) {
             int slot = 0;
-            if (lane == 0) slot = atomicAdd(s_nunits, __popc(m));
+            if (lane == 0) {
+              slot = atomicAdd(s_nunits, __popc(m));
+              if (OVF && slot + __popc(m) > cap_u) atomicMin(s_ovf, b);
+            }
             slot = __shfl_sync(0xffffffffu, slot, 0);
-            if (ov) units[slot + __popc(m & lanemask_lt)] = ((unsigned)b << 16) | (unsigned)a;
+            if (OVF) {
+              slot += __popc(m & lanemask_lt);
+              if (ov && slot < cap_u) units[slot] = ((unsigned)b << 16) | (unsigned)a;
+            } else if (ov) {
+              units[slot + __popc(m & lanemask_lt)] = ((unsigned)b << 16) | (unsigned)a;
+            }
           }
         }
       }
       __syncthreads();
-      const int nunits = *s_nunits;
+      const int nunits = OVF ? min(*s_nunits, cap_u) : *s_nunits;
+      const unsigned ovf = OVF ? (unsigned)*s_ovf : 0xffffffffu;  // groups >= ovf: next round
       // sparse overlap (< 1/4 of the round's (group, unit) pairs) means light
       // units: claim three at a time to amortise the claim; dense overlap
       // (heavy units) claims one at a time to keep the round's tail balanced
-      const int kpop = (4 * nunits < (b1 - b0) * p.nxt) ? 3 : 1;
+      const int kpop = (4 * (int64_t)nunits < (int64_t)(b1 - b0) * p.nxt) ? 3 : 1;
       for (int u = nunits, uend = nunits;; ++u) {
         if (u >= uend) {  // claim the next kpop units
           if (lane == 0) u = atomicAdd(s_next, kpop);
@@ -507,6 +538,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
           uend = min(nunits, u + kpop);
         }
         const unsigned unit = units[u];
+        if (OVF && (unit >> 16) >= ovf) continue;  // warp-uniform
         const YTile yt = load_ytile(p.yt, (int)(unit >> 16));
         const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + (unit & 0xffffu)));
         const int ustart = U.x, ucount = U.y;
@@ -570,7 +602,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
                                                         : nsafe + __popc(mrisk & lanemask_lt)),
                         make_int4(Pl.x, Pl.y, Pl.z, ustart + lane));
         __syncwarp();
-#define DSES_SLOTS(GP)                                                                         \
+  #define DSES_SLOTS(GP)                                                                         \
   int t = 0;                                                                                   \
   if (RISK)                                                                                    \
     for (; t + 3 < nsafe; t += 4)                                                              \
@@ -590,9 +622,15 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         if (gp == 0) { DSES_SLOTS(0) }
         else if (gp == 1) { DSES_SLOTS(1) }
         else { DSES_SLOTS(2) }
-#undef DSES_SLOTS
+  #undef DSES_SLOTS
       }
       __syncthreads();  // units[] is rebuilt by the next round
+      if (OVF) {
+        gnext = ((int)ovf == b0) ? 1 : gmax;
+        b0 = (int)ovf;
+      } else {
+        b0 += gmax;
+      }
     }
     if (L.nrare > 0) {
       L.rechecks += flush_rare<HSMEM, PSMEM>(p, R, P, hist, hist_sh, L.rare_sh, L.nrare, lane) & 0xffffu;
