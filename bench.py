@@ -730,6 +730,10 @@ def main():
             "data": data_desc,
             "config": {"workload": describe(args.config, c, cfg, n_src, preps[0].y.shape[0]),
                        "metric": cfg.metric.kind, "rotations": R},
+            "metric_note": ("truncated-L1 at 5 bins: the reference's default and pinned kind; "
+                            "BASELINE.json's 'truncated-L2' has no reference implementation "
+                            "(gridreg/metrics.py:35), its trunc_l2 extension here is parity-"
+                            "unpinned (oracle restatement only)"),
             "parallelism": f"replicas x{world} (registrations sharded over ranks, no collective)",
             "l2_flush": "512 MiB buffer zeroed between timed steps",
             "registrations_per_sec": args.steps * world / (ms_max * 1e-3),
