@@ -275,7 +275,7 @@ struct dses_plan {
   DevBuf yorig;                                        // (m, 3) reference, original order (sparse path)
   bool sparse = false;                                 // lattice beyond kDenseMaxBins: sort-based mode
   DevBuf lins64, sparse_scratch;
-  float gorg[3] = {0, 0, 0}, gh = 1.f;
+  float gorg[3] = {0, 0, 0}, gh = 1.f, g_pts_per_cell = 1.f;
   int gdim[3] = {1, 1, 1};
   DevBuf cth, sth, rots;                               // rotation sources
   DevBuf counts, lins, ties;                           // per-rotation outputs
@@ -653,7 +653,15 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     for (int c = 0; c < ncell; ++c) range[c] = make_int2(cnt[c], cnt[c + 1]);
     gp.resize(m);
     std::vector<int> fill(cnt.begin(), cnt.end() - 1);
-    for (int64_t j = 0; j < m; ++j) gp[fill[cid[j]]++] = yf[j];
+    for (int64_t j = 0; j < m; ++j) {  // .w: the point's index in axis-0 order (exact re-score)
+      float4 g = yf[j];
+      int jj = (int)j;
+      std::memcpy(&g.w, &jj, sizeof jj);
+      gp[fill[cid[j]]++] = g;
+    }
+    int occupied = 0;
+    for (int c = 0; c < ncell; ++c) occupied += range[c].y > range[c].x;
+    P->g_pts_per_cell = (float)m / (float)std::max(1, occupied);
     for (int k = 0; k < 3; ++k) { P->gorg[k] = mn[k]; P->gdim[k] = dim[k]; }
     P->gh = hf;
   }
@@ -1126,6 +1134,7 @@ ScoreParams score_params(const dses_plan* P, const RotSource& rs, int code, doub
   for (int k = 0; k < 3; ++k) { s.gorg[k] = P->gorg[k]; s.gdim[k] = P->gdim[k]; }
   s.gh = P->gh;
   s.ginv = 1.0f / P->gh;
+  s.gppc = P->g_pts_per_cell;
   return s;
 }
 

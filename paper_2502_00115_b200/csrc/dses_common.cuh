@@ -141,10 +141,11 @@ struct ScoreParams {     // scoring kernels (dses_score.cu)
   double tcen[3];         //       (engines.py:168-169), f = the lattice index of lin
   // uniform grid over the reference cloud (screen nearest-neighbour search)
   const int2* gcell;      // per cell: [begin, end) into gpts
-  const float4* gpts;     // reference points sorted by cell (fp32)
+  const float4* gpts;     // reference points sorted by cell (fp32; .w = int index in axis-0 order)
   float gorg[3];          // grid origin
   float gh, ginv;         // cell size and 1/cell size
   int gdim[3];            // cells per axis
+  float gppc;             // reference points per non-empty cell (exact re-score: grid vs window)
 };
 
 struct SparseParams {    // sort-based mode queries (dses_sparse.cu)

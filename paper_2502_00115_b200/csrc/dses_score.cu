@@ -135,8 +135,48 @@ __device__ double exact_point_best(const ScoreParams& s, double p0, double p1, d
   const double* y2 = s.ys2;
   const int m = s.m;
   if (s.code == kTruncL1 || s.code == kTruncL2) {
-    const int jlo = lower_bound_d(y0, m, dsub(p0, s.param));
-    const int jhi = lower_bound_d(y0, m, dadd(p0, s.param));
+    const double lo = dsub(p0, s.param), hi = dadd(p0, s.param);
+    const int jlo = lower_bound_d(y0, m, lo);
+    const int jhi = lower_bound_d(y0, m, hi);
+    // The reference scans the axis-0 window [lo, hi) (jlo..jhi in axis-0
+    // order).  When that slab is wide (surfaces perpendicular to axis 0),
+    // visit instead the uniform-grid cells around the tau-box: the same
+    // window test and the same binary64 distance per point, so the minimum
+    // is identical -- a point with |y_k - p_k| > tau on axis 1 or 2 has a
+    // distance >= tau (monotone rounding) and cannot lower best = tau.
+    int cl[3], ch[3];
+    int ncell = 1;
+    const double pk[3] = {p0, p1, p2};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      cl[k] = max(0, __float2int_rd(((float)dsub(pk[k], s.param) - s.gorg[k]) * s.ginv) - 1);
+      ch[k] = min(s.gdim[k] - 1, __float2int_rd(((float)dadd(pk[k], s.param) - s.gorg[k]) * s.ginv) + 1);
+      ncell *= max(0, ch[k] - cl[k] + 1);
+    }
+    if ((float)(jhi - jlo) > 2.0f * (float)ncell * (1.0f + s.gppc)) {
+      const double cap = s.code == kTruncL1 ? s.param : dmul(s.param, s.param);
+      double best = cap;
+      for (int x = cl[0]; x <= ch[0]; ++x)
+        for (int yy = cl[1]; yy <= ch[1]; ++yy)
+          for (int z = cl[2]; z <= ch[2]; ++z) {
+            const int2 rg = __ldg(&s.gcell[(x * s.gdim[1] + yy) * s.gdim[2] + z]);
+            for (int q = rg.x; q < rg.y; ++q) {
+              const int j = __float_as_int(__ldg(&s.gpts[q]).w);
+              const double yj0 = y0[j];
+              if (!(yj0 >= lo && yj0 < hi)) continue;  // the reference's window
+              double v;
+              if (s.code == kTruncL1) {
+                v = dadd(dadd(fabs(dsub(yj0, p0)), fabs(dsub(y1[j], p1))), fabs(dsub(y2[j], p2)));
+              } else {
+                const double a = dsub(yj0, p0), b = dsub(y1[j], p1), c = dsub(y2[j], p2);
+                v = dadd(dadd(dmul(a, a), dmul(b, b)), dmul(c, c));
+              }
+              if (v < best) best = v;
+            }
+          }
+      if (s.code == kTruncL1) return best;
+      return best < cap ? sqrt(best) : s.param;
+    }
     if (s.code == kTruncL1) {
       double best = s.param;
       for (int j = jlo; j < jhi; ++j) {
@@ -555,8 +595,99 @@ __global__ void rescore_compact_kernel(const double* err, int64_t ncand, double 
 // grid (ceil(n/128), nsel): per-point values; then one thread per candidate
 // sums them serially in source order (_kernels.py:315-324).
 // ---------------------------------------------------------------------------
+// One warp per (candidate, source point): _point_best (_kernels.py:34-80)
+// with the scan split over the lanes.  Each lane evaluates a subset of the
+// same points with the same binary64 operations as exact_point_best; the
+// minimum (and sat_l0's "any inlier") is order-independent, so the warp
+// reduction gives the identical value.  The points scanned are the
+// reference's own window (axis-0-sorted, [p0 - tau, p0 + tau) / half-width
+// for sat_l0), or -- when that slab is wide, e.g. a surface perpendicular to
+// axis 0 -- the uniform-grid cells around the (tau-)box with the same window
+// test per point (a point outside the box on axis 1 or 2 cannot lower the
+// truncated minimum, resp. cannot be a strict Chebyshev inlier).
+__device__ __forceinline__ double warp_min_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ double exact_point_best_warp(const ScoreParams& s, double p0, double p1, double p2,
+                                        int lane) {
+  const double* y0 = s.ys0;
+  const double* y1 = s.ys1;
+  const double* y2 = s.ys2;
+  const int m = s.m;
+  if (s.code == kL1 || s.code == kL2) {  // every reference point
+    double best = CUDART_INF;
+    for (int j = lane; j < m; j += 32) {
+      double v;
+      if (s.code == kL1) {
+        v = dadd(dadd(fabs(dsub(y0[j], p0)), fabs(dsub(y1[j], p1))), fabs(dsub(y2[j], p2)));
+      } else {
+        const double a = dsub(y0[j], p0), b = dsub(y1[j], p1), c = dsub(y2[j], p2);
+        v = dadd(dadd(dmul(a, a), dmul(b, b)), dmul(c, c));
+      }
+      if (v < best) best = v;
+    }
+    best = warp_min_d(best);
+    return s.code == kL1 ? best : sqrt(best);
+  }
+  const bool sat = s.code == kSatL0;
+  const double w = sat ? dmul(0.5, s.param) : s.param;   // window half-width
+  const double lo = dsub(p0, w), hi = dadd(p0, w);
+  const int jlo = lower_bound_d(y0, m, lo);
+  const int jhi = lower_bound_d(y0, m, hi);
+  const double cap = sat ? 1.0 : (s.code == kTruncL1 ? s.param : dmul(s.param, s.param));
+  double best = cap;
+  bool hit = false;
+  // the lane's point j: the truncated distance / strict inlier test
+  auto visit = [&](int j) {
+    const double yj0 = y0[j];
+    if (sat) {
+      hit |= fabs(dsub(yj0, p0)) < w && fabs(dsub(y1[j], p1)) < w && fabs(dsub(y2[j], p2)) < w;
+      return;
+    }
+    double v;
+    if (s.code == kTruncL1) {
+      v = dadd(dadd(fabs(dsub(yj0, p0)), fabs(dsub(y1[j], p1))), fabs(dsub(y2[j], p2)));
+    } else {
+      const double a = dsub(yj0, p0), b = dsub(y1[j], p1), c = dsub(y2[j], p2);
+      v = dadd(dadd(dmul(a, a), dmul(b, b)), dmul(c, c));
+    }
+    if (v < best) best = v;
+  };
+  int cl[3], ch[3];
+  int ncell = 1;
+  const double pk[3] = {p0, p1, p2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    cl[k] = max(0, __float2int_rd(((float)dsub(pk[k], w) - s.gorg[k]) * s.ginv) - 1);
+    ch[k] = min(s.gdim[k] - 1, __float2int_rd(((float)dadd(pk[k], w) - s.gorg[k]) * s.ginv) + 1);
+    ncell *= max(0, ch[k] - cl[k] + 1);
+  }
+  if ((float)(jhi - jlo) > 2.0f * (float)ncell * (1.0f + s.gppc)) {
+    const int ny = ch[1] - cl[1] + 1, nz = ch[2] - cl[2] + 1;
+    for (int t = lane; t < ncell; t += 32) {  // lane = cell of the box
+      const int x = cl[0] + t / (ny * nz), yy = cl[1] + (t / nz) % ny, z = cl[2] + t % nz;
+      const int2 rg = __ldg(&s.gcell[(x * s.gdim[1] + yy) * s.gdim[2] + z]);
+      for (int q = rg.x; q < rg.y; ++q) {
+        const int j = __float_as_int(__ldg(&s.gpts[q]).w);
+        const double yj0 = y0[j];
+        if (yj0 >= lo && yj0 < hi) visit(j);  // the reference's window
+      }
+    }
+  } else {
+    for (int j = jlo + lane; j < jhi; j += 32) visit(j);
+  }
+  if (sat) return __any_sync(0xffffffffu, hit) ? 0.0 : 1.0;
+  best = warp_min_d(best);
+  if (s.code == kTruncL1) return best;
+  return best < cap ? sqrt(best) : s.param;
+}
+
 constexpr int kExactThreads = 128;
 
+// warp = source point (kExactThreads / 32 points per block), y = candidate
 __global__ void __launch_bounds__(kExactThreads) exact_points_kernel(ScoreParams s,
                                                                      const int64_t* rows,
                                                                      const int* lins,
@@ -565,29 +696,62 @@ __global__ void __launch_bounds__(kExactThreads) exact_points_kernel(ScoreParams
                                                                      const unsigned long long* dcount) {
   __shared__ double R[9], t[3];
   const int64_t nsel = eff_count(dcount, nsel_cap);
+  const int lane = threadIdx.x & 31;
   for (int64_t k = blockIdx.y; k < nsel; k += gridDim.y) {
     const int64_t c = sel ? sel[k] : k;
     if (c < 0) continue;  // no winner (block-uniform)
     load_pose(s, rows[c], lins[c], R, t);
-    const int i = blockIdx.x * kExactThreads + threadIdx.x;
-    if (i < s.n) {
+    const int i = blockIdx.x * (kExactThreads / 32) + (threadIdx.x >> 5);
+    if (i < s.n) {  // warp-uniform
       double pp[3];
       pose_point(R, t, s.x + 3 * i, pp);
-      vals[(size_t)k * s.n + i] = exact_point_best(s, pp[0], pp[1], pp[2]);
+      const double v = exact_point_best_warp(s, pp[0], pp[1], pp[2], lane);
+      if (lane == 0) vals[(size_t)k * s.n + i] = v;
     }
     __syncthreads();
   }
 }
 
+// The serial binary64 sum over i in the reference's order
+// (_kernels.py:297-324: err += point_best, i = 0..n-1).  One warp per
+// candidate: lanes load 32 consecutive values (coalesced, in flight
+// together), lane 0 adds them in order as they arrive by shuffle -- the same
+// dependent chain of additions, without a global-load latency per term.
+// `integral`: the terms are 0.0 / 1.0 (sat_l0), so every summation order
+// gives the same (exact, integer) total and the lanes reduce in parallel.
 __global__ void exact_sum_kernel(const double* vals, int n, int64_t nsel_cap, double* out,
-                                 const unsigned long long* dcount) {
+                                 const unsigned long long* dcount, bool integral) {
   const int64_t nsel = eff_count(dcount, nsel_cap);
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nsel;
-       c += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < nsel; c += warps) {
     const double* v = vals + (size_t)c * n;
+    if (integral) {
+      double part = 0.0;
+      for (int i = lane; i < n; i += 32) part += v[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) out[c] = part;
+      continue;
+    }
     double total = 0.0;
-    for (int i = 0; i < n; ++i) total = dadd(total, v[i]);
-    out[c] = total;
+    int i0 = 0;
+    for (; i0 + 32 <= n; i0 += 32) {  // full chunks: shuffles issued ahead of the adds
+      const double mine = v[i0 + lane];
+#pragma unroll
+      for (int k0 = 0; k0 < 32; k0 += 8) {
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t[k] = __shfl_sync(0xffffffffu, mine, k0 + k);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) total = dadd(total, t[k]);
+      }
+    }
+    if (i0 < n) {
+      const double mine = i0 + lane < n ? v[i0 + lane] : 0.0;
+      for (int k = 0; k < n - i0; ++k) total = dadd(total, __shfl_sync(0xffffffffu, mine, k));
+    }
+    if (lane == 0) out[c] = total;
   }
 }
 
@@ -776,12 +940,12 @@ cudaError_t launch_exact(const ScoreParams& s, const int64_t* rows, const int* l
                          int64_t nsel, double* vals, double* out, cudaStream_t st,
                          const unsigned long long* dcount) {
   if (nsel <= 0) return cudaSuccess;
-  const int nblk = (s.n + kExactThreads - 1) / kExactThreads;
-  const int64_t cap_y = std::max<int64_t>(1, std::min<int64_t>(65535, 4096 / nblk));
+  const int nblk = (s.n + kExactThreads / 32 - 1) / (kExactThreads / 32);
+  const int64_t cap_y = std::max<int64_t>(1, std::min<int64_t>(65535, 16384 / nblk));
   exact_points_kernel<<<dim3(nblk, (unsigned)std::min<int64_t>(nsel, dcount ? cap_y : 65535)),
                         kExactThreads, 0, st>>>(s, rows, lins, sel, nsel, vals, dcount);
-  const int rb = (int)std::min<int64_t>(dcount ? 64 : 65535, (nsel + 127) / 128);
-  exact_sum_kernel<<<std::max(rb, 1), 128, 0, st>>>(vals, s.n, nsel, out, dcount);
+  const int rb = (int)std::min<int64_t>(dcount ? 1024 : 65535, (nsel + 3) / 4);  // 4 warps per block
+  exact_sum_kernel<<<std::max(rb, 1), 128, 0, st>>>(vals, s.n, nsel, out, dcount, s.code == kSatL0);
   return cudaGetLastError();
 }
 
