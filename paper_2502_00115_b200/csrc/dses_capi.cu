@@ -254,8 +254,14 @@ struct UploadPack {
 // ---------------------------------------------------------------------------
 // the plan
 // ---------------------------------------------------------------------------
+namespace {
+struct RefTopo;
+struct DeviceRef;
+}  // namespace
 struct dses_plan {
   int device = 0, sms = 0;
+  std::shared_ptr<const RefTopo> topo;  // the reference cloud's cached topology
+  std::shared_ptr<DeviceRef> dref;      // and its device copy (shared by plans)
   size_t smem_optin = 0;
   int64_t n = 0, m = 0, m_pad = 0;
   double bin = 0, inv_bin = 0;
@@ -565,39 +571,64 @@ std::vector<std::pair<int, int>> near_pairs(const double* y, int64_t m, double t
   return out;
 }
 
-int build_plan(dses_plan* P, const double* x, const double* y) {
-  const int64_t n = P->n, m = P->m;
-  cudaStream_t st = upload_stream(P->device);
-  // ---- fixed-point scale
-  trace("fixed-point scale");
-  double ymax = 0, xnorm = 0;
-  for (int64_t j = 0; j < m; ++j)
-    for (int k = 0; k < 3; ++k) ymax = std::max(ymax, std::fabs(y[3 * j + k]));
-  for (int64_t i = 0; i < n; ++i)
-    xnorm = std::max(xnorm, std::sqrt(x[3 * i] * x[3 * i] + x[3 * i + 1] * x[3 * i + 1] +
-                                      x[3 * i + 2] * x[3 * i + 2]));
-  double lomax = 0;
-  for (int k = 0; k < 3; ++k)
-    lomax = std::max(lomax, std::max(std::fabs((double)P->ilo[k]),
-                                     std::fabs((double)(P->ilo[k] + P->dims[k]))));
-  const double A = ymax * P->inv_bin + 3.0 * xnorm * P->inv_bin + lomax + 8.0;
-  int F = 0;
-  if (std::isfinite(A) && A > 0) F = (int)std::floor(std::log2(std::ldexp(1.0, 29) / A));
-  F = std::min(F, 20);
-  if (F < 6) F = 0;  // exact mode: every pair re-binned in binary64
-  P->F = F;
-  const double S = std::ldexp(1.0, F);
-  P->by = ymax;
-  double tmax = 0;
-  for (int k = 0; k < 3; ++k)
-    tmax = std::max(tmax, (std::fabs((double)P->ilo[k]) + (double)P->dims[k]) * P->bin);
-  P->bx = xnorm + tmax;
+// ---------------------------------------------------------------------------
+// Reference-cloud topology: everything of a plan that depends only on the
+// reference cloud and the bin size -- the scoring layout (axis-0 sort, fp32
+// copy, uniform grid), the dedup partners (points closer than one bin per
+// axis), their components, the reference groups (k-d tiles over the
+// components) and the exact path's near lists.  Cached for the most recent
+// clouds (content-compared), so registering many sources against one model
+// (the c4 tool-pose use) builds it once.
+// ---------------------------------------------------------------------------
+struct GroupSpan { int start, count, gm; };
+struct RefTopo {
+  int64_t m = 0;
+  double bin = 0;
+  std::vector<double> y;                       // the cloud (cache key, compared exactly)
+  std::vector<double> c0, c1, c2;              // axis-0-sorted columns
+  std::vector<float4> yf, gp;                  // fp32 copy; grid-ordered points
+  std::vector<int2> range;                     // grid cells
+  float gorg[3] = {0, 0, 0}, gh = 1.f, gppc = 1.f;
+  int gdim[3] = {1, 1, 1};
+  std::vector<std::pair<int, int>> near;       // dedup partner pairs
+  std::vector<int> aoff, aidx;                 // their adjacency (CSR, original indices)
+  std::vector<int> yidx;                       // tile-order entry -> original index
+  std::vector<char> yfar;                      // component too large for a warp
+  std::vector<GroupSpan> groups;
+  std::vector<int> pos;                        // original index -> tile-order entry
+  std::vector<int> noff, nidx;                 // exact-path near lists (tile order, j' < j)
+  std::vector<double> ys;                      // the cloud in tile order
+  mutable std::mutex dmu;
+  mutable std::shared_ptr<DeviceRef> dev[64];  // device copies of the arrays above
+};
 
+// A RefTopo's read-only arrays on one device, uploaded once and borrowed by
+// every plan of that reference cloud (freed with the last plan / eviction).
+struct DeviceRef {
+  int device = 0;
+  DevBuf arena, yorig, ys, near_off, near_idx, ys0, ys1, ys2, ysf, gcell, gpts;
+  ~DeviceRef() {  // possibly on another thread's current device (cache eviction)
+    if (!arena.p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    cudaFree(arena.p);  // synchronous: no plan of this cloud is left
+    cudaSetDevice(cur);
+    arena.p = nullptr;
+  }
+};
+
+static std::shared_ptr<const RefTopo> build_ref_topo(const double* y, int64_t m, double bin) {
+  auto T = std::make_shared<RefTopo>();
+  T->m = m;
+  T->bin = bin;
+  T->y.assign(y, y + 3 * m);
+  std::vector<double>& c0 = T->c0; std::vector<double>& c1 = T->c1; std::vector<double>& c2 = T->c2;
+  std::vector<float4>& yf = T->yf; std::vector<float4>& gp = T->gp;
+  std::vector<int2>& range = T->range;
+  RefTopo* PT = T.get();
   // ---- scoring layout (y sorted by axis 0, fp32 copy, uniform grid) on a
   //      helper thread: independent of the vote layout built below
-  std::vector<double> c0, c1, c2;
-  std::vector<float4> yf, gp;
-  std::vector<int2> range;
   // (small clouds: deferred, i.e. run inline at get(); a thread costs more)
   auto scoring = std::async(m >= 4096 ? std::launch::async : std::launch::deferred, [&]() {
   // ---- scoring layout: x original order, y sorted by axis 0 (stable)
@@ -627,7 +658,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
         mn[k] = std::min(mn[k], v);
         mx[k] = std::max(mx[k], v);
       }
-    double h = 4.0 * P->bin;
+    double h = 4.0 * bin;
     int dim[3];
     for (;;) {
       int64_t cells = 1;
@@ -661,46 +692,11 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     }
     int occupied = 0;
     for (int c = 0; c < ncell; ++c) occupied += range[c].y > range[c].x;
-    P->g_pts_per_cell = (float)m / (float)std::max(1, occupied);
-    for (int k = 0; k < 3; ++k) { P->gorg[k] = mn[k]; P->gdim[k] = dim[k]; }
-    P->gh = hf;
+    PT->gppc = (float)m / (float)std::max(1, occupied);
+    for (int k = 0; k < 3; ++k) { PT->gorg[k] = mn[k]; PT->gdim[k] = dim[k]; }
+    PT->gh = hf;
   }
   });
-  // ---- spatial tiles
-  trace("spatial tiles");
-  std::vector<int> px(n);
-  std::iota(px.begin(), px.end(), 0);
-  std::vector<std::pair<int, int>> tx;
-  kd_tiles(x, 0, n, px, tx, kTile, host_threads() >= 4 ? 2 : 0);  // source units
-  std::vector<double> xs(3 * n);
-  for (int64_t i = 0; i < n; ++i)
-    for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
-  const double inv_s = P->inv_bin * S;
-  // sphere (bbox centre, max distance) of source points [start, start+count)
-  auto sphere = [&](XTile& T) {
-    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int q = T.start; q < T.start + T.count; ++q)
-      for (int k = 0; k < 3; ++k) {
-        mn[k] = std::min(mn[k], xs[3 * q + k]);
-        mx[k] = std::max(mx[k], xs[3 * q + k]);
-      }
-    for (int k = 0; k < 3; ++k) T.c[k] = 0.5 * (mn[k] + mx[k]);
-    double rad = 0;
-    for (int q = T.start; q < T.start + T.count; ++q) {
-      double d2 = 0;
-      for (int k = 0; k < 3; ++k) d2 += (xs[3 * q + k] - T.c[k]) * (xs[3 * q + k] - T.c[k]);
-      rad = std::max(rad, std::sqrt(d2));
-    }
-    T.rad = F ? (int)std::ceil(rad * inv_s * (1.0 + 1e-9)) + 3 : 0;
-  };
-  std::vector<XTile> xt(tx.size());
-  for (size_t t = 0; t < tx.size(); ++t) {
-    XTile& T = xt[t];
-    T = XTile{};
-    T.start = tx[t].first;
-    T.count = tx[t].second;
-    sphere(T);
-  }
   // ---- reference layout.  Dedup partners (points closer than one bin per
   // axis: the only pairs that can share a bin for one source) form
   // components; groups of <= 32 points (one per lane) are k-d tiles over the
@@ -709,8 +705,9 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   // than kMaxComp, and points with more than two earlier partners, are
   // flagged "far" and take the exact path when they vote.
   trace("dedup components");
-  const double thr = P->bin * (1.0 + 1e-6);
-  const std::vector<std::pair<int, int>> near = near_pairs(y, m, thr);
+  const double thr = bin * (1.0 + 1e-6);
+  std::vector<std::pair<int, int>> near_v = near_pairs(y, m, thr);
+  const std::vector<std::pair<int, int>>& near = near_v;
   trace("  near pairs");
   // adjacency in CSR form
   std::vector<int> aoff(m + 1, 0), aidx(2 * near.size());
@@ -764,10 +761,9 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   kd_weighted(cen.data(), wt, 0, (int64_t)nitems, iperm, itiles, kTile, 0,
               host_threads() >= 8 ? 3 : host_threads() >= 4 ? 2 : 0);
   trace("  component k-d tiles");
-  std::vector<int> yidx;  // tile-order entry -> original reference index
-  std::vector<char> yfar;
-  struct GroupSpan { int start, count, gm; };
-  std::vector<GroupSpan> groups;
+  std::vector<int>& yidx = T->yidx;
+  std::vector<char>& yfar = T->yfar;
+  std::vector<GroupSpan>& groups = T->groups;
   for (const auto& t : itiles) {
     const int start = (int)yidx.size();
     for (int q = t.first; q < t.first + t.second; ++q)
@@ -777,11 +773,124 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       }
     groups.push_back({start, (int)yidx.size() - start, 1});
   }
+  const int64_t mp = (int64_t)yidx.size();
+  std::vector<int>& pos = T->pos;
+  pos.assign(m, 0);
+  for (int64_t q = 0; q < mp; ++q) pos[yidx[q]] = (int)q;
+  // ---- full dedup near lists (tile order, j' < j) for the exact path
+  trace("dedup near lists");
+  // CSR near lists in tile order: j' < j, sorted (the exact path's partners)
+  const int64_t npairs = (int64_t)near.size();
+  std::vector<int>& noff = T->noff;
+  std::vector<int>& nidx = T->nidx;
+  noff.assign(mp + 1, 0);
+  nidx.assign((size_t)npairs, 0);
+  for (const auto& e : near) ++noff[std::max(pos[e.first], pos[e.second]) + 1];
+  for (int64_t q = 0; q < mp; ++q) noff[q + 1] += noff[q];
+  {
+    std::vector<int> fill(noff.begin(), noff.end() - 1);
+    for (const auto& e : near) {
+      const int a = pos[e.first], b = pos[e.second];
+      nidx[fill[std::max(a, b)]++] = std::min(a, b);
+    }
+    for (int64_t q = 0; q < mp; ++q)
+      if (noff[q + 1] - noff[q] > 1) std::sort(nidx.begin() + noff[q], nidx.begin() + noff[q + 1]);
+  }
+  T->aoff = std::move(aoff);
+  T->aidx = std::move(aidx);
+  T->near = std::move(near_v);
+  T->ys.resize(3 * mp);
+  for (int64_t q = 0; q < mp; ++q)
+    for (int k = 0; k < 3; ++k) T->ys[3 * q + k] = y[3 * yidx[q] + k];
+  scoring.get();
+  return T;
+}
+
+static std::shared_ptr<const RefTopo> ref_topo(const double* y, int64_t m, double bin) {
+  static std::mutex mu;
+  static std::vector<std::shared_ptr<const RefTopo>> cache;  // most recent last
+  constexpr size_t kKeep = 4;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (size_t k = cache.size(); k-- > 0;) {
+      const auto& c = cache[k];
+      if (c->m == m && c->bin == bin && std::memcmp(c->y.data(), y, sizeof(double) * 3 * m) == 0) {
+        auto hit = c;
+        cache.erase(cache.begin() + (ptrdiff_t)k);
+        cache.push_back(hit);
+        trace("reference topology: cached");
+        return hit;
+      }
+    }
+  }
+  auto T = build_ref_topo(y, m, bin);
+  std::lock_guard<std::mutex> lk(mu);
+  cache.push_back(T);
+  if (cache.size() > kKeep) cache.erase(cache.begin());
+  return T;
+}
+
+int build_plan(dses_plan* P, const double* x, const double* y) {
+  const int64_t n = P->n, m = P->m;
+  cudaStream_t st = upload_stream(P->device);
+  // ---- fixed-point scale
+  trace("fixed-point scale");
+  double ymax = 0, xnorm = 0;
+  for (int64_t j = 0; j < m; ++j)
+    for (int k = 0; k < 3; ++k) ymax = std::max(ymax, std::fabs(y[3 * j + k]));
+  for (int64_t i = 0; i < n; ++i)
+    xnorm = std::max(xnorm, std::sqrt(x[3 * i] * x[3 * i] + x[3 * i + 1] * x[3 * i + 1] +
+                                      x[3 * i + 2] * x[3 * i + 2]));
+  double lomax = 0;
+  for (int k = 0; k < 3; ++k)
+    lomax = std::max(lomax, std::max(std::fabs((double)P->ilo[k]),
+                                     std::fabs((double)(P->ilo[k] + P->dims[k]))));
+  const double A = ymax * P->inv_bin + 3.0 * xnorm * P->inv_bin + lomax + 8.0;
+  int F = 0;
+  if (std::isfinite(A) && A > 0) F = (int)std::floor(std::log2(std::ldexp(1.0, 29) / A));
+  F = std::min(F, 20);
+  if (F < 6) F = 0;  // exact mode: every pair re-binned in binary64
+  P->F = F;
+  const double S = std::ldexp(1.0, F);
+  P->by = ymax;
+  double tmax = 0;
+  for (int k = 0; k < 3; ++k)
+    tmax = std::max(tmax, (std::fabs((double)P->ilo[k]) + (double)P->dims[k]) * P->bin);
+  P->bx = xnorm + tmax;
+
+  // ---- spatial tiles
+  trace("spatial tiles");
+  std::vector<int> px(n);
+  std::iota(px.begin(), px.end(), 0);
+  std::vector<std::pair<int, int>> tx;
+  kd_tiles(x, 0, n, px, tx, kTile, host_threads() >= 4 ? 2 : 0);  // source units
+  std::vector<double> xs(3 * n);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
+  const double inv_s = P->inv_bin * S;
+  // (the vote kernel bounds each unit by the exact box of its rotated
+  // fixed-point points, computed on the device per rotation)
+  std::vector<XTile> xt(tx.size());
+  for (size_t t = 0; t < tx.size(); ++t) {
+    XTile& T = xt[t];
+    T = XTile{};
+    T.start = tx[t].first;
+    T.count = tx[t].second;
+  }
+  // ---- reference topology (cached per reference cloud and bin size)
+  const std::shared_ptr<const RefTopo> topo = ref_topo(y, m, P->bin);
+  const std::vector<int>& yidx = topo->yidx;
+  const std::vector<char>& yfar = topo->yfar;
+  const std::vector<GroupSpan>& groups = topo->groups;
+  const std::vector<int>& aoff = topo->aoff;
+  const std::vector<int>& aidx = topo->aidx;
+  const std::vector<int>& pos = topo->pos;
+  for (int k = 0; k < 3; ++k) { P->gorg[k] = topo->gorg[k]; P->gdim[k] = topo->gdim[k]; }
+  P->gh = topo->gh;
+  P->g_pts_per_cell = topo->gppc;
   const int64_t mp = (int64_t)yidx.size();  // padded reference entries
   P->m_pad = mp;
-  std::vector<double> ys(3 * mp, 0.0);
-  for (int64_t q = 0; q < mp; ++q)
-    for (int k = 0; k < 3; ++k) ys[3 * q + k] = y[3 * yidx[q] + k];
+  const std::vector<double>& ys = topo->ys;
   // fixed-point reference: Yq = rint(fl(y*inv)*S) - lo*S + S/2 + G
   std::vector<int4> yq(mp);
   const int64_t Si = (int64_t)1 << F;
@@ -796,8 +905,6 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     }
     yq[q] = make_int4(v[0], v[1], v[2], 0);
   }
-  std::vector<int> pos(m);
-  for (int64_t q = 0; q < mp; ++q) pos[yidx[q]] = (int)q;
   std::vector<YTile> yt(groups.size());
   for (size_t t = 0; t < groups.size(); ++t) {
     YTile& T = yt[t];
@@ -891,45 +998,56 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   if (yt.size() >= 65536 || xt.size() >= 65536)  // (group << 16 | unit) work-unit encoding
     return fail(DSES_E_LIMIT, "cloud too large for the vote kernel: at most 65535 groups / units "
                 "of 32 points (about 2 million points) per cloud");
-  // ---- full dedup near lists (tile order, j' < j) for the exact path
-  trace("dedup near lists");
-  // CSR near lists in tile order: j' < j, sorted (the exact path's partners)
-  const int64_t npairs = (int64_t)near.size();
-  std::vector<int> noff(mp + 1, 0), nidx((size_t)npairs);
-  for (const auto& e : near) ++noff[std::max(pos[e.first], pos[e.second]) + 1];
-  for (int64_t q = 0; q < mp; ++q) noff[q + 1] += noff[q];
-  {
-    std::vector<int> fill(noff.begin(), noff.end() - 1);
-    for (const auto& e : near) {
-      const int a = pos[e.first], b = pos[e.second];
-      nidx[fill[std::max(a, b)]++] = std::min(a, b);
-    }
-    for (int64_t q = 0; q < mp; ++q)
-      if (noff[q + 1] - noff[q] > 1) std::sort(nidx.begin() + noff[q], nidx.begin() + noff[q + 1]);
-  }
-  P->near_pairs = npairs;
+  P->near_pairs = (int64_t)topo->near.size();
   std::vector<double> xv(x, x + 3 * n);
-  scoring.get();
   // ---- uploads
+  // the reference cloud's arrays: uploaded once per device, then borrowed
+  P->topo = topo;
+  {
+    std::lock_guard<std::mutex> lk(topo->dmu);
+    std::shared_ptr<DeviceRef>& d = topo->dev[P->device];
+    if (!d) {
+      auto nd = std::make_shared<DeviceRef>();
+      nd->device = P->device;
+      UploadPack rp;
+      static const std::vector<int> kOneZero(1, 0);
+      rp.add(nd->yorig, topo->y);
+      rp.add(nd->ys, topo->ys);
+      rp.add(nd->near_off, topo->noff);
+      rp.add(nd->near_idx, topo->nidx.empty() ? kOneZero : topo->nidx);
+      rp.add(nd->ys0, topo->c0);
+      rp.add(nd->ys1, topo->c1);
+      rp.add(nd->ys2, topo->c2);
+      rp.add(nd->ysf, topo->yf);
+      rp.add(nd->gcell, topo->range);
+      rp.add(nd->gpts, topo->gp);
+      CK(rp.commit(nd->arena, st));
+      CK(cudaStreamSynchronize(st));  // the staging buffer is reused below
+      d = nd;
+    }
+    P->dref = d;
+  }
+  {
+    const DeviceRef& d = *P->dref;
+    P->yorig.borrow(d.yorig.p, d.yorig.cap);
+    P->ys.borrow(d.ys.p, d.ys.cap);
+    P->near_off.borrow(d.near_off.p, d.near_off.cap);
+    P->near_idx.borrow(d.near_idx.p, d.near_idx.cap);
+    P->ys0.borrow(d.ys0.p, d.ys0.cap);
+    P->ys1.borrow(d.ys1.p, d.ys1.cap);
+    P->ys2.borrow(d.ys2.p, d.ys2.cap);
+    P->ysf.borrow(d.ysf.p, d.ysf.cap);
+    P->gcell.borrow(d.gcell.p, d.gcell.cap);
+    P->gpts.borrow(d.gpts.p, d.gpts.cap);
+  }
+  // the plan's own (source- and window-dependent) arrays
   UploadPack pack;
-  const std::vector<double> yv(y, y + 3 * m);
-  pack.add(P->yorig, yv);
   pack.add(P->xs, xs);
-  pack.add(P->ys, ys);
   pack.add(P->yq, yq);
-  pack.add(P->near_off, noff);
-  if (nidx.empty()) nidx.push_back(0);
-  pack.add(P->near_idx, nidx);
   pack.add(P->xt, xt);
   pack.add(P->yt, yt);
   pack.add(P->risk, risk);
   pack.add(P->x0, xv);
-  pack.add(P->ys0, c0);
-  pack.add(P->ys1, c1);
-  pack.add(P->ys2, c2);
-  pack.add(P->ysf, yf);
-  pack.add(P->gcell, range);
-  pack.add(P->gpts, gp);
   CK(pack.commit(P->arena, st));
   CK(P->stats.ensure(4 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(P->stats.p, 0, 4 * sizeof(unsigned long long), st));

@@ -44,11 +44,8 @@ constexpr int kVoteThreads = 1024;
 
 enum Metric { kL2 = 0, kL1 = 1, kTruncL1 = 2, kSatL0 = 3, kTruncL2 = 4 };
 
-struct XTile {          // spatial tile of the (sorted) source cloud
+struct XTile {          // spatial tile (source unit) of the (sorted) source cloud
   int start, count;
-  int rad;              // bounding-sphere radius in fixed-point units (+ rounding margin)
-  int pad;
-  double c[3];          // sphere centre (metres)
 };
 
 struct __align__(16) YTile {  // spatial tile of the (sorted) reference cloud; 3 x 16 bytes
