@@ -104,6 +104,10 @@ int dses_plan_destroy(dses_plan* plan);
 /* Fixed-point fraction bits chosen for the vote kernel (0 = exact fp64 mode). */
 int dses_plan_info(const dses_plan* plan, int64_t* frac_bits, int64_t* x_tiles, int64_t* y_tiles,
                    int64_t* near_pairs);
+/* Testing hook: run the vote kernel on at most `ctas` persistent CTAs
+ * (0 = the default, one wave of resident CTAs).  Results do not depend on it
+ * (tests/test_gpu_api.py checks 1, 7 and 148 CTAs against the default). */
+int dses_plan_set_vote_grid(dses_plan* plan, int64_t ctas);
 
 /* ---- the reference kernel seams ------------------------------------------ */
 /* Per-rotation histogram mode (count, flat bin, tied bins) for `nrot`

@@ -67,6 +67,7 @@ _SIGS = [
                                         _ip, _ip, ctypes.POINTER(_vp)]),
     ("dses_plan_destroy", ctypes.c_int, [_vp]),
     ("dses_plan_info", ctypes.c_int, [_vp, _ip, _ip, _ip, _ip]),
+    ("dses_plan_set_vote_grid", ctypes.c_int, [_vp, _i64]),
     ("dses_mode_batch", ctypes.c_int, [_vp, _dp, _i64, _ip, _ip, _ip, _vp]),
     ("dses_mode_grid", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, _ip, _ip, _ip, _vp]),
     ("dses_refine_batch", ctypes.c_int, [_vp, _dp, _dp, _i64, ctypes.c_int, ctypes.c_double, _dp,
@@ -273,6 +274,10 @@ class Plan:
         check(self._L.dses_plan_info(self._h, *[ctypes.byref(a) for a in v]), "dses_plan_info")
         return {"frac_bits": v[0].value, "x_tiles": v[1].value, "y_tiles": v[2].value,
                 "near_pairs": v[3].value}
+
+    def set_vote_grid(self, ctas):
+        """Testing hook: cap the vote kernel's persistent grid (0 = default)."""
+        check(self._L.dses_plan_set_vote_grid(self._h, int(ctas)), "dses_plan_set_vote_grid")
 
     def mode_batch(self, rots, stream=None):
         rots = np.ascontiguousarray(rots, dtype=np.float64).reshape(-1, 9)

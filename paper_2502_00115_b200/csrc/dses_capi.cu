@@ -272,6 +272,7 @@ struct dses_plan {
   VoteParams vp{};
   bool hsmem = true, psmem = true;
   int vote_grid = 0, vote_threads = kVoteThreads;
+  int vote_grid_cap = 0;                               // testing hook: 0 = one wave
   // device data
   DevBuf xs, ys, yq, near_off, near_idx, xt, yt;  // vote (tile order)
   DevBuf risk;                                         // vote: guard-band risk bitmaps per group
@@ -1203,7 +1204,7 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
   P->cur_r_count = r_count;
   P->cur_rot = rs;
   if (r_count <= 0) return DSES_OK;
-  int grid = (int)std::min<int64_t>(P->vote_grid, r_count);
+  int grid = (int)std::min<int64_t>(P->vote_grid_cap > 0 ? P->vote_grid_cap : P->vote_grid, r_count);
   // global-memory fallbacks: one slab per CTA, at most ~4 GiB in total
   const size_t per_cta = (P->hsmem ? 0 : (size_t)v.hist_words * 4) + (P->psmem ? 0 : (size_t)v.n_pad * 16);
   if (per_cta) {
@@ -1339,6 +1340,13 @@ extern "C" int dses_plan_info(const dses_plan* P, int64_t* frac_bits, int64_t* x
   if (x_tiles) *x_tiles = P->vp.nxt;
   if (y_tiles) *y_tiles = P->vp.nyt;
   if (near_pairs) *near_pairs = P->near_pairs;
+  return DSES_OK;
+}
+
+extern "C" int dses_plan_set_vote_grid(dses_plan* P, int64_t ctas) {
+  if (!P) return fail(DSES_E_INVALID, "null plan");
+  if (ctas < 0) return fail(DSES_E_INVALID, "negative CTA count");
+  P->vote_grid_cap = (int)std::min<int64_t>(ctas, P->vote_grid);
   return DSES_OK;
 }
 

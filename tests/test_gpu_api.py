@@ -225,6 +225,47 @@ def test_sharded_slices_equal_whole_grid_and_runs_repeat():
     assert whole[0].max() > 0
 
 
+@pytest.mark.parametrize("name,nrot", [("c2", 3000), ("c4", 600), ("big", 40)])
+def test_votes_invariant_to_cta_count_and_stream(name, nrot):
+    """The persistent vote kernel's result does not depend on how many CTAs
+    share the rotation queue or on the stream (the reference's determinism
+    across thread counts, test_acceptance.py:287-318): 1, 7 and 148 CTAs and
+    a private stream against the default one-wave launch.  c2 = shared-memory
+    histogram with guard-band risk bitmaps, c4 = overflow-tolerant rounds,
+    big = global-memory histograms."""
+    from paper_2502_00115_b200 import _native
+    from paper_2502_00115_b200.engines import prepare
+    import bench
+    if name == "big":
+        rng = np.random.default_rng(21)
+        x, y = rng.normal(size=(300, 3)), rng.normal(size=(400, 3))
+        b, ilo, dims = 0.02, np.full(3, -100), np.full(3, 201)
+        rots = _rots(nrot, 21)
+        run = lambda plan, st=None: plan.mode_batch(rots, st)  # noqa: E731
+    else:
+        cfg = bench.search_config(bench.workload(name))
+        (x0, y0, _), = bench.bench_pairs(name, 1)[0]
+        prep = prepare(x0, y0, cfg)
+        grid = _native.make_grid(cfg.k_rot, prep.cos_tab, prep.sin_tab, prep.center_rot)
+        x, y, b, ilo, dims = prep.x, prep.y, cfg.trans_bin, prep.ilo, prep.dims
+        r0 = cfg.rotation_count // 3
+        run = lambda plan, st=None: plan.mode_grid(grid, r0, nrot, st)  # noqa: E731
+    with _native.Plan(x, y, b, ilo, dims) as plan:
+        ref = run(plan)
+        assert ref[0].max() > 0
+        for ctas in (1, 7, 148):
+            plan.set_vote_grid(ctas)
+            got = run(plan)
+            assert all(np.array_equal(a, g) for a, g in zip(ref, got)), ctas
+        plan.set_vote_grid(0)
+        st = _native.Stream(0)
+        try:
+            got = run(plan, st.handle)
+        finally:
+            st.close()
+        assert all(np.array_equal(a, g) for a, g in zip(ref, got))
+
+
 @pytest.mark.parametrize("kind,param", [("trunc_l2", 0.1), ("l2", None), ("l1", None),
                                         ("trunc_l1", 0.06)])
 def test_dses_every_metric_matches_oracle(api, kind, param):
