@@ -68,6 +68,7 @@ _SIGS = [
     ("dses_plan_destroy", ctypes.c_int, [_vp]),
     ("dses_plan_info", ctypes.c_int, [_vp, _ip, _ip, _ip, _ip]),
     ("dses_plan_set_vote_grid", ctypes.c_int, [_vp, _i64]),
+    ("dses_plan_set_block_rotations", ctypes.c_int, [_vp, _i64, _i64]),
     ("dses_mode_batch", ctypes.c_int, [_vp, _dp, _i64, _ip, _ip, _ip, _vp]),
     ("dses_mode_grid", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, _ip, _ip, _ip, _vp]),
     ("dses_refine_batch", ctypes.c_int, [_vp, _dp, _dp, _i64, ctypes.c_int, ctypes.c_double, _dp,
@@ -278,6 +279,13 @@ class Plan:
     def set_vote_grid(self, ctas):
         """Testing hook: cap the vote kernel's persistent grid (0 = default)."""
         check(self._L.dses_plan_set_vote_grid(self._h, int(ctas)), "dses_plan_set_vote_grid")
+
+    def set_block_rotations(self, n, list_cap=0):
+        """Rotation-block length of the vote (0 = the per-rotation kernel) and
+        the list entries per CTA (0 = default; testing hook for the overflow
+        path)."""
+        check(self._L.dses_plan_set_block_rotations(self._h, int(n), int(list_cap)),
+              "dses_plan_set_block_rotations")
 
     def mode_batch(self, rots, stream=None):
         rots = np.ascontiguousarray(rots, dtype=np.float64).reshape(-1, 9)

@@ -35,6 +35,8 @@ cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, i
 int vote_max_ctas_per_sm(const VoteParams& p, bool hsmem, bool psmem, int threads);
 size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads);
 size_t vote_static_smem();
+cudaError_t launch_vote_blocks(const VoteParams& p, int grid, int threads, cudaStream_t stream);
+cudaError_t launch_vote_redo(const VoteParams& p, int grid, int threads, cudaStream_t stream);
 // dses_sparse.cu
 size_t sparse_scratch_bytes(int64_t n, int64_t m);
 cudaError_t launch_sparse_modes(const SparseParams& s, int64_t r_begin, int64_t r_count,
@@ -273,6 +275,9 @@ struct dses_plan {
   bool hsmem = true, psmem = true;
   int vote_grid = 0, vote_threads = kVoteThreads;
   int vote_grid_cap = 0;                               // testing hook: 0 = one wave
+  int blk_L = 0;                                       // rotation-block length (0: per-rotation kernel)
+  int blk_cap = kBlockListCap;                         // list entries per CTA (testing hook)
+  DevBuf blist, redo;                                  // block kernel: candidate lists, redo rotations
   // device data
   DevBuf xs, ys, yq, near_off, near_idx, xt, yt;  // vote (tile order)
   DevBuf risk;                                         // vote: guard-band risk bitmaps per group
@@ -595,6 +600,7 @@ struct RefTopo {
   std::vector<int> aoff, aidx;                 // their adjacency (CSR, original indices)
   std::vector<int> yidx;                       // tile-order entry -> original index
   std::vector<char> yfar;                      // component too large for a warp
+  std::vector<int> ycomp;                      // tile-order entry of its component's first point
   std::vector<GroupSpan> groups;
   std::vector<int> pos;                        // original index -> tile-order entry
   std::vector<int> noff, nidx;                 // exact-path near lists (tile order, j' < j)
@@ -765,13 +771,17 @@ static std::shared_ptr<const RefTopo> build_ref_topo(const double* y, int64_t m,
   std::vector<int>& yidx = T->yidx;
   std::vector<char>& yfar = T->yfar;
   std::vector<GroupSpan>& groups = T->groups;
+  std::vector<int>& ycomp = T->ycomp;
   for (const auto& t : itiles) {
     const int start = (int)yidx.size();
-    for (int q = t.first; q < t.first + t.second; ++q)
+    for (int q = t.first; q < t.first + t.second; ++q) {
+      const int cfirst = (int)yidx.size();
       for (int a = ioff[iperm[q]]; a < ioff[iperm[q] + 1]; ++a) {
         yidx.push_back(ipts[a]);
         yfar.push_back(item_far[iperm[q]]);
+        ycomp.push_back(cfirst);
       }
+    }
     groups.push_back({start, (int)yidx.size() - start, 1});
   }
   const int64_t mp = (int64_t)yidx.size();
@@ -958,6 +968,17 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       }
     }
   }
+  // ---- rotation-block kernel metadata in Yq.w (bits above the shuffle
+  // partner lanes): "has a dedup partner", "component split over groups",
+  // the point's offset from its dedup component's first point (tile order)
+  {
+    const std::vector<int>& ycomp = topo->ycomp;
+    for (const YTile& T : yt)
+      for (int q = T.start; q < T.start + T.count; ++q) {
+        yq[q].w |= (aoff[yidx[q] + 1] > aoff[yidx[q]] ? kPartFlag : 0) |
+                   (yfar[q] ? kSplitFlag : 0) | (std::min(15, q - ycomp[q]) << kCompOffShift);
+      }
+  }
   // ---- guard-band risk bitmaps: per group and axis, which fraction buckets of
   // a source's rotated coordinate can put some point of the group within the
   // guard band of a bin edge.  A pair is "near" iff frac(Yq - Pq) < 2G, i.e.
@@ -1044,6 +1065,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   // the plan's own (source- and window-dependent) arrays
   UploadPack pack;
   pack.add(P->xs, xs);
+  yq.push_back(make_int4(kNoRef, 0, 0, 0));  // the block kernel's empty sentinel slot (j = m_pad)
   pack.add(P->yq, yq);
   pack.add(P->xt, xt);
   pack.add(P->yt, yt);
@@ -1081,6 +1103,37 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.risk_shift = risk_on ? F - kRiskBits : 0;
   v.gthr = F ? 2u * kGuard : 0xffffffffu;
   v.stats = P->stats.as<unsigned long long>();
+  v.redo = nullptr;
+  v.redo_n = nullptr;
+  v.blk_L = 0;
+  {  // rotation-block kernel: entry encoding and the sources' extent per axis
+    int jb = 1;
+    while (jb < 31 && ((int64_t)1 << jb) <= P->m_pad) ++jb;  // j <= m_pad (sentinel)
+    v.jbits = (((uint64_t)std::max<int64_t>(n - 1, 0) << jb) >> 32) == 0 ? jb : 0;
+    for (int k = 0; k < 3; ++k) {
+      double a = 0;
+      for (int64_t i = 0; i < n; ++i) a = std::max(a, std::fabs(xs[3 * i + k]));
+      v.xa_s[k] = a * inv_s;
+    }
+    static const int envL = [] {
+      const char* e = getenv("DSES_BLOCK_L");
+      return e && *e ? std::max(0, std::min(kMaxBlockRot, atoi(e))) : -1;
+    }();
+    // Rotation blocks pay off when a source point's window holds few of a
+    // reference group's points (the per-rotation kernel then idles most lanes
+    // of its (source, group) steps): windows small against the reference
+    // cloud (c4: 36 mm in a 1.4 m cloud -> 1.7x).  With windows comparable to
+    // the cloud (c1-c3, c5) most lanes vote and the per-rotation kernel is
+    // faster (c2: 10.1 vs 18 ms with blocks).
+    double ext = 0, win = 0;
+    for (int k = 0; k < 3; ++k) {
+      double lo = INFINITY, hi = -INFINITY;
+      for (int64_t j = 0; j < m; ++j) { lo = std::min(lo, y[3 * j + k]); hi = std::max(hi, y[3 * j + k]); }
+      ext = std::max(ext, hi - lo);
+      win = std::max(win, (double)P->dims[k] * P->bin);
+    }
+    P->blk_L = envL >= 0 ? envL : (win < kBlockWindowFrac * ext ? kDefaultBlockL : 0);
+  }
   v.count16 = n < 65536 ? 1 : 0;
   const int64_t words = v.count16 ? (v.nbins + 1) / 2 : v.nbins;
   v.hist_words = (int)((words + 3) / 4 * 4);
@@ -1188,6 +1241,13 @@ int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_cou
   return DSES_OK;
 }
 
+// Rotation-block kernel eligibility: grid rotations (blocks are runs of one
+// grid row), shared-memory histogram and points, fixed-point binning, and
+// list entries i << jbits | j in 32 bits.
+static bool use_blocks(const dses_plan* P, const RotSource& rs) {
+  return P->blk_L > 0 && rs.cth && !rs.rots && P->hsmem && P->psmem && P->F > 0 && P->vp.jbits > 0;
+}
+
 int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
   if (P->sparse) return run_sparse(P, rs, r_begin, r_count, st);
   CK(P->counts.ensure(sizeof(int) * std::max<int64_t>(r_count, 1), st));
@@ -1221,7 +1281,23 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
   }
   CK(cudaEventRecord(P->ev[5], st));
   CK(cudaMemsetAsync(v.stats + 3, 0, sizeof(unsigned long long), st));  // rotation queue
-  CK(launched(launch_vote(v, P->hsmem, P->psmem, grid, P->vote_threads, st)));
+  if (use_blocks(P, rs)) {
+    // rotation blocks: one candidate list per run of blk_L rotations; blocks
+    // whose list overflows the slab are re-run by the per-rotation kernel
+    v.blk_L = P->blk_L;
+    v.list_cap = P->blk_cap;
+    CK(P->blist.ensure((size_t)grid * v.list_cap * 4, st));
+    CK(P->redo.ensure(8 * (size_t)(r_count + 1), st));
+    v.list = P->blist.as<unsigned>();
+    v.redo_n = P->redo.as<unsigned long long>();
+    v.redo = P->redo.as<long long>() + 1;
+    CK(cudaMemsetAsync(v.redo_n, 0, 8, st));
+    CK(launched(launch_vote_blocks(v, grid, P->vote_threads, st)));
+    CK(cudaMemsetAsync(v.stats + 3, 0, sizeof(unsigned long long), st));
+    CK(launched(launch_vote_redo(v, grid, P->vote_threads, st)));
+  } else {
+    CK(launched(launch_vote(v, P->hsmem, P->psmem, grid, P->vote_threads, st)));
+  }
   CK(cudaEventRecord(P->ev[6], st));
   P->vote_timed = true;
   return DSES_OK;
@@ -1347,6 +1423,15 @@ extern "C" int dses_plan_set_vote_grid(dses_plan* P, int64_t ctas) {
   if (!P) return fail(DSES_E_INVALID, "null plan");
   if (ctas < 0) return fail(DSES_E_INVALID, "negative CTA count");
   P->vote_grid_cap = (int)std::min<int64_t>(ctas, P->vote_grid);
+  return DSES_OK;
+}
+
+extern "C" int dses_plan_set_block_rotations(dses_plan* P, int64_t len, int64_t list_cap) {
+  if (!P) return fail(DSES_E_INVALID, "null plan");
+  if (len < 0 || len > kMaxBlockRot) return fail(DSES_E_INVALID, "block length must be in [0, %d]", kMaxBlockRot);
+  if (list_cap < 0 || list_cap > kBlockListCap) return fail(DSES_E_INVALID, "list capacity must be in [0, %d]", kBlockListCap);
+  P->blk_L = (int)len;
+  P->blk_cap = list_cap > 0 ? (int)((list_cap + 31) / 32 * 32) : kBlockListCap;
   return DSES_OK;
 }
 

@@ -38,6 +38,15 @@ constexpr int kDenseMaxBins = 1 << 26;  // beyond: sort-based (sparse) mode quer
 constexpr int kNoRef = -3 * (1 << 29);
 constexpr int kMaxComp = 16;     // dedup components up to this size stay in one warp
 constexpr int kFarFlag = 1 << 12; // Yq.w: the point's dedup needs the exact path
+// Yq.w bits read by the rotation-block kernel (vote_blocks_kernel):
+constexpr int kPartFlag = 1 << 18;   // the point has a dedup partner
+constexpr int kSplitFlag = 1 << 19;  // its component spans several groups (always exact)
+constexpr int kCompOffShift = 20;    // bits 20..23: its offset from the component's first point
+                                     // (components are contiguous in tile order)
+constexpr int kMaxBlockRot = 8;   // rotations per block (the block kernel's R area in shared memory)
+constexpr int kDefaultBlockL = 5; // rotations per block unless DSES_BLOCK_L says otherwise
+constexpr double kBlockWindowFrac = 0.15;  // blocks when the window is below this part of the cloud
+constexpr int kBlockListCap = 1 << 18;  // candidate-list entries per CTA (1 MiB)
 constexpr int kRiskBits = 10;     // fraction buckets per axis of the guard-band risk bitmaps
 constexpr int kRiskWords = 3 * (1 << kRiskBits) / 32;  // words per group (3 axes)
 constexpr int kVoteThreads = 1024;
@@ -116,6 +125,16 @@ struct VoteParams {
   int hist_words;             // u32 words per histogram (padded to a multiple of 4)
   int n_pad;
   int count16;                // two 16-bit counts per word (n < 65536)
+  // rotation blocks (vote_blocks_kernel): runs of blk_L consecutive rotations
+  // of a grid row share one candidate-pair list built at the block's centre
+  // rotation with the window widened by the block's maximal point motion
+  int blk_L;                  // 0: per-rotation kernel only
+  int jbits;                  // list entry = i << jbits | j; j = m_pad is the empty sentinel slot
+  int list_cap;               // entries per CTA slab (multiple of 32)
+  unsigned* list;             // per-CTA slabs
+  double xa_s[3];             // max_i |x_i| per axis in fixed-point units (x * inv_s)
+  long long* redo;            // rotations of blocks whose list overflowed ...
+  unsigned long long* redo_n; // ... and their number: vote_kernel runs them (redo mode)
 };
 
 struct ScoreParams {     // scoring kernels (dses_score.cu)

@@ -313,7 +313,9 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
 }
 
 // RISK: guard-band risk bitmaps in use (small reference clouds; dses_capi.cu)
-template <bool HSMEM, bool PSMEM, bool RISK>
+// REDO: the rotations come from a device-side list (redo / redo_n): those of
+// rotation blocks whose candidate list overflowed (vote_blocks_kernel)
+template <bool HSMEM, bool PSMEM, bool RISK, bool REDO = false>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   int4* CB = XB + 2 * p.nxt;                       // [2*nxc] their union per chunk
   off += (size_t)(p.nxt + nxc) * 32;
   double* R = reinterpret_cast<double*>(smem + off);
-  off += 16 * 8;
+  off += kMaxBlockRot * 9 * 8;                     // (the block kernel's layout: same offsets)
   int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + counters
   off += 4 * 32 * 4;
   unsigned* units = reinterpret_cast<unsigned*>(smem + off);  // [unit_cap] (group << 16 | unit)
@@ -394,8 +396,9 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   // rotations: the first one static, the rest from a global queue (the cost
   // of a rotation varies with its angle; dynamic claims balance the tail)
   __shared__ long long s_rr;
-  for (int64_t rr = blockIdx.x; rr < p.r_count;) {
-    const int64_t r = p.r_begin + rr;
+  const int64_t r_count = REDO ? (int64_t)*p.redo_n : p.r_count;
+  for (int64_t rr = blockIdx.x; rr < r_count;) {
+    const int64_t r = REDO ? p.redo[rr] : p.r_begin + rr;
     if (tid < 9) R[tid] = rotation_entry(p.rot, r, tid);
     __syncthreads();
 
@@ -705,9 +708,10 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
         bties += __shfl_xor_sync(0xffffffffu, bties, o);
       }
       if (lane == 0) {
-        p.counts[rr] = best;
-        p.lins[rr] = best > 0 ? blin : -1;
-        p.ties[rr] = best > 0 ? bties : 0;
+        const int64_t ro = REDO ? r - p.r_begin : rr;
+        p.counts[ro] = best;
+        p.lins[ro] = best > 0 ? blin : -1;
+        p.ties[ro] = best > 0 ? bties : 0;
         s_rr = (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull);
       }
     }
@@ -730,11 +734,449 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   }
 }
 
+// ===========================================================================
+// Rotation-block kernel.  A block is a run of up to kMaxBlockRot consecutive
+// rotations of one grid row (the innermost Euler axis).  Every rotation R of
+// the block moves a source point by at most
+//     |(R - Rc) x|_k <= sum_l |R_kl - Rc_kl| * max_i |x_il|
+// from its position under the block's centre rotation Rc, so the pairs that
+// can vote for ANY rotation of the block are among the pairs inside the
+// window widened by that bound (dq fixed-point units per axis, with margin
+// for the two roundings) at Rc.  The kernel
+//   1. builds that candidate-pair list ONCE per block: the per-rotation
+//      kernel's culling (unit boxes, group boxes, per-source tests) with the
+//      widened window, then one ballot per (source, group) and the candidate
+//      lanes appended as entries i << jbits | j;
+//   2. votes it for each rotation of the block: lane = one entry (no idle
+//      lanes on out-of-window reference points), the same fixed-point bin
+//      and guard band as the per-rotation kernel, and the per-source dedup by
+//      __match_any_sync on (i, bin) within the 32-entry segment.
+// Exact dedup needs every pair that can share (i, bin) -- dedup partners, i.e.
+// points of one component -- in the same segment: a (source, group) run's
+// entries never straddle a segment boundary (the rest of the segment is
+// padded with the empty sentinel entry).  A segment holding a guard-band ("near") or
+// split-component pair sends all its partnered pairs through the exact
+// binary64 path (vote_exact: the reference's rule over the full near list).
+// A block whose list exceeds the CTA's slab is left to vote_kernel (redo
+// list).  Counts, bins and ties are those of the per-rotation kernel.
+
+// Widened window test of a source box [lo, hi] against a group box:
+// Yq - Pq in [-dq, W + dq) possible on every axis (wq = W + dq)?
+__device__ __forceinline__ bool boxes_meet_w(const YTile& yt, const int4& lo, const int4& hi,
+                                             int dq0, int dq1, int dq2, int wq0, int wq1, int wq2) {
+  return (yt.hi[0] - lo.x >= -dq0) & (yt.lo[0] - hi.x < wq0) & (yt.hi[1] - lo.y >= -dq1) &
+         (yt.lo[1] - hi.y < wq1) & (yt.hi[2] - lo.z >= -dq2) & (yt.lo[2] - hi.z < wq2);
+}
+
+// Append the set lanes of m (entry `entry` each, in lane order) to the warp's
+// open list segment.  One (source, group) run never straddles two segments
+// (so neither does a dedup component): a run that does not fit the open
+// segment's room closes it (the rest padded with the empty sentinel entry).
+// seg / fill: the warp's open segment (entry offset in p.list; fill == 32:
+// none).  Returns false once the CTA's slab is full.
+__device__ __forceinline__ bool emit_entries(const VoteParams& p, unsigned m, unsigned entry, int lane,
+                                             unsigned lanemask_lt, uint32_t nseg_sh, unsigned slab,
+                                             unsigned pad_entry, unsigned& seg, int& fill,
+                                             unsigned& wcount) {
+  const int cnt = __popc(m);
+  wcount += (unsigned)cnt;
+  if (cnt > 32 - fill) {  // warp-uniform
+    if (lane >= fill) __stcg(p.list + (seg + (unsigned)lane), pad_entry);
+    unsigned s = 0;
+    if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(s) : "r"(nseg_sh) : "memory");
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (32u * (s + 1u) > (unsigned)p.list_cap) { fill = 32; return false; }
+    seg = slab + 32u * s;
+    fill = 0;
+  }
+  if ((m >> lane) & 1u) __stcg(p.list + (seg + (unsigned)fill + (unsigned)__popc(m & lanemask_lt)), entry);
+  fill += cnt;
+  return true;
+}
+
+#ifndef DSES_BLOCK_THREADS
+#define DSES_BLOCK_THREADS kVoteThreads
+#endif
+__global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(const VoteParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nthreads = blockDim.x, nwarps = nthreads >> 5, warp = tid >> 5;
+
+  // the per-rotation kernel's layout (hsmem, psmem)
+  size_t off = 0;
+  unsigned* hist = reinterpret_cast<unsigned*>(smem);
+  off += (size_t)p.hist_words * 4;
+  int4* P = reinterpret_cast<int4*>(smem + off);
+  off += (size_t)p.n_pad * 16;
+  const int nxc = (p.nxt + 31) >> 5;
+  int4* XB = reinterpret_cast<int4*>(smem + off);
+  int4* CB = XB + 2 * p.nxt;
+  off += (size_t)(p.nxt + nxc) * 32;
+  double* Rb = reinterpret_cast<double*>(smem + off);  // [kMaxBlockRot][9]
+  off += kMaxBlockRot * 9 * 8;
+  int* red = reinterpret_cast<int*>(smem + off);
+  off += 4 * 32 * 4;
+  unsigned* units = reinterpret_cast<unsigned*>(smem + off);
+  off += (size_t)p.unit_cap * 4;
+  int2* rare = reinterpret_cast<int2*>(smem + off) + warp * kRare;
+  off += (size_t)nwarps * kRare * 8;
+  int4* stage = reinterpret_cast<int4*>(smem + off) + warp * 32;
+  const uint32_t stage_sh = (uint32_t)__cvta_generic_to_shared(stage);
+
+  int* s_nunits = red + 96;
+  int* s_next = red + 97;
+  int* s_ovf = red + 98;
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+  const uint32_t P_sh = (uint32_t)__cvta_generic_to_shared(P);
+  __shared__ __align__(16) unsigned kc[12];
+  __shared__ int s_dq[3];
+  __shared__ int s_nseg;
+  __shared__ int s_lovf;
+  __shared__ long long s_bb;
+  if (tid == 0) {
+    kc[0] = p.W0; kc[1] = p.W1; kc[2] = p.W2; kc[3] = p.fmask; kc[4] = p.gthr;
+    kc[5] = (unsigned)p.d1; kc[6] = (unsigned)p.d2; kc[7] = (unsigned)p.F;
+    kc[8] = (uint32_t)__cvta_generic_to_shared(hist);
+    kc[9] = 0u - (1u << p.F);
+    kc[10] = kc[11] = 0u;
+    g_exR = Rb;
+    g_exP = P;
+    g_exH = hist;
+  }
+  __syncthreads();
+  const uint32_t hist_sh = kc[8];
+  unsigned long long st_pairs = 0, st_votes = 0;
+  Lane L;
+  asm volatile("mov.u32 %0, %1;" : "=r"(L.rare_sh) : "r"((uint32_t)__cvta_generic_to_shared(rare)));
+  L.nrare = 0;
+  L.rechecks = 0;
+
+  uint4* hist4 = reinterpret_cast<uint4*>(hist);
+  const int nw4 = p.hist_words >> 2;
+  for (int w = tid; w < nw4; w += nthreads) hist4[w] = make_uint4(0, 0, 0, 0);
+
+  const unsigned slab = (unsigned)blockIdx.x * (unsigned)p.list_cap;  // this CTA's list (entry offset)
+  const uint32_t nseg_sh = (uint32_t)__cvta_generic_to_shared(&s_nseg);
+  const unsigned jmask = (1u << p.jbits) - 1u;
+  const unsigned pad_entry = (unsigned)p.m_pad;  // i = 0, j = the empty sentinel slot
+  const int BL = p.blk_L;
+  const int64_t side = 2 * p.rot.k + 1;
+  const int64_t r_end = p.r_begin + p.r_count;
+  const int64_t row0 = p.r_begin / side;
+  const int64_t bpr = (side + BL - 1) / BL;
+  const int64_t nblk = ((r_end - 1) / side - row0 + 1) * bpr;
+  const int gmax = max(1, min(min(p.nyt, p.unit_cap / 4), p.unit_cap - p.nxt - 1));
+  const bool masks = nxc > 1 && nxc <= 32;
+
+  for (int64_t bb = blockIdx.x; bb < nblk;) {
+    const int64_t row = row0 + bb / bpr, c0 = (bb % bpr) * BL;
+    const int64_t lo = max(row * side + c0, p.r_begin);
+    const int64_t hi = min(row * side + min(side, c0 + (int64_t)BL), r_end);
+    const int nb = (int)max((int64_t)0, hi - lo);
+    if (nb > 0) {  // block-uniform
+      const int rc = nb >> 1;
+      if (tid < 9 * nb) Rb[tid] = rotation_entry(p.rot, lo + tid / 9, tid % 9);
+      if (tid == 0) { s_nseg = 0; s_lovf = 0; }
+      __syncthreads();
+      if (tid < 3) {  // widening of the window per axis
+        double d = 0.0;
+        for (int t = 0; t < nb; ++t) {
+          double s = 0.0;
+          for (int l = 0; l < 3; ++l) s += fabs(Rb[9 * t + 3 * tid + l] - Rb[9 * rc + 3 * tid + l]) * p.xa_s[l];
+          d = fmax(d, s);
+        }
+        // (a widening beyond 2^27 units -- huge steps -- leaves the block to vote_kernel)
+        s_dq[tid] = d < 134217728.0 ? (int)ceil(d * (1.0 + 1e-9)) + 3 : -1;
+      }
+      const double* R = Rb + 9 * rc;
+      // ---- A at the centre rotation: fixed-point points and unit boxes
+      for (int a = warp; a < p.nxt; a += nwarps) {
+        const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + a));
+        const bool valid = lane < U.y;
+        const int i = U.x + (valid ? lane : 0);
+        int4 v = make_int4(0, 0, 0, 0);
+        if (valid) {
+          const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
+          v.x = __double2int_rn(dmul(rot_row(R, 0, x0, x1, x2), p.inv_s));
+          v.y = __double2int_rn(dmul(rot_row(R, 1, x0, x1, x2), p.inv_s));
+          v.z = __double2int_rn(dmul(rot_row(R, 2, x0, x1, x2), p.inv_s));
+          P[i] = v;
+        }
+        const int4 blo = make_int4(__reduce_min_sync(0xffffffffu, valid ? v.x : INT_MAX),
+                                   __reduce_min_sync(0xffffffffu, valid ? v.y : INT_MAX),
+                                   __reduce_min_sync(0xffffffffu, valid ? v.z : INT_MAX), U.x);
+        const int4 bhi = make_int4(__reduce_max_sync(0xffffffffu, valid ? v.x : INT_MIN),
+                                   __reduce_max_sync(0xffffffffu, valid ? v.y : INT_MIN),
+                                   __reduce_max_sync(0xffffffffu, valid ? v.z : INT_MIN), U.x + U.y);
+        if (lane == 0) { XB[2 * a] = blo; XB[2 * a + 1] = bhi; }
+      }
+      __syncthreads();
+      for (int c = warp; c < nxc; c += nwarps) {
+        const int t = 32 * c + lane;
+        const bool valid = t < p.nxt;
+        int4 blo = valid ? XB[2 * t] : make_int4(INT_MAX, INT_MAX, INT_MAX, 0);
+        int4 bhi = valid ? XB[2 * t + 1] : make_int4(INT_MIN, INT_MIN, INT_MIN, 0);
+        blo.x = __reduce_min_sync(0xffffffffu, blo.x);
+        blo.y = __reduce_min_sync(0xffffffffu, blo.y);
+        blo.z = __reduce_min_sync(0xffffffffu, blo.z);
+        bhi.x = __reduce_max_sync(0xffffffffu, bhi.x);
+        bhi.y = __reduce_max_sync(0xffffffffu, bhi.y);
+        bhi.z = __reduce_max_sync(0xffffffffu, bhi.z);
+        if (lane == 0) { CB[2 * c] = blo; CB[2 * c + 1] = bhi; }
+      }
+      __syncthreads();
+      const int dq0 = s_dq[0], dq1 = s_dq[1], dq2 = s_dq[2];
+      const int wq0 = (int)p.W0 + dq0, wq1 = (int)p.W1 + dq1, wq2 = (int)p.W2 + dq2;
+      const unsigned Wp0 = p.W0 + 2u * (unsigned)dq0, Wp1 = p.W1 + 2u * (unsigned)dq1,
+                     Wp2 = p.W2 + 2u * (unsigned)dq2;
+
+      // ---- build the block's list (rounds of reference groups, as vote_kernel)
+      unsigned seg = 0;
+      int fill = 32;
+      const bool wide = (dq0 | dq1 | dq2) < 0;  // block-uniform
+      bool room = !wide;
+      unsigned wcount = 0;
+      for (int b0 = 0, gnext = gmax; b0 < (wide ? 0 : p.nyt);) {
+        const int b1 = min(p.nyt, b0 + gnext);
+        if (tid == 0) { *s_nunits = 0; *s_next = 0; *s_ovf = b1; }
+        const int cap_u = p.unit_cap - gmax;
+        unsigned* gmask = units + cap_u;
+        if (masks)
+          for (int k = tid; k < b1 - b0; k += nthreads) {
+            const YTile yg = load_ytile(p.yt, b0 + k);
+            unsigned mk = 0;
+            for (int c = 0; c < nxc; ++c)
+              if (boxes_meet_w(yg, CB[2 * c], CB[2 * c + 1], dq0, dq1, dq2, wq0, wq1, wq2)) mk |= 1u << c;
+            gmask[k] = mk;
+          }
+        __syncthreads();
+        for (int b = b0 + warp; b < b1; b += nwarps) {
+          const YTile yt = load_ytile(p.yt, b);
+          for (int a0 = 0; a0 < p.nxt; a0 += 32) {
+            if (masks ? !((gmask[b - b0] >> (a0 >> 5)) & 1u)
+                      : (nxc > 1 && !boxes_meet_w(yt, CB[2 * (a0 >> 5)], CB[2 * (a0 >> 5) + 1], dq0, dq1,
+                                                  dq2, wq0, wq1, wq2)))
+              continue;
+            const int a = a0 + lane;
+            const bool ov = a < p.nxt &&
+                            boxes_meet_w(yt, XB[2 * a], XB[2 * a + 1], dq0, dq1, dq2, wq0, wq1, wq2);
+            const unsigned m = __ballot_sync(0xffffffffu, ov);
+            if (m) {
+              int slot = 0;
+              if (lane == 0) {
+                slot = atomicAdd(s_nunits, __popc(m));
+                if (slot + __popc(m) > cap_u) atomicMin(s_ovf, b);
+              }
+              slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(m & lanemask_lt);
+              if (ov && slot < cap_u) units[slot] = ((unsigned)b << 16) | (unsigned)a;
+            }
+          }
+        }
+        __syncthreads();
+        const int nunits = min(*s_nunits, cap_u);
+        const unsigned ovf = (unsigned)*s_ovf;
+        for (int u = 0;; ++u) {
+          if (lane == 0) u = atomicAdd(s_next, 1);
+          u = __shfl_sync(0xffffffffu, u, 0);
+          if (u >= nunits) break;
+          const unsigned unit = units[u];
+          if ((unit >> 16) >= ovf) continue;  // warp-uniform
+          const YTile yt = load_ytile(p.yt, (int)(unit >> 16));
+          const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + (unit & 0xffffu)));
+          const bool valid = lane < yt.count;
+          const int j = yt.start + (valid ? lane : 0);
+          int4 Y = __ldg(&p.yq[j]);
+          if (!valid) Y = make_int4(kNoRef, 0, 0, 0);
+          const int y0 = (int)((unsigned)Y.x + (unsigned)dq0), y1 = (int)((unsigned)Y.y + (unsigned)dq1),
+                    y2 = (int)((unsigned)Y.z + (unsigned)dq2);
+          bool sok = false;
+          int4 Pl = make_int4(0, 0, 0, 0);
+          if (lane < U.y) {
+            Pl = lds_v4(P_sh + 16u * (unsigned)(U.x + lane));
+            sok = (yt.hi[0] - Pl.x >= -dq0) & (yt.lo[0] - Pl.x < wq0) & (yt.hi[1] - Pl.y >= -dq1) &
+                  (yt.lo[1] - Pl.y < wq1) & (yt.hi[2] - Pl.z >= -dq2) & (yt.lo[2] - Pl.z < wq2);
+          }
+          const unsigned sm = __ballot_sync(0xffffffffu, sok);
+          const int nsrc = __popc(sm);
+          __syncwarp();
+          if (sok) sts_v4(stage_sh + 16u * (unsigned)__popc(sm & lanemask_lt),
+                          make_int4(Pl.x, Pl.y, Pl.z, U.x + lane));
+          __syncwarp();
+          for (int t = 0; t < nsrc && room; ++t) {
+            const int4 Pi = lds_v4(stage_sh + 16u * (unsigned)t);
+            const bool c = ((unsigned)y0 - (unsigned)Pi.x < Wp0) & ((unsigned)y1 - (unsigned)Pi.y < Wp1) &
+                           ((unsigned)y2 - (unsigned)Pi.z < Wp2);
+            const unsigned m = __ballot_sync(0xffffffffu, c);
+            if (m)
+              room = emit_entries(p, m, ((unsigned)Pi.w << p.jbits) | (unsigned)j, lane, lanemask_lt,
+                                  nseg_sh, slab, pad_entry, seg, fill, wcount);
+          }
+        }
+        __syncthreads();
+        gnext = ((int)ovf == b0) ? 1 : gmax;
+        b0 = (int)ovf;
+      }
+      if (!room) {
+        if (lane == 0) s_lovf = 1;
+      } else if (fill < 32 && lane >= fill) {  // close the warp's open segment
+        __stcg(p.list + (seg + (unsigned)lane), pad_entry);
+      }
+      __syncthreads();
+      if (s_lovf) {  // left to vote_kernel
+        if (tid < nb) p.redo[atomicAdd(p.redo_n, 1ull)] = lo + tid;
+      } else {
+        const int nseg = s_nseg;
+        if (lane == 0) st_pairs += (unsigned long long)wcount * (unsigned long long)nb;
+        for (int t0 = 0; t0 < nb; ++t0) {
+          const int t = t0 == 0 ? rc : (t0 <= rc ? t0 - 1 : t0);  // the centre first: P holds it
+          const double* Rt = Rb + 9 * t;
+          if (t0 > 0) {
+            for (int i = tid; i < p.n; i += nthreads) {
+              const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
+              P[i] = make_int4(__double2int_rn(dmul(rot_row(Rt, 0, x0, x1, x2), p.inv_s)),
+                               __double2int_rn(dmul(rot_row(Rt, 1, x0, x1, x2), p.inv_s)),
+                               __double2int_rn(dmul(rot_row(Rt, 2, x0, x1, x2), p.inv_s)), 0);
+            }
+          }
+          if (tid == 0) g_exR = Rt;
+          __syncthreads();
+          // ---- vote the list: lane = one entry
+          FastK fk;
+          {
+            const uint4 k0 = *reinterpret_cast<const uint4*>(kc);
+            const uint4 k1 = *reinterpret_cast<const uint4*>(kc + 4);
+            fk.W0 = k0.x; fk.W1 = k0.y; fk.W2 = k0.z; fk.fmask = k0.w;
+            fk.gthr = k1.x; fk.d1 = k1.y; fk.d2 = k1.z; fk.F = (int)k1.w; fk.negP = kc[9];
+          }
+          // (the next segment's entry is loaded one iteration ahead: the list
+          // comes from L2)
+          unsigned e_next = warp < nseg ? __ldcg(p.list + (slab + 32u * (unsigned)warp + (unsigned)lane)) : pad_entry;
+          for (int sg = warp; sg < nseg; sg += nwarps) {
+            const unsigned e = e_next;
+            if (sg + nwarps < nseg)
+              e_next = __ldcg(p.list + (slab + 32u * (unsigned)(sg + nwarps) + (unsigned)lane));
+            const int i = (int)(e >> p.jbits), j = (int)(e & jmask);
+            const int4 Pi = lds_v4(P_sh + 16u * (unsigned)i);
+            const int4 Y = __ldg(&p.yq[j]);
+            const unsigned u0 = (unsigned)(Y.x - Pi.x), u1 = (unsigned)(Y.y - Pi.y), u2 = (unsigned)(Y.z - Pi.z);
+            const bool cand = (u0 < fk.W0) & (u1 < fk.W1) & (u2 < fk.W2);
+            const unsigned q0 = u0 >> fk.F, q1 = u1 >> fk.F, q2 = u2 >> fk.F;
+            const unsigned gthr = (Y.w & kSplitFlag) ? 0xffffffffu : fk.gthr;
+            const bool near = cand & (__vimin3_u32(u0 + q0 * fk.negP, u1 + q1 * fk.negP, u2 + q2 * fk.negP) < gthr);
+            const unsigned lin = (q0 * fk.d1 + q1) * fk.d2 + q2;
+            if (!__any_sync(0xffffffffu, near)) {
+              // every candidate decided: a (source, bin) votes once, by its lowest
+              // lane.  Lanes that can share it are entries of one component for
+              // one source: contiguous, the earlier ones at lane distance d <=
+              // off (the point's offset in its component), entry e - d' with
+              // 1 <= d' <= off
+              const int off = (Y.w >> kCompOffShift) & 15;
+              const int key = cand ? (int)lin : -1;
+              const int dmax = __reduce_max_sync(0xffffffffu, cand ? off : 0);
+              bool ok = cand;
+              for (int d = 1; d <= dmax; ++d) {
+                const unsigned e2 = __shfl_up_sync(0xffffffffu, e, d);
+                const int k2 = __shfl_up_sync(0xffffffffu, key, d);
+                ok &= !((e - e2 - 1u < (unsigned)off) & (k2 == key));
+              }
+              const uint32_t a = ok ? hist_sh + ((lin + lin) & ~3u) : g_dummy_sh + 4u * (unsigned)lane;
+              reds_add(a, __funnelshift_l(0u, 1u, lin << 4));
+            } else {
+              // a near / split pair in the segment: its partners' bins are not
+              // known exactly -- every partnered candidate takes the exact path
+              const bool def = near | (cand & ((Y.w & kPartFlag) != 0));
+              vote_if<true>(hist, hist_sh, lin, cand & !def, (unsigned)p.nbins);
+              const unsigned dm = __ballot_sync(0xffffffffu, def);
+              if (dm) defer_pairs<true, true>(p, hist_sh, L, dm, def, i, j, lane, lanemask_lt);
+            }
+          }
+          if (L.nrare > 0) {
+            L.rechecks += flush_rare<true, true>(p, Rt, P, hist, hist_sh, L.rare_sh, L.nrare, lane) & 0xffffu;
+            L.nrare = 0;
+          }
+          __syncthreads();
+          // ---- mode (vote_kernel's two passes)
+          unsigned mx = 0;
+          for (int w = tid; w < nw4; w += nthreads) {
+            const uint4 v = hist4[w];
+            st_votes += ((v.x * 0x10001u) >> 16) + ((v.y * 0x10001u) >> 16) + ((v.z * 0x10001u) >> 16) +
+                        ((v.w * 0x10001u) >> 16);
+            mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w)));
+          }
+          mx = max(mx & 0xffffu, mx >> 16);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          if (lane == 0) red[warp] = (int)mx;
+          __syncthreads();
+          int M = 0;
+          for (int w = 0; w < nwarps; ++w) M = max(M, red[w]);
+          __syncthreads();
+          int blin = INT_MAX, bties = 0;
+          const unsigned MM = (unsigned)M * 0x10001u;
+          for (int w = tid; w < nw4; w += nthreads) {
+            const uint4 v = hist4[w];
+            if ((v.x | v.y | v.z | v.w) == 0u) continue;
+            hist4[w] = make_uint4(0, 0, 0, 0);
+            if (M == 0) continue;
+            const unsigned z = __vminu2(__vminu2(v.x ^ MM, v.y ^ MM), __vminu2(v.z ^ MM, v.w ^ MM));
+            if ((z & 0xffffu) != 0u && (z >> 16) != 0u) continue;
+            const unsigned vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+              const int c = (int)((vv[h >> 1] >> ((h & 1) * 16)) & 0xffffu);
+              if (c == M) { blin = min(blin, 8 * w + h); ++bties; }
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            blin = min(blin, __shfl_xor_sync(0xffffffffu, blin, o));
+            bties += __shfl_xor_sync(0xffffffffu, bties, o);
+          }
+          if (lane == 0) { red[32 + warp] = blin; red[64 + warp] = bties; }
+          __syncthreads();
+          if (warp == 0) {
+            blin = lane < nwarps ? red[32 + lane] : INT_MAX;
+            bties = lane < nwarps ? red[64 + lane] : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              blin = min(blin, __shfl_xor_sync(0xffffffffu, blin, o));
+              bties += __shfl_xor_sync(0xffffffffu, bties, o);
+            }
+            if (lane == 0) {
+              const int64_t ro = lo + t - p.r_begin;
+              p.counts[ro] = M;
+              p.lins[ro] = M > 0 ? blin : -1;
+              p.ties[ro] = M > 0 ? bties : 0;
+            }
+          }
+          __syncthreads();
+        }
+      }
+    }
+    if (tid == 0) s_bb = (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull);
+    __syncthreads();
+    bb = s_bb;
+  }
+
+  unsigned long long st_rechecks = L.rechecks;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    st_pairs += __shfl_xor_sync(0xffffffffu, st_pairs, o);
+    st_votes += __shfl_xor_sync(0xffffffffu, st_votes, o);
+    st_rechecks += __shfl_xor_sync(0xffffffffu, st_rechecks, o);
+  }
+  if (lane == 0) {
+    atomicAdd(&p.stats[0], st_pairs);
+    atomicAdd(&p.stats[1], st_votes);
+    atomicAdd(&p.stats[2], st_rechecks);
+  }
+}
+
 size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads) {
   size_t b = 0;
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n_pad * 16;
-  b += (size_t)(p.nxt + (p.nxt + 31) / 32) * 32 + 16 * 8 + 4 * 32 * 4 + (size_t)p.unit_cap * 4;
+  b += (size_t)(p.nxt + (p.nxt + 31) / 32) * 32 + kMaxBlockRot * 9 * 8 + 4 * 32 * 4 + (size_t)p.unit_cap * 4;
   b += (size_t)(threads / 32) * kRare * 8;
   b += (size_t)(threads / 32) * 32 * 16;  // per-warp staged sources
   return b;
@@ -745,7 +1187,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
 // lowered: plan construction on one thread and launches on another must not
 // race on this process-wide attribute (a lowered limit between another
 // thread's set and launch would fail that launch).
-template <bool H, bool PS, bool RK>
+template <bool H, bool PS, bool RK, bool RD = false>
 static cudaError_t raise_smem_limit() {
   static std::once_flag once[64];
   static cudaError_t err[64];
@@ -757,9 +1199,9 @@ static cudaError_t raise_smem_limit() {
     int optin = 0;
     cudaFuncAttributes a{};
     err[dev] = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (err[dev] == cudaSuccess) err[dev] = cudaFuncGetAttributes(&a, vote_kernel<H, PS, RK>);
+    if (err[dev] == cudaSuccess) err[dev] = cudaFuncGetAttributes(&a, vote_kernel<H, PS, RK, RD>);
     if (err[dev] == cudaSuccess)
-      err[dev] = cudaFuncSetAttribute(vote_kernel<H, PS, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      err[dev] = cudaFuncSetAttribute(vote_kernel<H, PS, RK, RD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       optin - (int)a.sharedSizeBytes);
   });
   return err[dev];
@@ -782,6 +1224,35 @@ cudaError_t launch_vote(const VoteParams& p, bool hsmem, bool psmem, int grid, i
   return cudaGetLastError();
 }
 
+cudaError_t launch_vote_redo(const VoteParams& p, int grid, int threads, cudaStream_t stream) {
+  const cudaError_t e = raise_smem_limit<true, true, false, true>();
+  if (e != cudaSuccess) return e;
+  vote_kernel<true, true, false, true><<<grid, threads, vote_smem_bytes(p, true, true, threads), stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vote_blocks(const VoteParams& p, int grid, int threads, cudaStream_t stream) {
+  static std::once_flag once[64];
+  static cudaError_t err[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
+    int optin = 0;
+    cudaFuncAttributes a{};
+    err[dev] = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (err[dev] == cudaSuccess) err[dev] = cudaFuncGetAttributes(&a, vote_blocks_kernel);
+    if (err[dev] == cudaSuccess)
+      err[dev] = cudaFuncSetAttribute(vote_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      optin - (int)a.sharedSizeBytes);
+  });
+  if (err[dev] != cudaSuccess) return err[dev];
+  threads = DSES_BLOCK_THREADS;
+  vote_blocks_kernel<<<grid, threads, vote_smem_bytes(p, true, true, threads), stream>>>(p);
+  return cudaGetLastError();
+}
+
 // Static shared memory of the vote kernel (kc[], exact-path pointers, ...):
 // the dynamic part is sized against opt-in limit minus this.
 size_t vote_static_smem() {
@@ -792,6 +1263,8 @@ size_t vote_static_smem() {
   if (cudaFuncGetAttributes(&a, vote_kernel<true, false, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
   if (cudaFuncGetAttributes(&a, vote_kernel<false, true, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
   if (cudaFuncGetAttributes(&a, vote_kernel<false, false, false>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_blocks_kernel) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
+  if (cudaFuncGetAttributes(&a, vote_kernel<true, true, false, true>) == cudaSuccess) m = std::max(m, a.sharedSizeBytes);
   return m;
 }
 
