@@ -112,7 +112,7 @@ int dses_plan_set_vote_grid(dses_plan* plan, int64_t ctas);
  * candidate-pair list; 0 = the per-rotation vote kernel.
  * Default: 5 when the translation window is small against the reference cloud,
  * else 0 (environment DSES_BLOCK_L overrides).  list_cap: list entries per CTA
- * (0 = default 2^18; blocks whose list overflows are re-run by the
+ * (0 = default 2^17; blocks whose list overflows are re-run by the
  * per-rotation kernel).  Results do not depend on either. */
 int dses_plan_set_block_rotations(dses_plan* plan, int64_t len, int64_t list_cap);
 

@@ -107,6 +107,12 @@ static int fail(int code, const char* fmt, ...) {
                   "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
   } while (0)
 
+#define CK_STATUS(call)              \
+  do {                               \
+    const int s_ = (call);           \
+    if (s_ != DSES_OK) return s_;    \
+  } while (0)
+
 extern "C" const char* dses_last_error(void) { return g_err.c_str(); }
 
 namespace dses {
@@ -259,11 +265,13 @@ struct UploadPack {
 namespace {
 struct RefTopo;
 struct DeviceRef;
+struct DeviceFixed;
 }  // namespace
 struct dses_plan {
   int device = 0, sms = 0;
   std::shared_ptr<const RefTopo> topo;  // the reference cloud's cached topology
   std::shared_ptr<DeviceRef> dref;      // and its device copy (shared by plans)
+  std::shared_ptr<DeviceFixed> dfix;    // the fixed-point reference layout on the device (shared)
   size_t smem_optin = 0;
   int64_t n = 0, m = 0, m_pad = 0;
   double bin = 0, inv_bin = 0;
@@ -368,10 +376,13 @@ void trace(const char* what) {
 // round-half-away-from-zero integer of v (host side fixed-point conversion)
 inline int64_t rint64(double v) { return (int64_t)std::llrint(v); }
 
-// recursive median split until tiles hold <= kTile points; splits at a
-// multiple of kTile so that all but the last tile of each branch are full.
-void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
-              std::vector<std::pair<int, int>>& tiles, int tile, int spawn = 0) {
+struct KdPoint {  // a point with its index, contiguous for the median splits
+  double c[3];
+  int idx;
+};
+
+static void kd_split(KdPoint* a, int64_t lo, int64_t hi, std::vector<std::pair<int, int>>& tiles,
+                     int tile, int spawn) {
   const int64_t cnt = hi - lo;
   if (cnt <= tile) {
     if (cnt > 0) tiles.emplace_back((int)lo, (int)cnt);
@@ -380,30 +391,45 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t q = lo; q < hi; ++q)
     for (int k = 0; k < 3; ++k) {
-      mn[k] = std::min(mn[k], pts[3 * perm[q] + k]);
-      mx[k] = std::max(mx[k], pts[3 * perm[q] + k]);
+      mn[k] = std::min(mn[k], a[q].c[k]);
+      mx[k] = std::max(mx[k], a[q].c[k]);
     }
   int axis = 0;
   for (int k = 1; k < 3; ++k)
     if (mx[k] - mn[k] > mx[axis] - mn[axis]) axis = k;
   const int64_t ntile = (cnt + tile - 1) / tile;
   const int64_t left = (ntile / 2) * tile;
-  std::nth_element(perm.begin() + lo, perm.begin() + lo + left, perm.begin() + hi,
-                   [&](int a, int b) {
-                     const double va = pts[3 * a + axis], vb = pts[3 * b + axis];
-                     return va < vb || (va == vb && a < b);
-                   });
-  if (spawn > 0 && cnt >= 4096) {  // disjoint halves: left on a helper thread
+  std::nth_element(a + lo, a + lo + left, a + hi, [axis](const KdPoint& u, const KdPoint& v) {
+    return u.c[axis] < v.c[axis] || (u.c[axis] == v.c[axis] && u.idx < v.idx);
+  });
+  if (spawn > 0 && cnt >= 32768) {  // disjoint halves: left on a helper thread
     std::vector<std::pair<int, int>> lt, rt;
-    std::thread th([&] { kd_tiles(pts, lo, lo + left, perm, lt, tile, spawn - 1); });
-    kd_tiles(pts, lo + left, hi, perm, rt, tile, spawn - 1);
+    std::thread th([&] { kd_split(a, lo, lo + left, lt, tile, spawn - 1); });
+    kd_split(a, lo + left, hi, rt, tile, spawn - 1);
     th.join();
     tiles.insert(tiles.end(), lt.begin(), lt.end());
     tiles.insert(tiles.end(), rt.begin(), rt.end());
     return;
   }
-  kd_tiles(pts, lo, lo + left, perm, tiles, tile);
-  kd_tiles(pts, lo + left, hi, perm, tiles, tile);
+  kd_split(a, lo, lo + left, tiles, tile, 0);
+  kd_split(a, lo + left, hi, tiles, tile, 0);
+}
+
+// Recursive median split of pts[perm[lo..hi)] until tiles hold <= `tile`
+// points; splits at a multiple of `tile` so that all but the last tile of
+// each branch are full.  perm is reordered into tile order.
+void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
+              std::vector<std::pair<int, int>>& tiles, int tile, int spawn = 0) {
+  std::vector<KdPoint> a((size_t)(hi - lo));
+  for (int64_t q = lo; q < hi; ++q) {
+    KdPoint& k = a[(size_t)(q - lo)];
+    k.idx = perm[q];
+    for (int d = 0; d < 3; ++d) k.c[d] = pts[3 * (int64_t)k.idx + d];
+  }
+  std::vector<std::pair<int, int>> t;
+  kd_split(a.data(), 0, hi - lo, t, tile, spawn);
+  for (int64_t q = lo; q < hi; ++q) perm[q] = a[(size_t)(q - lo)].idx;
+  for (const auto& e : t) tiles.emplace_back(e.first + (int)lo, e.second);
 }
 
 // Like kd_tiles for weighted items (centroids cen, weights wt >= 1): leaves
@@ -587,6 +613,7 @@ std::vector<std::pair<int, int>> near_pairs(const double* y, int64_t m, double t
 // (the c4 tool-pose use) builds it once.
 // ---------------------------------------------------------------------------
 struct GroupSpan { int start, count, gm; };
+struct RefFixed;
 struct RefTopo {
   int64_t m = 0;
   double bin = 0;
@@ -605,8 +632,11 @@ struct RefTopo {
   std::vector<int> pos;                        // original index -> tile-order entry
   std::vector<int> noff, nidx;                 // exact-path near lists (tile order, j' < j)
   std::vector<double> ys;                      // the cloud in tile order
+  double ymax = 0, ext = 0;                    // max |y| over the axes; largest axis extent
   mutable std::mutex dmu;
   mutable std::shared_ptr<DeviceRef> dev[64];  // device copies of the arrays above
+  mutable std::mutex fmu;
+  mutable std::vector<std::shared_ptr<const RefFixed>> fixed;  // fixed-point layouts (ref_fixed)
 };
 
 // A RefTopo's read-only arrays on one device, uploaded once and borrowed by
@@ -813,6 +843,15 @@ static std::shared_ptr<const RefTopo> build_ref_topo(const double* y, int64_t m,
   T->ys.resize(3 * mp);
   for (int64_t q = 0; q < mp; ++q)
     for (int k = 0; k < 3; ++k) T->ys[3 * q + k] = y[3 * yidx[q] + k];
+  for (int k = 0; k < 3; ++k) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int64_t j = 0; j < m; ++j) {
+      lo = std::min(lo, y[3 * j + k]);
+      hi = std::max(hi, y[3 * j + k]);
+      T->ymax = std::max(T->ymax, std::fabs(y[3 * j + k]));
+    }
+    if (m > 0) T->ext = std::max(T->ext, hi - lo);
+  }
   scoring.get();
   return T;
 }
@@ -841,74 +880,56 @@ static std::shared_ptr<const RefTopo> ref_topo(const double* y, int64_t m, doubl
   return T;
 }
 
-int build_plan(dses_plan* P, const double* x, const double* y) {
-  const int64_t n = P->n, m = P->m;
-  cudaStream_t st = upload_stream(P->device);
-  // ---- fixed-point scale
-  trace("fixed-point scale");
-  double ymax = 0, xnorm = 0;
-  for (int64_t j = 0; j < m; ++j)
-    for (int k = 0; k < 3; ++k) ymax = std::max(ymax, std::fabs(y[3 * j + k]));
-  for (int64_t i = 0; i < n; ++i)
-    xnorm = std::max(xnorm, std::sqrt(x[3 * i] * x[3 * i] + x[3 * i + 1] * x[3 * i + 1] +
-                                      x[3 * i + 2] * x[3 * i + 2]));
-  double lomax = 0;
-  for (int k = 0; k < 3; ++k)
-    lomax = std::max(lomax, std::max(std::fabs((double)P->ilo[k]),
-                                     std::fabs((double)(P->ilo[k] + P->dims[k]))));
-  const double A = ymax * P->inv_bin + 3.0 * xnorm * P->inv_bin + lomax + 8.0;
-  int F = 0;
-  if (std::isfinite(A) && A > 0) F = (int)std::floor(std::log2(std::ldexp(1.0, 29) / A));
-  F = std::min(F, 20);
-  if (F < 6) F = 0;  // exact mode: every pair re-binned in binary64
-  P->F = F;
-  const double S = std::ldexp(1.0, F);
-  P->by = ymax;
-  double tmax = 0;
-  for (int k = 0; k < 3; ++k)
-    tmax = std::max(tmax, (std::fabs((double)P->ilo[k]) + (double)P->dims[k]) * P->bin);
-  P->bx = xnorm + tmax;
-
-  // ---- spatial tiles
-  trace("spatial tiles");
-  std::vector<int> px(n);
-  std::iota(px.begin(), px.end(), 0);
-  std::vector<std::pair<int, int>> tx;
-  kd_tiles(x, 0, n, px, tx, kTile, host_threads() >= 4 ? 2 : 0);  // source units
-  std::vector<double> xs(3 * n);
-  for (int64_t i = 0; i < n; ++i)
-    for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
-  const double inv_s = P->inv_bin * S;
-  // (the vote kernel bounds each unit by the exact box of its rotated
-  // fixed-point points, computed on the device per rotation)
-  std::vector<XTile> xt(tx.size());
-  for (size_t t = 0; t < tx.size(); ++t) {
-    XTile& T = xt[t];
-    T = XTile{};
-    T.start = tx[t].first;
-    T.count = tx[t].second;
+// The reference cloud in fixed point for one (F, window origin): Yq in tile
+// order (the vote kernels' metadata in .w, the block kernel's empty sentinel
+// slot at m_pad), the group tiles and the guard-band risk bitmaps.  Cached per
+// reference topology (most recent few) and uploaded once per device, like
+// the topology: registrations of many sources against one model with one
+// search configuration build it once.
+struct DeviceFixed {
+  int device = 0;
+  DevBuf arena, yq, yt, risk;
+  ~DeviceFixed() {
+    if (!arena.p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    cudaFree(arena.p);  // synchronous: no plan of this layout is left
+    cudaSetDevice(cur);
+    arena.p = nullptr;
   }
-  // ---- reference topology (cached per reference cloud and bin size)
-  const std::shared_ptr<const RefTopo> topo = ref_topo(y, m, P->bin);
-  const std::vector<int>& yidx = topo->yidx;
-  const std::vector<char>& yfar = topo->yfar;
-  const std::vector<GroupSpan>& groups = topo->groups;
-  const std::vector<int>& aoff = topo->aoff;
-  const std::vector<int>& aidx = topo->aidx;
-  const std::vector<int>& pos = topo->pos;
-  for (int k = 0; k < 3; ++k) { P->gorg[k] = topo->gorg[k]; P->gdim[k] = topo->gdim[k]; }
-  P->gh = topo->gh;
-  P->g_pts_per_cell = topo->gppc;
-  const int64_t mp = (int64_t)yidx.size();  // padded reference entries
-  P->m_pad = mp;
-  const std::vector<double>& ys = topo->ys;
+};
+struct RefFixed {
+  int F = 0;
+  int64_t ilo[3] = {0, 0, 0};
+  std::vector<int4> yq;
+  std::vector<YTile> yt;
+  std::vector<unsigned> risk;
+  bool risk_on = false;
+  mutable std::mutex dmu;
+  mutable std::shared_ptr<DeviceFixed> dev[64];
+};
+
+static int build_ref_fixed(const RefTopo& T, double inv_bin, int F, const int64_t ilo[3], RefFixed* R) {
+  R->F = F;
+  for (int k = 0; k < 3; ++k) R->ilo[k] = ilo[k];
+  const std::vector<int>& yidx = T.yidx;
+  const std::vector<char>& yfar = T.yfar;
+  const std::vector<GroupSpan>& groups = T.groups;
+  const std::vector<int>& aoff = T.aoff;
+  const std::vector<int>& aidx = T.aidx;
+  const std::vector<int>& pos = T.pos;
+  const std::vector<double>& ys = T.ys;
+  const int64_t mp = (int64_t)yidx.size();
+  const double S = std::ldexp(1.0, F);
   // fixed-point reference: Yq = rint(fl(y*inv)*S) - lo*S + S/2 + G
-  std::vector<int4> yq(mp);
+  std::vector<int4>& yq = R->yq;
+  yq.resize(mp);
   const int64_t Si = (int64_t)1 << F;
   for (int64_t q = 0; q < mp; ++q) {
     int v[3];
     for (int k = 0; k < 3; ++k) {
-      int64_t w = F ? rint64((ys[3 * q + k] * P->inv_bin) * S) - P->ilo[k] * Si + Si / 2 + kGuard : 0;
+      int64_t w = F ? rint64((ys[3 * q + k] * inv_bin) * S) - ilo[k] * Si + Si / 2 + kGuard : 0;
       if (w > (1ll << 30) || w < -(1ll << 30)) {
         return fail(DSES_E_INVALID, "internal: fixed-point overflow (F=%d)", F);
       }
@@ -916,7 +937,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     }
     yq[q] = make_int4(v[0], v[1], v[2], 0);
   }
-  std::vector<YTile> yt(groups.size());
+  std::vector<YTile>& yt = R->yt;
+  yt.resize(groups.size());
   for (size_t t = 0; t < groups.size(); ++t) {
     YTile& T = yt[t];
     T = YTile{};
@@ -972,7 +994,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   // partner lanes): "has a dedup partner", "component split over groups",
   // the point's offset from its dedup component's first point (tile order)
   {
-    const std::vector<int>& ycomp = topo->ycomp;
+    const std::vector<int>& ycomp = T.ycomp;
     for (const YTile& T : yt)
       for (int q = T.start; q < T.start + T.count; ++q) {
         yq[q].w |= (aoff[yidx[q] + 1] > aoff[yidx[q]] ? kPartFlag : 0) |
@@ -991,8 +1013,8 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   // (only for small reference clouds: the bitmaps, 384 B per group, are read
   // per (group, unit) and must stay L1-resident; with many groups and few
   // survivors per unit -- c4 -- the lookups cost more than they save)
-  const bool risk_on = F >= kRiskBits + 2 && yt.size() <= 128;
-  std::vector<unsigned> risk;
+  const bool risk_on = R->risk_on = F >= kRiskBits + 2 && yt.size() <= 128;
+  std::vector<unsigned>& risk = R->risk;
   if (risk_on) {
     const int sh = F - kRiskBits;
     const unsigned fm = (unsigned)((1u << F) - 1u);
@@ -1017,6 +1039,91 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     risk.assign(kRiskWords, 0u);
     for (YTile& T : yt) T.pad[0] = 1;  // exact mode / few fraction bits: no source is safe
   }
+  yq.push_back(make_int4(kNoRef, 0, 0, 0));  // the block kernel's empty sentinel slot (j = m_pad)
+  return DSES_OK;
+}
+
+static int ref_fixed(const RefTopo& T, double inv_bin, int F, const int64_t ilo[3],
+                     std::shared_ptr<const RefFixed>* out) {
+  {
+    std::lock_guard<std::mutex> lk(T.fmu);
+    for (size_t k = T.fixed.size(); k-- > 0;) {
+      const auto& c = T.fixed[k];
+      if (c->F == F && c->ilo[0] == ilo[0] && c->ilo[1] == ilo[1] && c->ilo[2] == ilo[2]) {
+        *out = c;
+        return DSES_OK;
+      }
+    }
+  }
+  auto R = std::make_shared<RefFixed>();
+  const int rc = build_ref_fixed(T, inv_bin, F, ilo, R.get());
+  if (rc != DSES_OK) return rc;
+  std::lock_guard<std::mutex> lk(T.fmu);
+  T.fixed.push_back(R);
+  if (T.fixed.size() > 4) T.fixed.erase(T.fixed.begin());
+  *out = R;
+  return DSES_OK;
+}
+
+int build_plan(dses_plan* P, const double* x, const double* y) {
+  const int64_t n = P->n, m = P->m;
+  cudaStream_t st = upload_stream(P->device);
+  // ---- reference topology (cached per reference cloud and bin size)
+  const std::shared_ptr<const RefTopo> topo = ref_topo(y, m, P->bin);
+  // ---- fixed-point scale
+  trace("fixed-point scale");
+  const double ymax = topo->ymax;
+  double xnorm = 0;
+  for (int64_t i = 0; i < n; ++i)
+    xnorm = std::max(xnorm, std::sqrt(x[3 * i] * x[3 * i] + x[3 * i + 1] * x[3 * i + 1] +
+                                      x[3 * i + 2] * x[3 * i + 2]));
+  double lomax = 0;
+  for (int k = 0; k < 3; ++k)
+    lomax = std::max(lomax, std::max(std::fabs((double)P->ilo[k]),
+                                     std::fabs((double)(P->ilo[k] + P->dims[k]))));
+  const double A = ymax * P->inv_bin + 3.0 * xnorm * P->inv_bin + lomax + 8.0;
+  int F = 0;
+  if (std::isfinite(A) && A > 0) F = (int)std::floor(std::log2(std::ldexp(1.0, 29) / A));
+  F = std::min(F, 20);
+  if (F < 6) F = 0;  // exact mode: every pair re-binned in binary64
+  P->F = F;
+  const double S = std::ldexp(1.0, F);
+  const int64_t Si = (int64_t)1 << F;
+  P->by = ymax;
+  double tmax = 0;
+  for (int k = 0; k < 3; ++k)
+    tmax = std::max(tmax, (std::fabs((double)P->ilo[k]) + (double)P->dims[k]) * P->bin);
+  P->bx = xnorm + tmax;
+
+  // ---- spatial tiles
+  trace("spatial tiles");
+  std::vector<int> px(n);
+  std::iota(px.begin(), px.end(), 0);
+  std::vector<std::pair<int, int>> tx;
+  kd_tiles(x, 0, n, px, tx, kTile, host_threads() >= 4 ? 2 : 0);  // source units
+  std::vector<double> xs(3 * n);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) xs[3 * i + k] = x[3 * px[i] + k];
+  const double inv_s = P->inv_bin * S;
+  // (the vote kernel bounds each unit by the exact box of its rotated
+  // fixed-point points, computed on the device per rotation)
+  std::vector<XTile> xt(tx.size());
+  for (size_t t = 0; t < tx.size(); ++t) {
+    XTile& T = xt[t];
+    T = XTile{};
+    T.start = tx[t].first;
+    T.count = tx[t].second;
+  }
+  for (int k = 0; k < 3; ++k) { P->gorg[k] = topo->gorg[k]; P->gdim[k] = topo->gdim[k]; }
+  P->gh = topo->gh;
+  P->g_pts_per_cell = topo->gppc;
+  P->m_pad = (int64_t)topo->yidx.size();  // reference entries (tile order)
+  // fixed-point reference (cached per reference cloud, F and window origin)
+  trace("fixed-point reference");
+  std::shared_ptr<const RefFixed> fx;
+  CK_STATUS(ref_fixed(*topo, P->inv_bin, F, P->ilo, &fx));
+  const std::vector<YTile>& yt = fx->yt;
+  const bool risk_on = fx->risk_on;
   if (yt.size() >= 65536 || xt.size() >= 65536)  // (group << 16 | unit) work-unit encoding
     return fail(DSES_E_LIMIT, "cloud too large for the vote kernel: at most 65535 groups / units "
                 "of 32 points (about 2 million points) per cloud");
@@ -1062,14 +1169,29 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     P->gcell.borrow(d.gcell.p, d.gcell.cap);
     P->gpts.borrow(d.gpts.p, d.gpts.cap);
   }
+  {  // the fixed-point reference layout: uploaded once per device, then borrowed
+    std::lock_guard<std::mutex> lk(fx->dmu);
+    std::shared_ptr<DeviceFixed>& d = fx->dev[P->device];
+    if (!d) {
+      auto nd = std::make_shared<DeviceFixed>();
+      nd->device = P->device;
+      UploadPack rp;
+      rp.add(nd->yq, fx->yq);
+      rp.add(nd->yt, fx->yt);
+      rp.add(nd->risk, fx->risk);
+      CK(rp.commit(nd->arena, st));
+      CK(cudaStreamSynchronize(st));  // the staging buffer is reused below
+      d = nd;
+    }
+    P->dfix = d;
+    P->yq.borrow(d->yq.p, d->yq.cap);
+    P->yt.borrow(d->yt.p, d->yt.cap);
+    P->risk.borrow(d->risk.p, d->risk.cap);
+  }
   // the plan's own (source- and window-dependent) arrays
   UploadPack pack;
   pack.add(P->xs, xs);
-  yq.push_back(make_int4(kNoRef, 0, 0, 0));  // the block kernel's empty sentinel slot (j = m_pad)
-  pack.add(P->yq, yq);
   pack.add(P->xt, xt);
-  pack.add(P->yt, yt);
-  pack.add(P->risk, risk);
   pack.add(P->x0, xv);
   CK(pack.commit(P->arena, st));
   CK(P->stats.ensure(4 * sizeof(unsigned long long), st));
@@ -1125,14 +1247,9 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     // cloud (c4: 36 mm in a 1.4 m cloud -> 1.7x).  With windows comparable to
     // the cloud (c1-c3, c5) most lanes vote and the per-rotation kernel is
     // faster (c2: 10.1 vs 18 ms with blocks).
-    double ext = 0, win = 0;
-    for (int k = 0; k < 3; ++k) {
-      double lo = INFINITY, hi = -INFINITY;
-      for (int64_t j = 0; j < m; ++j) { lo = std::min(lo, y[3 * j + k]); hi = std::max(hi, y[3 * j + k]); }
-      ext = std::max(ext, hi - lo);
-      win = std::max(win, (double)P->dims[k] * P->bin);
-    }
-    P->blk_L = envL >= 0 ? envL : (win < kBlockWindowFrac * ext ? kDefaultBlockL : 0);
+    double win = 0;
+    for (int k = 0; k < 3; ++k) win = std::max(win, (double)P->dims[k] * P->bin);
+    P->blk_L = envL >= 0 ? envL : (win < kBlockWindowFrac * topo->ext ? kDefaultBlockL : 0);
   }
   v.count16 = n < 65536 ? 1 : 0;
   const int64_t words = v.count16 ? (v.nbins + 1) / 2 : v.nbins;
@@ -1400,7 +1517,7 @@ extern "C" int dses_plan_destroy(dses_plan* P) {
                     &P->counts, &P->lins, &P->ties, &P->hist_g, &P->p_g, &P->stats, &P->scal,
                     &P->cand_rows, &P->cand_lins, &P->err32, &P->partial, &P->sel, &P->vals,
                     &P->err64, &P->win_err, &P->win_row, &P->win_c, &P->tmp_rows, &P->tmp_lins,
-                    &P->tvec};
+                    &P->tvec, &P->blist, &P->redo};
   if (P->pend.active) cudaEventSynchronize(P->ev[4]);  // an unwaited search
   for (DevBuf* b : bufs) b->release();
   for (auto& e : P->ev) cudaEventDestroy(e);
@@ -1777,6 +1894,10 @@ static int reserve_search(dses_plan* P, int64_t nr, cudaStream_t st = 0) {
         1, std::min<size_t>((size_t)std::min<int64_t>(P->vote_grid, nr), budget / per_cta));
     if (!P->hsmem) CK(P->hist_g.ensure((size_t)grid * v.hist_words * 4, st));
     if (!P->psmem) CK(P->p_g.ensure((size_t)grid * v.n_pad * 16, st));
+  }
+  if (P->blk_L > 0 && P->hsmem && P->psmem && P->F > 0 && P->vp.jbits > 0 && !P->sparse) {
+    CK(P->blist.ensure((size_t)P->vote_grid * P->blk_cap * 4, st));  // rotation-block lists
+    CK(P->redo.ensure(8 * (size_t)(nr + 1), st));
   }
   const int64_t cap = std::min<int64_t>(nr, kFusedRescoreCap);
   const int nblk = (int)((P->n + screen_threads() - 1) / screen_threads());

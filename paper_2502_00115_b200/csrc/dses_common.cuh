@@ -46,7 +46,7 @@ constexpr int kCompOffShift = 20;    // bits 20..23: its offset from the compone
 constexpr int kMaxBlockRot = 8;   // rotations per block (the block kernel's R area in shared memory)
 constexpr int kDefaultBlockL = 5; // rotations per block unless DSES_BLOCK_L says otherwise
 constexpr double kBlockWindowFrac = 0.15;  // blocks when the window is below this part of the cloud
-constexpr int kBlockListCap = 1 << 18;  // candidate-list entries per CTA (1 MiB)
+constexpr int kBlockListCap = 1 << 17;  // candidate-list entries per CTA (512 KiB)
 constexpr int kRiskBits = 10;     // fraction buckets per axis of the guard-band risk bitmaps
 constexpr int kRiskWords = 3 * (1 << kRiskBits) / 32;  // words per group (3 axes)
 constexpr int kVoteThreads = 1024;
