@@ -768,30 +768,41 @@ __device__ __forceinline__ bool boxes_meet_w(const YTile& yt, const int4& lo, co
          (yt.lo[1] - hi.y < wq1) & (yt.hi[2] - lo.z >= -dq2) & (yt.lo[2] - hi.z < wq2);
 }
 
-// Append the set lanes of m (entry `entry` each, in lane order) to the warp's
-// open list segment.  One (source, group) run never straddles two segments
-// (so neither does a dedup component): a run that does not fit the open
-// segment's room closes it (the rest padded with the empty sentinel entry).
-// seg / fill: the warp's open segment (entry offset in p.list; fill == 32:
-// none).  Returns false once the CTA's slab is full.
+// The warp's open list segment is staged in shared memory (the warp's
+// exact-path list area, unused while a block's list is built) and written to
+// the CTA's slab, 32 entries at once, when full.  One (source, group) run
+// never straddles two segments (so neither does a dedup component): a run
+// that does not fit the open segment's room closes it (the rest padded with
+// the empty sentinel entry).  Returns false once the CTA's slab is full.
+__device__ __forceinline__ bool flush_segment(const VoteParams& p, uint32_t buf_sh, int lane,
+                                              uint32_t nseg_sh, unsigned slab, unsigned pad_entry,
+                                              int& fill) {
+  if (fill == 0) return true;
+  if (lane >= fill) asm volatile("st.shared.u32 [%0], %1;" ::"r"(buf_sh + 4u * (unsigned)lane), "r"(pad_entry) : "memory");
+  __syncwarp();
+  unsigned e, s = 0;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(buf_sh + 4u * (unsigned)lane) : "memory");
+  if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(s) : "r"(nseg_sh) : "memory");
+  s = __shfl_sync(0xffffffffu, s, 0);
+  fill = 0;
+  if (32u * (s + 1u) > (unsigned)p.list_cap) return false;
+  __stcg(p.list + (slab + 32u * s + (unsigned)lane), e);
+  return true;
+}
+
 __device__ __forceinline__ bool emit_entries(const VoteParams& p, unsigned m, unsigned entry, int lane,
-                                             unsigned lanemask_lt, uint32_t nseg_sh, unsigned slab,
-                                             unsigned pad_entry, unsigned& seg, int& fill,
+                                             unsigned lanemask_lt, uint32_t buf_sh, uint32_t nseg_sh,
+                                             unsigned slab, unsigned pad_entry, int& fill,
                                              unsigned& wcount) {
   const int cnt = __popc(m);
   wcount += (unsigned)cnt;
-  if (cnt > 32 - fill) {  // warp-uniform
-    if (lane >= fill) __stcg(p.list + (seg + (unsigned)lane), pad_entry);
-    unsigned s = 0;
-    if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(s) : "r"(nseg_sh) : "memory");
-    s = __shfl_sync(0xffffffffu, s, 0);
-    if (32u * (s + 1u) > (unsigned)p.list_cap) { fill = 32; return false; }
-    seg = slab + 32u * s;
-    fill = 0;
-  }
-  if ((m >> lane) & 1u) __stcg(p.list + (seg + (unsigned)fill + (unsigned)__popc(m & lanemask_lt)), entry);
+  bool ok = true;
+  if (cnt > 32 - fill) ok = flush_segment(p, buf_sh, lane, nseg_sh, slab, pad_entry, fill);  // warp-uniform
+  if ((m >> lane) & 1u)
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(buf_sh + 4u * (unsigned)(fill + __popc(m & lanemask_lt))),
+                 "r"(entry) : "memory");
   fill += cnt;
-  return true;
+  return ok;
 }
 
 #ifndef DSES_BLOCK_THREADS
@@ -832,7 +843,10 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   __shared__ int s_dq[3];
   __shared__ int s_nseg;
   __shared__ int s_lovf;
-  __shared__ long long s_bb;
+  __shared__ long long s_lo;                     // the current block: first rotation ...
+  __shared__ int s_nb;                           // ... and count (-1: done)
+  __shared__ unsigned long long s_wst[32][2];    // per-warp (pairs, votes) statistics
+  if (tid < 64) s_wst[tid >> 1][tid & 1] = 0;
   if (tid == 0) {
     kc[0] = p.W0; kc[1] = p.W1; kc[2] = p.W2; kc[3] = p.fmask; kc[4] = p.gthr;
     kc[5] = (unsigned)p.d1; kc[6] = (unsigned)p.d2; kc[7] = (unsigned)p.F;
@@ -845,7 +859,6 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   }
   __syncthreads();
   const uint32_t hist_sh = kc[8];
-  unsigned long long st_pairs = 0, st_votes = 0;
   Lane L;
   asm volatile("mov.u32 %0, %1;" : "=r"(L.rare_sh) : "r"((uint32_t)__cvta_generic_to_shared(rare)));
   L.nrare = 0;
@@ -859,24 +872,38 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   const uint32_t nseg_sh = (uint32_t)__cvta_generic_to_shared(&s_nseg);
   const unsigned jmask = (1u << p.jbits) - 1u;
   const unsigned pad_entry = (unsigned)p.m_pad;  // i = 0, j = the empty sentinel slot
-  const int BL = p.blk_L;
-  const int64_t side = 2 * p.rot.k + 1;
-  const int64_t r_end = p.r_begin + p.r_count;
-  const int64_t row0 = p.r_begin / side;
-  const int64_t bpr = (side + BL - 1) / BL;
-  const int64_t nblk = ((r_end - 1) / side - row0 + 1) * bpr;
   const int gmax = max(1, min(min(p.nyt, p.unit_cap / 4), p.unit_cap - p.nxt - 1));
   const bool masks = nxc > 1 && nxc <= 32;
 
-  for (int64_t bb = blockIdx.x; bb < nblk;) {
-    const int64_t row = row0 + bb / bpr, c0 = (bb % bpr) * BL;
-    const int64_t lo = max(row * side + c0, p.r_begin);
-    const int64_t hi = min(row * side + min(side, c0 + (int64_t)BL), r_end);
-    const int nb = (int)max((int64_t)0, hi - lo);
-    if (nb > 0) {  // block-uniform
+  // blocks: runs of blk_L rotations of a grid row, from a global queue (the
+  // first one static); thread 0 keeps the claim state, the rest read the
+  // block from shared memory (no 64-bit loop state in every thread)
+  long long bclaim = blockIdx.x;
+  for (;;) {
+    if (tid == 0) {
+      const int64_t BL = p.blk_L, side = 2 * p.rot.k + 1, r_end = p.r_begin + p.r_count;
+      const int64_t row0 = p.r_begin / side, bpr = (side + BL - 1) / BL;
+      const int64_t nblk = ((r_end - 1) / side - row0 + 1) * bpr;
+      int nb = -1;
+      int64_t lo = 0;
+      while (bclaim < nblk) {
+        const int64_t row = row0 + bclaim / bpr, c0 = (bclaim % bpr) * BL;
+        lo = max(row * side + c0, p.r_begin);
+        const int64_t hi = min(row * side + min(side, c0 + BL), r_end);
+        bclaim = (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull);
+        if (hi > lo) { nb = (int)(hi - lo); break; }
+      }
+      s_lo = lo;
+      s_nb = nb;
+      s_nseg = 0;
+      s_lovf = 0;
+    }
+    __syncthreads();
+    const int nb = s_nb;
+    if (nb < 0) break;
+    {
       const int rc = nb >> 1;
-      if (tid < 9 * nb) Rb[tid] = rotation_entry(p.rot, lo + tid / 9, tid % 9);
-      if (tid == 0) { s_nseg = 0; s_lovf = 0; }
+      if (tid < 9 * nb) Rb[tid] = rotation_entry(p.rot, s_lo + tid / 9, tid % 9);
       __syncthreads();
       if (tid < 3) {  // widening of the window per axis
         double d = 0.0;
@@ -931,8 +958,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
                      Wp2 = p.W2 + 2u * (unsigned)dq2;
 
       // ---- build the block's list (rounds of reference groups, as vote_kernel)
-      unsigned seg = 0;
-      int fill = 32;
+      int fill = 0;
       const bool wide = (dq0 | dq1 | dq2) < 0;  // block-uniform
       bool room = !wide;
       unsigned wcount = 0;
@@ -1009,24 +1035,21 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
             const unsigned m = __ballot_sync(0xffffffffu, c);
             if (m)
               room = emit_entries(p, m, ((unsigned)Pi.w << p.jbits) | (unsigned)j, lane, lanemask_lt,
-                                  nseg_sh, slab, pad_entry, seg, fill, wcount);
+                                  L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
           }
         }
         __syncthreads();
         gnext = ((int)ovf == b0) ? 1 : gmax;
         b0 = (int)ovf;
       }
-      if (!room) {
-        if (lane == 0) s_lovf = 1;
-      } else if (fill < 32 && lane >= fill) {  // close the warp's open segment
-        __stcg(p.list + (seg + (unsigned)lane), pad_entry);
-      }
+      if (room) room = flush_segment(p, L.rare_sh, lane, nseg_sh, slab, pad_entry, fill);
+      if (!room && lane == 0) s_lovf = 1;
       __syncthreads();
       if (s_lovf) {  // left to vote_kernel
-        if (tid < nb) p.redo[atomicAdd(p.redo_n, 1ull)] = lo + tid;
+        if (tid < nb) p.redo[atomicAdd(p.redo_n, 1ull)] = s_lo + tid;
       } else {
         const int nseg = s_nseg;
-        if (lane == 0) st_pairs += (unsigned long long)wcount * (unsigned long long)nb;
+        if (lane == 0) s_wst[warp][0] += (unsigned long long)wcount * (unsigned long long)nb;
         for (int t0 = 0; t0 < nb; ++t0) {
           const int t = t0 == 0 ? rc : (t0 <= rc ? t0 - 1 : t0);  // the centre first: P holds it
           const double* Rt = Rb + 9 * t;
@@ -1096,17 +1119,20 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           }
           __syncthreads();
           // ---- mode (vote_kernel's two passes)
-          unsigned mx = 0;
+          unsigned mx = 0, nv = 0;
           for (int w = tid; w < nw4; w += nthreads) {
             const uint4 v = hist4[w];
-            st_votes += ((v.x * 0x10001u) >> 16) + ((v.y * 0x10001u) >> 16) + ((v.z * 0x10001u) >> 16) +
-                        ((v.w * 0x10001u) >> 16);
+            nv += ((v.x * 0x10001u) >> 16) + ((v.y * 0x10001u) >> 16) + ((v.z * 0x10001u) >> 16) +
+                  ((v.w * 0x10001u) >> 16);
             mx = __vmaxu2(mx, __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w)));
           }
           mx = max(mx & 0xffffu, mx >> 16);
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          if (lane == 0) red[warp] = (int)mx;
+          for (int o = 16; o > 0; o >>= 1) {
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            nv += __shfl_xor_sync(0xffffffffu, nv, o);
+          }
+          if (lane == 0) { red[warp] = (int)mx; s_wst[warp][1] += nv; }
           __syncthreads();
           int M = 0;
           for (int w = 0; w < nwarps; ++w) M = max(M, red[w]);
@@ -1143,7 +1169,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
               bties += __shfl_xor_sync(0xffffffffu, bties, o);
             }
             if (lane == 0) {
-              const int64_t ro = lo + t - p.r_begin;
+              const int64_t ro = s_lo + t - p.r_begin;
               p.counts[ro] = M;
               p.lins[ro] = M > 0 ? blin : -1;
               p.ties[ro] = M > 0 ? bties : 0;
@@ -1153,22 +1179,16 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
         }
       }
     }
-    if (tid == 0) s_bb = (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull);
-    __syncthreads();
-    bb = s_bb;
+    __syncthreads();  // s_lo / s_nb are rewritten for the next block
   }
 
-  unsigned long long st_rechecks = L.rechecks;
+  unsigned st_rechecks = L.rechecks;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    st_pairs += __shfl_xor_sync(0xffffffffu, st_pairs, o);
-    st_votes += __shfl_xor_sync(0xffffffffu, st_votes, o);
-    st_rechecks += __shfl_xor_sync(0xffffffffu, st_rechecks, o);
-  }
+  for (int o = 16; o > 0; o >>= 1) st_rechecks += __shfl_xor_sync(0xffffffffu, st_rechecks, o);
   if (lane == 0) {
-    atomicAdd(&p.stats[0], st_pairs);
-    atomicAdd(&p.stats[1], st_votes);
-    atomicAdd(&p.stats[2], st_rechecks);
+    atomicAdd(&p.stats[0], s_wst[warp][0]);
+    atomicAdd(&p.stats[1], s_wst[warp][1]);
+    atomicAdd(&p.stats[2], (unsigned long long)st_rechecks);
   }
 }
 
