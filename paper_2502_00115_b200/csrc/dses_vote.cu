@@ -1028,21 +1028,29 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           if (sok) sts_v4(stage_sh + 16u * (unsigned)__popc(sm & lanemask_lt),
                           make_int4(Pl.x, Pl.y, Pl.z, U.x + lane));
           __syncwarp();
-          for (int t = 0; t < nsrc && room; ++t) {
-            const int4 Pi = lds_v4(stage_sh + 16u * (unsigned)t);
-            const bool c = ((unsigned)y0 - (unsigned)Pi.x < Wp0) & ((unsigned)y1 - (unsigned)Pi.y < Wp1) &
-                           ((unsigned)y2 - (unsigned)Pi.z < Wp2);
-            const unsigned m = __ballot_sync(0xffffffffu, c);
-            if (m)
-              room = emit_entries(p, m, ((unsigned)Pi.w << p.jbits) | (unsigned)j, lane, lanemask_lt,
-                                  L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
+          // two staged sources per step (a slab overflow only stops the
+          // writes: the block goes to vote_kernel)
+          for (int t = 0; t < nsrc; t += 2) {
+            const int4 P0 = lds_v4(stage_sh + 16u * (unsigned)t);
+            const int4 P1 = lds_v4(stage_sh + 16u * (unsigned)min(t + 1, 31));
+            const bool c0 = ((unsigned)y0 - (unsigned)P0.x < Wp0) & ((unsigned)y1 - (unsigned)P0.y < Wp1) &
+                            ((unsigned)y2 - (unsigned)P0.z < Wp2);
+            const bool c1 = ((unsigned)y0 - (unsigned)P1.x < Wp0) & ((unsigned)y1 - (unsigned)P1.y < Wp1) &
+                            ((unsigned)y2 - (unsigned)P1.z < Wp2) & (t + 1 < nsrc);
+            const unsigned m0 = __ballot_sync(0xffffffffu, c0), m1 = __ballot_sync(0xffffffffu, c1);
+            if (m0)
+              room &= emit_entries(p, m0, ((unsigned)P0.w << p.jbits) | (unsigned)j, lane, lanemask_lt,
+                                   L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
+            if (m1)
+              room &= emit_entries(p, m1, ((unsigned)P1.w << p.jbits) | (unsigned)j, lane, lanemask_lt,
+                                   L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
           }
         }
         __syncthreads();
         gnext = ((int)ovf == b0) ? 1 : gmax;
         b0 = (int)ovf;
       }
-      if (room) room = flush_segment(p, L.rare_sh, lane, nseg_sh, slab, pad_entry, fill);
+      room &= flush_segment(p, L.rare_sh, lane, nseg_sh, slab, pad_entry, fill);
       if (!room && lane == 0) s_lovf = 1;
       __syncthreads();
       if (s_lovf) {  // left to vote_kernel
