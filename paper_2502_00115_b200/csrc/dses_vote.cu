@@ -760,14 +760,6 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 // A block whose list exceeds the CTA's slab is left to vote_kernel (redo
 // list).  Counts, bins and ties are those of the per-rotation kernel.
 
-// Widened window test of a source box [lo, hi] against a group box:
-// Yq - Pq in [-dq, W + dq) possible on every axis (wq = W + dq)?
-__device__ __forceinline__ bool boxes_meet_w(const YTile& yt, const int4& lo, const int4& hi,
-                                             int dq0, int dq1, int dq2, int wq0, int wq1, int wq2) {
-  return (yt.hi[0] - lo.x >= -dq0) & (yt.lo[0] - hi.x < wq0) & (yt.hi[1] - lo.y >= -dq1) &
-         (yt.lo[1] - hi.y < wq1) & (yt.hi[2] - lo.z >= -dq2) & (yt.lo[2] - hi.z < wq2);
-}
-
 // The warp's open list segment is staged in shared memory (the warp's
 // exact-path list area, unused while a block's list is built) and written to
 // the CTA's slab, 32 entries at once, when full.  One (source, group) run
@@ -820,9 +812,10 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   int4* P = reinterpret_cast<int4*>(smem + off);
   off += (size_t)p.n_pad * 16;
   const int nxc = (p.nxt + 31) >> 5;
-  int4* XB = reinterpret_cast<int4*>(smem + off);
+  int4* XB = reinterpret_cast<int4*>(smem + off);  // unit boxes, widened by the unit's motion bound
   int4* CB = XB + 2 * p.nxt;
-  off += (size_t)(p.nxt + nxc) * 32;
+  int4* DQ = CB + 2 * nxc;                          // per unit: the widening per axis
+  off += (size_t)(p.nxt + nxc) * 32 + (size_t)p.nxt * 16;
   double* Rb = reinterpret_cast<double*>(smem + off);  // [kMaxBlockRot][9]
   off += kMaxBlockRot * 9 * 8;
   int* red = reinterpret_cast<int*>(smem + off);
@@ -840,7 +833,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   const unsigned lanemask_lt = (1u << lane) - 1u;
   const uint32_t P_sh = (uint32_t)__cvta_generic_to_shared(P);
   __shared__ __align__(16) unsigned kc[12];
-  __shared__ int s_dq[3];
+  __shared__ int s_wide;                         // some unit's widening overflowed
   __shared__ int s_nseg;
   __shared__ int s_lovf;
   __shared__ long long s_lo;                     // the current block: first rotation ...
@@ -897,6 +890,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
       s_nb = nb;
       s_nseg = 0;
       s_lovf = 0;
+      s_wide = 0;
     }
     __syncthreads();
     const int nb = s_nb;
@@ -905,37 +899,56 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
       const int rc = nb >> 1;
       if (tid < 9 * nb) Rb[tid] = rotation_entry(p.rot, s_lo + tid / 9, tid % 9);
       __syncthreads();
-      if (tid < 3) {  // widening of the window per axis
-        double d = 0.0;
-        for (int t = 0; t < nb; ++t) {
-          double s = 0.0;
-          for (int l = 0; l < 3; ++l) s += fabs(Rb[9 * t + 3 * tid + l] - Rb[9 * rc + 3 * tid + l]) * p.xa_s[l];
-          d = fmax(d, s);
-        }
-        // (a widening beyond 2^27 units -- huge steps -- leaves the block to vote_kernel)
-        s_dq[tid] = d < 134217728.0 ? (int)ceil(d * (1.0 + 1e-9)) + 3 : -1;
-      }
       const double* R = Rb + 9 * rc;
-      // ---- A at the centre rotation: fixed-point points and unit boxes
+      // ---- A at the centre rotation: fixed-point points, and per unit the
+      //      bound on its points' motion over the block's rotations,
+      //      |(R_t - Rc) x|_k <= sum_l |R_t,kl - Rc,kl| max_unit |x_l|
+      //      (fixed-point units, + 3 for the two roundings), and its box
+      //      widened by that bound
       for (int a = warp; a < p.nxt; a += nwarps) {
         const int2 U = __ldg(reinterpret_cast<const int2*>(p.xt + a));
         const bool valid = lane < U.y;
         const int i = U.x + (valid ? lane : 0);
         int4 v = make_int4(0, 0, 0, 0);
+        int ax0 = 0, ax1 = 0, ax2 = 0;
         if (valid) {
           const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
           v.x = __double2int_rn(dmul(rot_row(R, 0, x0, x1, x2), p.inv_s));
           v.y = __double2int_rn(dmul(rot_row(R, 1, x0, x1, x2), p.inv_s));
           v.z = __double2int_rn(dmul(rot_row(R, 2, x0, x1, x2), p.inv_s));
           P[i] = v;
+          ax0 = (int)ceil(fabs(x0) * p.inv_s);
+          ax1 = (int)ceil(fabs(x1) * p.inv_s);
+          ax2 = (int)ceil(fabs(x2) * p.inv_s);
         }
-        const int4 blo = make_int4(__reduce_min_sync(0xffffffffu, valid ? v.x : INT_MAX),
-                                   __reduce_min_sync(0xffffffffu, valid ? v.y : INT_MAX),
-                                   __reduce_min_sync(0xffffffffu, valid ? v.z : INT_MAX), U.x);
-        const int4 bhi = make_int4(__reduce_max_sync(0xffffffffu, valid ? v.x : INT_MIN),
-                                   __reduce_max_sync(0xffffffffu, valid ? v.y : INT_MIN),
-                                   __reduce_max_sync(0xffffffffu, valid ? v.z : INT_MIN), U.x + U.y);
-        if (lane == 0) { XB[2 * a] = blo; XB[2 * a + 1] = bhi; }
+        ax0 = __reduce_max_sync(0xffffffffu, ax0);
+        ax1 = __reduce_max_sync(0xffffffffu, ax1);
+        ax2 = __reduce_max_sync(0xffffffffu, ax2);
+        int dq = 0;
+        if (lane < 3) {  // axis `lane`
+          double d = 0.0;
+          for (int t = 0; t < nb; ++t) {
+            const double* Rt = Rb + 9 * t + 3 * lane;
+            const double* Rc = R + 3 * lane;
+            d = fmax(d, fabs(Rt[0] - Rc[0]) * ax0 + fabs(Rt[1] - Rc[1]) * ax1 + fabs(Rt[2] - Rc[2]) * ax2);
+          }
+          // (a widening beyond 2^27 units -- huge steps -- leaves the block to vote_kernel)
+          dq = d < 134217728.0 ? (int)ceil(d * (1.0 + 1e-9)) + 3 : -1;
+        }
+        const int dq0 = __shfl_sync(0xffffffffu, dq, 0), dq1 = __shfl_sync(0xffffffffu, dq, 1),
+                  dq2 = __shfl_sync(0xffffffffu, dq, 2);
+        const int4 blo = make_int4(__reduce_min_sync(0xffffffffu, valid ? v.x : INT_MAX) - dq0,
+                                   __reduce_min_sync(0xffffffffu, valid ? v.y : INT_MAX) - dq1,
+                                   __reduce_min_sync(0xffffffffu, valid ? v.z : INT_MAX) - dq2, U.x);
+        const int4 bhi = make_int4(__reduce_max_sync(0xffffffffu, valid ? v.x : INT_MIN) + dq0,
+                                   __reduce_max_sync(0xffffffffu, valid ? v.y : INT_MIN) + dq1,
+                                   __reduce_max_sync(0xffffffffu, valid ? v.z : INT_MIN) + dq2, U.x + U.y);
+        if (lane == 0) {
+          XB[2 * a] = blo;
+          XB[2 * a + 1] = bhi;
+          DQ[a] = make_int4(dq0, dq1, dq2, 0);
+          if ((dq0 | dq1 | dq2) < 0) s_wide = 1;
+        }
       }
       __syncthreads();
       for (int c = warp; c < nxc; c += nwarps) {
@@ -952,14 +965,11 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
         if (lane == 0) { CB[2 * c] = blo; CB[2 * c + 1] = bhi; }
       }
       __syncthreads();
-      const int dq0 = s_dq[0], dq1 = s_dq[1], dq2 = s_dq[2];
-      const int wq0 = (int)p.W0 + dq0, wq1 = (int)p.W1 + dq1, wq2 = (int)p.W2 + dq2;
-      const unsigned Wp0 = p.W0 + 2u * (unsigned)dq0, Wp1 = p.W1 + 2u * (unsigned)dq1,
-                     Wp2 = p.W2 + 2u * (unsigned)dq2;
 
-      // ---- build the block's list (rounds of reference groups, as vote_kernel)
+      // ---- build the block's list (rounds of reference groups, as vote_kernel,
+      //      against the widened unit boxes)
       int fill = 0;
-      const bool wide = (dq0 | dq1 | dq2) < 0;  // block-uniform
+      const bool wide = s_wide != 0;  // block-uniform
       bool room = !wide;
       unsigned wcount = 0;
       for (int b0 = 0, gnext = gmax; b0 < (wide ? 0 : p.nyt);) {
@@ -972,7 +982,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
             const YTile yg = load_ytile(p.yt, b0 + k);
             unsigned mk = 0;
             for (int c = 0; c < nxc; ++c)
-              if (boxes_meet_w(yg, CB[2 * c], CB[2 * c + 1], dq0, dq1, dq2, wq0, wq1, wq2)) mk |= 1u << c;
+              if (boxes_meet(p, yg, CB[2 * c], CB[2 * c + 1])) mk |= 1u << c;
             gmask[k] = mk;
           }
         __syncthreads();
@@ -980,12 +990,10 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           const YTile yt = load_ytile(p.yt, b);
           for (int a0 = 0; a0 < p.nxt; a0 += 32) {
             if (masks ? !((gmask[b - b0] >> (a0 >> 5)) & 1u)
-                      : (nxc > 1 && !boxes_meet_w(yt, CB[2 * (a0 >> 5)], CB[2 * (a0 >> 5) + 1], dq0, dq1,
-                                                  dq2, wq0, wq1, wq2)))
+                      : (nxc > 1 && !boxes_meet(p, yt, CB[2 * (a0 >> 5)], CB[2 * (a0 >> 5) + 1])))
               continue;
             const int a = a0 + lane;
-            const bool ov = a < p.nxt &&
-                            boxes_meet_w(yt, XB[2 * a], XB[2 * a + 1], dq0, dq1, dq2, wq0, wq1, wq2);
+            const bool ov = a < p.nxt && boxes_meet(p, yt, XB[2 * a], XB[2 * a + 1]);
             const unsigned m = __ballot_sync(0xffffffffu, ov);
             if (m) {
               int slot = 0;
@@ -1013,14 +1021,18 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           const int j = yt.start + (valid ? lane : 0);
           int4 Y = __ldg(&p.yq[j]);
           if (!valid) Y = make_int4(kNoRef, 0, 0, 0);
-          const int y0 = (int)((unsigned)Y.x + (unsigned)dq0), y1 = (int)((unsigned)Y.y + (unsigned)dq1),
-                    y2 = (int)((unsigned)Y.z + (unsigned)dq2);
+          const int4 dq = DQ[unit & 0xffffu];  // the unit's widening
+          const int y0 = (int)((unsigned)Y.x + (unsigned)dq.x), y1 = (int)((unsigned)Y.y + (unsigned)dq.y),
+                    y2 = (int)((unsigned)Y.z + (unsigned)dq.z);
+          const unsigned Wp0 = p.W0 + 2u * (unsigned)dq.x, Wp1 = p.W1 + 2u * (unsigned)dq.y,
+                         Wp2 = p.W2 + 2u * (unsigned)dq.z;
           bool sok = false;
           int4 Pl = make_int4(0, 0, 0, 0);
           if (lane < U.y) {
             Pl = lds_v4(P_sh + 16u * (unsigned)(U.x + lane));
-            sok = (yt.hi[0] - Pl.x >= -dq0) & (yt.lo[0] - Pl.x < wq0) & (yt.hi[1] - Pl.y >= -dq1) &
-                  (yt.lo[1] - Pl.y < wq1) & (yt.hi[2] - Pl.z >= -dq2) & (yt.lo[2] - Pl.z < wq2);
+            sok = (yt.hi[0] - Pl.x >= -dq.x) & (yt.lo[0] - Pl.x < (int)p.W0 + dq.x) &
+                  (yt.hi[1] - Pl.y >= -dq.y) & (yt.lo[1] - Pl.y < (int)p.W1 + dq.y) &
+                  (yt.hi[2] - Pl.z >= -dq.z) & (yt.lo[2] - Pl.z < (int)p.W2 + dq.z);
           }
           const unsigned sm = __ballot_sync(0xffffffffu, sok);
           const int nsrc = __popc(sm);
@@ -1204,7 +1216,8 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
   size_t b = 0;
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n_pad * 16;
-  b += (size_t)(p.nxt + (p.nxt + 31) / 32) * 32 + kMaxBlockRot * 9 * 8 + 4 * 32 * 4 + (size_t)p.unit_cap * 4;
+  b += (size_t)(p.nxt + (p.nxt + 31) / 32) * 32 + (size_t)p.nxt * 16 + kMaxBlockRot * 9 * 8 + 4 * 32 * 4 +
+       (size_t)p.unit_cap * 4;  // (unit boxes, chunk boxes, the block kernel's per-unit widening, ...)
   b += (size_t)(threads / 32) * kRare * 8;
   b += (size_t)(threads / 32) * 32 * 16;  // per-warp staged sources
   return b;
