@@ -110,7 +110,7 @@ int dses_plan_info(const dses_plan* plan, int64_t* frac_bits, int64_t* x_tiles, 
 int dses_plan_set_vote_grid(dses_plan* plan, int64_t ctas);
 /* Rotation blocks: runs of `len` consecutive rotations of a grid row share one
  * candidate-pair list; 0 = the per-rotation vote kernel.
- * Default: 5 when the translation window is small against the reference cloud,
+ * Default: 7 when the translation window is small against the reference cloud,
  * else 0 (environment DSES_BLOCK_L overrides).  list_cap: list entries per CTA
  * (0 = default 2^17; blocks whose list overflows are re-run by the
  * per-rotation kernel).  Results do not depend on either. */

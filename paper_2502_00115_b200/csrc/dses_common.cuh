@@ -43,8 +43,8 @@ constexpr int kPartFlag = 1 << 18;   // the point has a dedup partner
 constexpr int kSplitFlag = 1 << 19;  // its component spans several groups (always exact)
 constexpr int kCompOffShift = 20;    // bits 20..23: its offset from the component's first point
                                      // (components are contiguous in tile order)
-constexpr int kMaxBlockRot = 8;   // rotations per block (the block kernel's R area in shared memory)
-constexpr int kDefaultBlockL = 5; // rotations per block unless DSES_BLOCK_L says otherwise
+constexpr int kMaxBlockRot = 16;  // rotations per block (the block kernel's R area in shared memory)
+constexpr int kDefaultBlockL = 7; // rotations per block unless DSES_BLOCK_L says otherwise
 constexpr double kBlockWindowFrac = 0.15;  // blocks when the window is below this part of the cloud
 constexpr int kBlockListCap = 1 << 17;  // candidate-list entries per CTA (512 KiB)
 constexpr int kRiskBits = 10;     // fraction buckets per axis of the guard-band risk bitmaps

@@ -880,9 +880,10 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
       int nb = -1;
       int64_t lo = 0;
       while (bclaim < nblk) {
-        const int64_t row = row0 + bclaim / bpr, c0 = (bclaim % bpr) * BL;
-        lo = max(row * side + c0, p.r_begin);
-        const int64_t hi = min(row * side + min(side, c0 + BL), r_end);
+        // a row's bpr blocks are balanced: sizes differ by at most one
+        const int64_t row = row0 + bclaim / bpr, k = bclaim % bpr;
+        lo = max(row * side + k * side / bpr, p.r_begin);
+        const int64_t hi = min(row * side + (k + 1) * side / bpr, r_end);
         bclaim = (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull);
         if (hi > lo) { nb = (int)(hi - lo); break; }
       }
