@@ -1228,15 +1228,10 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.redo = nullptr;
   v.redo_n = nullptr;
   v.blk_L = 0;
-  {  // rotation-block kernel: entry encoding and the sources' extent per axis
+  {  // rotation-block kernel: list entry encoding i << jbits | j (0: no blocks)
     int jb = 1;
     while (jb < 31 && ((int64_t)1 << jb) <= P->m_pad) ++jb;  // j <= m_pad (sentinel)
     v.jbits = (((uint64_t)std::max<int64_t>(n - 1, 0) << jb) >> 32) == 0 ? jb : 0;
-    for (int k = 0; k < 3; ++k) {
-      double a = 0;
-      for (int64_t i = 0; i < n; ++i) a = std::max(a, std::fabs(xs[3 * i + k]));
-      v.xa_s[k] = a * inv_s;
-    }
     static const int envL = [] {
       const char* e = getenv("DSES_BLOCK_L");
       return e && *e ? std::max(0, std::min(kMaxBlockRot, atoi(e))) : -1;

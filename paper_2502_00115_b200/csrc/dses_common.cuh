@@ -125,14 +125,14 @@ struct VoteParams {
   int hist_words;             // u32 words per histogram (padded to a multiple of 4)
   int n_pad;
   int count16;                // two 16-bit counts per word (n < 65536)
-  // rotation blocks (vote_blocks_kernel): runs of blk_L consecutive rotations
-  // of a grid row share one candidate-pair list built at the block's centre
-  // rotation with the window widened by the block's maximal point motion
+  // rotation blocks (vote_blocks_kernel): runs of up to blk_L consecutive
+  // rotations of a grid row share one candidate-pair list built at the
+  // block's centre rotation with each source unit's window widened by its
+  // points' maximal motion over the block
   int blk_L;                  // 0: per-rotation kernel only
   int jbits;                  // list entry = i << jbits | j; j = m_pad is the empty sentinel slot
   int list_cap;               // entries per CTA slab (multiple of 32)
   unsigned* list;             // per-CTA slabs
-  double xa_s[3];             // max_i |x_i| per axis in fixed-point units (x * inv_s)
   long long* redo;            // rotations of blocks whose list overflowed ...
   unsigned long long* redo_n; // ... and their number: vote_kernel runs them (redo mode)
 };
