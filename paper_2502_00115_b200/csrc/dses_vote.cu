@@ -69,6 +69,19 @@ __device__ __forceinline__ bool boxes_meet(const VoteParams& p, const YTile& yt,
          (yt.lo[1] - hi.y < (int)p.W1) & (yt.hi[2] - lo.z >= 0) & (yt.lo[2] - hi.z < (int)p.W2);
 }
 
+// Lane index and lower-lanes mask from the special registers (one S2R each
+// wherever the compiler re-materialises them).
+__device__ __forceinline__ unsigned lane_sr() {
+  unsigned r;
+  asm("mov.u32 %0, %%laneid;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned lanemask_lt_sr() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
 // 32-bit shared-memory accessors (shared window addresses computed once).
 __device__ __forceinline__ int4 lds_v4(uint32_t a) {
   int4 v;
@@ -802,7 +815,7 @@ __device__ __forceinline__ bool emit_entries(const VoteParams& p, unsigned m, un
 #endif
 __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(const VoteParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = (int)lane_sr();
   const int nthreads = blockDim.x, nwarps = nthreads >> 5, warp = tid >> 5;
 
   // the per-rotation kernel's layout (hsmem, psmem)
@@ -830,8 +843,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   int* s_nunits = red + 96;
   int* s_next = red + 97;
   int* s_ovf = red + 98;
-  const unsigned lanemask_lt = (1u << lane) - 1u;
-  const uint32_t P_sh = (uint32_t)__cvta_generic_to_shared(P);
+  const unsigned lanemask_lt = lanemask_lt_sr();
   __shared__ __align__(16) unsigned kc[12];
   __shared__ int s_wide;                         // some unit's widening overflowed
   __shared__ int s_nseg;
@@ -845,13 +857,17 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
     kc[5] = (unsigned)p.d1; kc[6] = (unsigned)p.d2; kc[7] = (unsigned)p.F;
     kc[8] = (uint32_t)__cvta_generic_to_shared(hist);
     kc[9] = 0u - (1u << p.F);
-    kc[10] = kc[11] = 0u;
+    kc[10] = (uint32_t)__cvta_generic_to_shared(P);
+    kc[11] = (1u << p.jbits) - 1u;
     g_exR = Rb;
     g_exP = P;
     g_exH = hist;
   }
   __syncthreads();
+  // constants through shared memory: re-loaded where needed rather than
+  // re-derived from the kernel parameters (register pressure at 64)
   const uint32_t hist_sh = kc[8];
+  const uint32_t P_sh = kc[10];
   Lane L;
   asm volatile("mov.u32 %0, %1;" : "=r"(L.rare_sh) : "r"((uint32_t)__cvta_generic_to_shared(rare)));
   L.nrare = 0;
@@ -863,7 +879,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
 
   const unsigned slab = (unsigned)blockIdx.x * (unsigned)p.list_cap;  // this CTA's list (entry offset)
   const uint32_t nseg_sh = (uint32_t)__cvta_generic_to_shared(&s_nseg);
-  const unsigned jmask = (1u << p.jbits) - 1u;
+  const unsigned jmask = kc[11];
   const unsigned pad_entry = (unsigned)p.m_pad;  // i = 0, j = the empty sentinel slot
   const int gmax = max(1, min(min(p.nyt, p.unit_cap / 4), p.unit_cap - p.nxt - 1));
   const bool masks = nxc > 1 && nxc <= 32;
@@ -917,7 +933,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           v.x = __double2int_rn(dmul(rot_row(R, 0, x0, x1, x2), p.inv_s));
           v.y = __double2int_rn(dmul(rot_row(R, 1, x0, x1, x2), p.inv_s));
           v.z = __double2int_rn(dmul(rot_row(R, 2, x0, x1, x2), p.inv_s));
-          P[i] = v;
+          sts_v4(P_sh + 16u * (unsigned)i, v);
           ax0 = (int)ceil(fabs(x0) * p.inv_s);
           ax1 = (int)ceil(fabs(x1) * p.inv_s);
           ax2 = (int)ceil(fabs(x2) * p.inv_s);
@@ -1077,9 +1093,10 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           if (t0 > 0) {
             for (int i = tid; i < p.n; i += nthreads) {
               const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
-              P[i] = make_int4(__double2int_rn(dmul(rot_row(Rt, 0, x0, x1, x2), p.inv_s)),
+              sts_v4(P_sh + 16u * (unsigned)i,
+                     make_int4(__double2int_rn(dmul(rot_row(Rt, 0, x0, x1, x2), p.inv_s)),
                                __double2int_rn(dmul(rot_row(Rt, 1, x0, x1, x2), p.inv_s)),
-                               __double2int_rn(dmul(rot_row(Rt, 2, x0, x1, x2), p.inv_s)), 0);
+                               __double2int_rn(dmul(rot_row(Rt, 2, x0, x1, x2), p.inv_s)), 0));
             }
           }
           if (tid == 0) g_exR = Rt;
@@ -1094,11 +1111,10 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           }
           // (the next segment's entry is loaded one iteration ahead: the list
           // comes from L2)
-          unsigned e_next = warp < nseg ? __ldcg(p.list + (slab + 32u * (unsigned)warp + (unsigned)lane)) : pad_entry;
+          unsigned e_next = __ldcg(p.list + (slab + 32u * (unsigned)min(warp, max(nseg - 1, 0)) + (unsigned)lane));
           for (int sg = warp; sg < nseg; sg += nwarps) {
             const unsigned e = e_next;
-            if (sg + nwarps < nseg)
-              e_next = __ldcg(p.list + (slab + 32u * (unsigned)(sg + nwarps) + (unsigned)lane));
+            e_next = __ldcg(p.list + (slab + 32u * (unsigned)min(sg + nwarps, nseg - 1) + (unsigned)lane));
             const int i = (int)(e >> p.jbits), j = (int)(e & jmask);
             const int4 Pi = lds_v4(P_sh + 16u * (unsigned)i);
             const int4 Y = __ldg(&p.yq[j]);
