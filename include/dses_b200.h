@@ -115,6 +115,8 @@ int dses_plan_set_vote_grid(dses_plan* plan, int64_t ctas);
  * (0 = default 2^17; blocks whose list overflows are re-run by the
  * per-rotation kernel).  Results do not depend on either. */
 int dses_plan_set_block_rotations(dses_plan* plan, int64_t len, int64_t list_cap);
+/* The block length grid searches of this plan use (0: the per-rotation kernel). */
+int dses_plan_block_rotations(const dses_plan* plan, int64_t* len);
 
 /* ---- the reference kernel seams ------------------------------------------ */
 /* Per-rotation histogram mode (count, flat bin, tied bins) for `nrot`

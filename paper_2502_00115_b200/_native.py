@@ -69,6 +69,7 @@ _SIGS = [
     ("dses_plan_info", ctypes.c_int, [_vp, _ip, _ip, _ip, _ip]),
     ("dses_plan_set_vote_grid", ctypes.c_int, [_vp, _i64]),
     ("dses_plan_set_block_rotations", ctypes.c_int, [_vp, _i64, _i64]),
+    ("dses_plan_block_rotations", ctypes.c_int, [_vp, _ip]),
     ("dses_mode_batch", ctypes.c_int, [_vp, _dp, _i64, _ip, _ip, _ip, _vp]),
     ("dses_mode_grid", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, _ip, _ip, _ip, _vp]),
     ("dses_refine_batch", ctypes.c_int, [_vp, _dp, _dp, _i64, ctypes.c_int, ctypes.c_double, _dp,
@@ -279,6 +280,12 @@ class Plan:
     def set_vote_grid(self, ctas):
         """Testing hook: cap the vote kernel's persistent grid (0 = default)."""
         check(self._L.dses_plan_set_vote_grid(self._h, int(ctas)), "dses_plan_set_vote_grid")
+
+    def block_rotations(self):
+        """Block length of this plan's grid searches (0: per-rotation kernel)."""
+        v = ctypes.c_int64()
+        check(self._L.dses_plan_block_rotations(self._h, ctypes.byref(v)), "dses_plan_block_rotations")
+        return v.value
 
     def set_block_rotations(self, n, list_cap=0):
         """Rotation-block length of the vote (0 = the per-rotation kernel) and

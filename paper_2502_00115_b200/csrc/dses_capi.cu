@@ -1538,6 +1538,12 @@ extern "C" int dses_plan_set_vote_grid(dses_plan* P, int64_t ctas) {
   return DSES_OK;
 }
 
+extern "C" int dses_plan_block_rotations(const dses_plan* P, int64_t* len) {
+  if (!P || !len) return fail(DSES_E_INVALID, "null argument");
+  *len = (P->blk_L > 0 && P->hsmem && P->psmem && P->F > 0 && P->vp.jbits > 0 && !P->sparse) ? P->blk_L : 0;
+  return DSES_OK;
+}
+
 extern "C" int dses_plan_set_block_rotations(dses_plan* P, int64_t len, int64_t list_cap) {
   if (!P) return fail(DSES_E_INVALID, "null plan");
   if (len < 0 || len > kMaxBlockRot) return fail(DSES_E_INVALID, "block length must be in [0, %d]", kMaxBlockRot);
