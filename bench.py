@@ -534,7 +534,7 @@ def workload_line(name, args, rank, world, local, steps=10, warmup=3):
         if world > 1:
             dist.all_reduce(tb, op=dist.ReduceOp.MAX)
         ms_batch = float(tb.item())
-        blk = plans[0].block_rotations()
+        blk = plans[0].blocks()
         for pl in plans:
             pl.close()
         R = cfg.rotation_count
@@ -546,8 +546,8 @@ def workload_line(name, args, rank, world, local, steps=10, warmup=3):
             "config": {"workload": describe(name, c, cfg, preps[0].x.shape[0], preps[0].y.shape[0]),
                        "metric": cfg.metric.kind, "rotations": R},
             "vote_kernel_ms_per_step": sum(r["ms_vote_kernel"] for r in res) / steps,
-            "vote_path": (f"vote_blocks_kernel: blocks of up to {blk} consecutive grid rotations share one "
-                          "candidate-pair list (pairs_evaluated = list entries voted)") if blk else
+            "vote_path": (f"vote_blocks_kernel: blocks of {blk[0]}x{blk[1]}x{blk[2]} neighbouring grid rotations "
+                          "share one candidate-pair list (pairs_evaluated = list entries voted)") if blk[0] else
                          "vote_kernel (per rotation)",
             "pairs_evaluated_per_rotation": sum(r["pairs_evaluated"] for r in res) / (steps * R),
             "e2e": {"value": tot / (ms_batch * 1e-3), "unit": UNIT,

@@ -108,15 +108,17 @@ int dses_plan_info(const dses_plan* plan, int64_t* frac_bits, int64_t* x_tiles, 
  * (0 = the default, one wave of resident CTAs).  Results do not depend on it
  * (tests/test_gpu_api.py checks 1, 7 and 148 CTAs against the default). */
 int dses_plan_set_vote_grid(dses_plan* plan, int64_t ctas);
-/* Rotation blocks: runs of `len` consecutive rotations of a grid row share one
- * candidate-pair list; 0 = the per-rotation vote kernel.
- * Default: 7 when the translation window is small against the reference cloud,
- * else 0 (environment DSES_BLOCK_L overrides).  list_cap: list entries per CTA
- * (0 = default 2^17; blocks whose list overflows are re-run by the
- * per-rotation kernel).  Results do not depend on either. */
-int dses_plan_set_block_rotations(dses_plan* plan, int64_t len, int64_t list_cap);
-/* The block length grid searches of this plan use (0: the per-rotation kernel). */
-int dses_plan_block_rotations(const dses_plan* plan, int64_t* len);
+/* Rotation blocks: boxes of shape[0] x shape[1] x shape[2]
+ * neighbouring grid rotations (along the three Euler-index axes, at most 32
+ * rotations) share one candidate-pair list; 0,0,0 = the per-rotation vote
+ * kernel.  Default: 1,1,7 when the translation window is small against the
+ * reference cloud, else 0,0,0 (environment DSES_BLOCK_SHAPE="a,b,c"
+ * overrides).  list_cap: list entries per CTA (0 = default 2^17; blocks whose
+ * list overflows are re-run by the per-rotation kernel).  Results do not
+ * depend on either. */
+int dses_plan_set_blocks(dses_plan* plan, const int64_t shape[3], int64_t list_cap);
+/* The block shape this plan's grid searches use (0,0,0: per-rotation kernel). */
+int dses_plan_blocks(const dses_plan* plan, int64_t shape[3]);
 
 /* ---- the reference kernel seams ------------------------------------------ */
 /* Per-rotation histogram mode (count, flat bin, tied bins) for `nrot`

@@ -68,8 +68,8 @@ _SIGS = [
     ("dses_plan_destroy", ctypes.c_int, [_vp]),
     ("dses_plan_info", ctypes.c_int, [_vp, _ip, _ip, _ip, _ip]),
     ("dses_plan_set_vote_grid", ctypes.c_int, [_vp, _i64]),
-    ("dses_plan_set_block_rotations", ctypes.c_int, [_vp, _i64, _i64]),
-    ("dses_plan_block_rotations", ctypes.c_int, [_vp, _ip]),
+    ("dses_plan_set_blocks", ctypes.c_int, [_vp, _ip, _i64]),
+    ("dses_plan_blocks", ctypes.c_int, [_vp, _ip]),
     ("dses_mode_batch", ctypes.c_int, [_vp, _dp, _i64, _ip, _ip, _ip, _vp]),
     ("dses_mode_grid", ctypes.c_int, [_vp, ctypes.POINTER(Grid), _i64, _i64, _ip, _ip, _ip, _vp]),
     ("dses_refine_batch", ctypes.c_int, [_vp, _dp, _dp, _i64, ctypes.c_int, ctypes.c_double, _dp,
@@ -281,18 +281,20 @@ class Plan:
         """Testing hook: cap the vote kernel's persistent grid (0 = default)."""
         check(self._L.dses_plan_set_vote_grid(self._h, int(ctas)), "dses_plan_set_vote_grid")
 
-    def block_rotations(self):
-        """Block length of this plan's grid searches (0: per-rotation kernel)."""
-        v = ctypes.c_int64()
-        check(self._L.dses_plan_block_rotations(self._h, ctypes.byref(v)), "dses_plan_block_rotations")
-        return v.value
+    def blocks(self):
+        """Block shape of this plan's grid searches ((0, 0, 0): per-rotation kernel)."""
+        v = np.zeros(3, dtype=np.int64)
+        check(self._L.dses_plan_blocks(self._h, iptr(v)), "dses_plan_blocks")
+        return tuple(int(a) for a in v)
 
-    def set_block_rotations(self, n, list_cap=0):
-        """Rotation-block length of the vote (0 = the per-rotation kernel) and
-        the list entries per CTA (0 = default; testing hook for the overflow
-        path)."""
-        check(self._L.dses_plan_set_block_rotations(self._h, int(n), int(list_cap)),
-              "dses_plan_set_block_rotations")
+    def set_blocks(self, shape, list_cap=0):
+        """Rotation-block shape of the vote ((0, 0, 0) or 0 = the per-rotation
+        kernel; an int n = (1, 1, n)) and the list entries per CTA (0 =
+        default; testing hook for the overflow path)."""
+        if isinstance(shape, int):
+            shape = (0, 0, 0) if shape == 0 else (1, 1, shape)
+        v = np.ascontiguousarray(shape, dtype=np.int64).reshape(3)
+        check(self._L.dses_plan_set_blocks(self._h, iptr(v), int(list_cap)), "dses_plan_set_blocks")
 
     def mode_batch(self, rots, stream=None):
         rots = np.ascontiguousarray(rots, dtype=np.float64).reshape(-1, 9)

@@ -6,6 +6,7 @@
 // the small host<->device scalar traffic between stages.  The Python layer
 // (paper_2502_00115_b200/engines.py) mirrors gridreg's API and exceptions on top.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -283,7 +284,7 @@ struct dses_plan {
   bool hsmem = true, psmem = true;
   int vote_grid = 0, vote_threads = kVoteThreads;
   int vote_grid_cap = 0;                               // testing hook: 0 = one wave
-  int blk_L = 0;                                       // rotation-block length (0: per-rotation kernel)
+  int blk_s[3] = {0, 0, 0};                            // rotation-block sides (0: per-rotation kernel)
   int blk_cap = kBlockListCap;                         // list entries per CTA (testing hook)
   DevBuf blist, redo;                                  // block kernel: candidate lists, redo rotations
   // device data
@@ -1065,6 +1066,17 @@ static int ref_fixed(const RefTopo& T, double inv_bin, int F, const int64_t ilo[
   return DSES_OK;
 }
 
+// Block shape: all three sides >= 1 with at most kMaxBlockRot rotations, or
+// all zero (the per-rotation kernel).
+static int set_block_shape(dses_plan* P, const int* sh) {
+  const bool off = sh[0] == 0 && sh[1] == 0 && sh[2] == 0;
+  if (!off && (sh[0] < 1 || sh[1] < 1 || sh[2] < 1 || (int64_t)sh[0] * sh[1] * sh[2] > kMaxBlockRot))
+    return fail(DSES_E_INVALID, "block shape must be 0,0,0 or three sides >= 1 with at most %d rotations",
+                kMaxBlockRot);
+  for (int k = 0; k < 3; ++k) P->blk_s[k] = sh[k];
+  return DSES_OK;
+}
+
 int build_plan(dses_plan* P, const double* x, const double* y) {
   const int64_t n = P->n, m = P->m;
   cudaStream_t st = upload_stream(P->device);
@@ -1227,14 +1239,17 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
   v.stats = P->stats.as<unsigned long long>();
   v.redo = nullptr;
   v.redo_n = nullptr;
-  v.blk_L = 0;
+  v.blk_s[0] = v.blk_s[1] = v.blk_s[2] = 0;
   {  // rotation-block kernel: list entry encoding i << jbits | j (0: no blocks)
     int jb = 1;
     while (jb < 31 && ((int64_t)1 << jb) <= P->m_pad) ++jb;  // j <= m_pad (sentinel)
     v.jbits = (((uint64_t)std::max<int64_t>(n - 1, 0) << jb) >> 32) == 0 ? jb : 0;
-    static const int envL = [] {
-      const char* e = getenv("DSES_BLOCK_L");
-      return e && *e ? std::max(0, std::min(kMaxBlockRot, atoi(e))) : -1;
+    // DSES_BLOCK_SHAPE="a,b,c" overrides the default block shape ("0,0,0": off)
+    static const std::array<int, 3> env_shape = [] {
+      std::array<int, 3> v{-1, -1, -1};
+      const char* e = getenv("DSES_BLOCK_SHAPE");
+      if (e && *e && sscanf(e, "%d,%d,%d", &v[0], &v[1], &v[2]) != 3) v = {-1, -1, -1};
+      return v;
     }();
     // Rotation blocks pay off when a source point's window holds few of a
     // reference group's points (the per-rotation kernel then idles most lanes
@@ -1244,7 +1259,11 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     // faster (c2: 10.1 vs 18 ms with blocks).
     double win = 0;
     for (int k = 0; k < 3; ++k) win = std::max(win, (double)P->dims[k] * P->bin);
-    P->blk_L = envL >= 0 ? envL : (win < kBlockWindowFrac * topo->ext ? kDefaultBlockL : 0);
+    const bool small = win < kBlockWindowFrac * topo->ext;
+    for (int k = 0; k < 3; ++k) P->blk_s[k] = small ? kDefaultBlockShape[k] : 0;
+    if (env_shape[0] >= 0 && set_block_shape(P, env_shape.data()) != DSES_OK) {
+      for (int k = 0; k < 3; ++k) P->blk_s[k] = 0;
+    }
   }
   v.count16 = n < 65536 ? 1 : 0;
   const int64_t words = v.count16 ? (v.nbins + 1) / 2 : v.nbins;
@@ -1356,8 +1375,11 @@ int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_cou
 // Rotation-block kernel eligibility: grid rotations (blocks are runs of one
 // grid row), shared-memory histogram and points, fixed-point binning, and
 // list entries i << jbits | j in 32 bits.
+static bool blocks_enabled(const dses_plan* P) {
+  return P->blk_s[0] > 0 && P->hsmem && P->psmem && P->F > 0 && P->vp.jbits > 0 && !P->sparse;
+}
 static bool use_blocks(const dses_plan* P, const RotSource& rs) {
-  return P->blk_L > 0 && rs.cth && !rs.rots && P->hsmem && P->psmem && P->F > 0 && P->vp.jbits > 0;
+  return blocks_enabled(P) && rs.cth && !rs.rots;
 }
 
 int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count, cudaStream_t st) {
@@ -1396,7 +1418,7 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
   if (use_blocks(P, rs)) {
     // rotation blocks: one candidate list per run of blk_L rotations; blocks
     // whose list overflows the slab are re-run by the per-rotation kernel
-    v.blk_L = P->blk_L;
+    for (int k = 0; k < 3; ++k) v.blk_s[k] = P->blk_s[k];
     v.list_cap = P->blk_cap;
     CK(P->blist.ensure((size_t)grid * v.list_cap * 4, st));
     CK(P->redo.ensure(8 * (size_t)(r_count + 1), st));
@@ -1538,17 +1560,19 @@ extern "C" int dses_plan_set_vote_grid(dses_plan* P, int64_t ctas) {
   return DSES_OK;
 }
 
-extern "C" int dses_plan_block_rotations(const dses_plan* P, int64_t* len) {
-  if (!P || !len) return fail(DSES_E_INVALID, "null argument");
-  *len = (P->blk_L > 0 && P->hsmem && P->psmem && P->F > 0 && P->vp.jbits > 0 && !P->sparse) ? P->blk_L : 0;
+extern "C" int dses_plan_blocks(const dses_plan* P, int64_t* shape) {
+  if (!P || !shape) return fail(DSES_E_INVALID, "null argument");
+  for (int k = 0; k < 3; ++k) shape[k] = blocks_enabled(P) ? P->blk_s[k] : 0;
   return DSES_OK;
 }
 
-extern "C" int dses_plan_set_block_rotations(dses_plan* P, int64_t len, int64_t list_cap) {
-  if (!P) return fail(DSES_E_INVALID, "null plan");
-  if (len < 0 || len > kMaxBlockRot) return fail(DSES_E_INVALID, "block length must be in [0, %d]", kMaxBlockRot);
+extern "C" int dses_plan_set_blocks(dses_plan* P, const int64_t* shape, int64_t list_cap) {
+  if (!P || !shape) return fail(DSES_E_INVALID, "null argument");
   if (list_cap < 0 || list_cap > kBlockListCap) return fail(DSES_E_INVALID, "list capacity must be in [0, %d]", kBlockListCap);
-  P->blk_L = (int)len;
+  const int sh[3] = {(int)std::max<int64_t>(std::min<int64_t>(shape[0], 1 << 20), -1),
+                     (int)std::max<int64_t>(std::min<int64_t>(shape[1], 1 << 20), -1),
+                     (int)std::max<int64_t>(std::min<int64_t>(shape[2], 1 << 20), -1)};
+  CK_STATUS(set_block_shape(P, sh));
   P->blk_cap = list_cap > 0 ? (int)((list_cap + 31) / 32 * 32) : kBlockListCap;
   return DSES_OK;
 }
@@ -1896,7 +1920,7 @@ static int reserve_search(dses_plan* P, int64_t nr, cudaStream_t st = 0) {
     if (!P->hsmem) CK(P->hist_g.ensure((size_t)grid * v.hist_words * 4, st));
     if (!P->psmem) CK(P->p_g.ensure((size_t)grid * v.n_pad * 16, st));
   }
-  if (P->blk_L > 0 && P->hsmem && P->psmem && P->F > 0 && P->vp.jbits > 0 && !P->sparse) {
+  if (blocks_enabled(P)) {
     CK(P->blist.ensure((size_t)P->vote_grid * P->blk_cap * 4, st));  // rotation-block lists
     CK(P->redo.ensure(8 * (size_t)(nr + 1), st));
   }

@@ -43,9 +43,12 @@ constexpr int kPartFlag = 1 << 18;   // the point has a dedup partner
 constexpr int kSplitFlag = 1 << 19;  // its component spans several groups (always exact)
 constexpr int kCompOffShift = 20;    // bits 20..23: its offset from the component's first point
                                      // (components are contiguous in tile order)
-constexpr int kMaxBlockRot = 16;  // rotations per block (the block kernel's R area in shared memory)
-constexpr int kDefaultBlockL = 7; // rotations per block unless DSES_BLOCK_L says otherwise
+constexpr int kMaxBlockRot = 32;  // rotations per block (the block kernel's R area in shared memory)
+// shared-memory bytes of the rotation-matrix area (the block's rotations and
+// its centre), a multiple of 16 so that the int4 areas after it stay aligned
+constexpr int kRotAreaBytes = ((kMaxBlockRot + 1) * 9 * 8 + 15) / 16 * 16;
 constexpr double kBlockWindowFrac = 0.15;  // blocks when the window is below this part of the cloud
+constexpr int kDefaultBlockShape[3] = {1, 1, 7};  // rotations per block along the Euler-index axes
 constexpr int kBlockListCap = 1 << 17;  // candidate-list entries per CTA (512 KiB)
 constexpr int kRiskBits = 10;     // fraction buckets per axis of the guard-band risk bitmaps
 constexpr int kRiskWords = 3 * (1 << kRiskBits) / 32;  // words per group (3 axes)
@@ -125,11 +128,11 @@ struct VoteParams {
   int hist_words;             // u32 words per histogram (padded to a multiple of 4)
   int n_pad;
   int count16;                // two 16-bit counts per word (n < 65536)
-  // rotation blocks (vote_blocks_kernel): runs of up to blk_L consecutive
-  // rotations of a grid row share one candidate-pair list built at the
-  // block's centre rotation with each source unit's window widened by its
-  // points' maximal motion over the block
-  int blk_L;                  // 0: per-rotation kernel only
+  // rotation blocks (vote_blocks_kernel): boxes of up to blk_s[0] x blk_s[1]
+  // x blk_s[2] neighbouring grid rotations share one candidate-pair list
+  // built at the block's centre rotation with each source unit's window
+  // widened by its points' maximal motion over the block
+  int blk_s[3];               // sides along the three Euler-index axes (0: per-rotation kernel)
   int jbits;                  // list entry = i << jbits | j; j = m_pad is the empty sentinel slot
   int list_cap;               // entries per CTA slab (multiple of 32)
   unsigned* list;             // per-CTA slabs

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
   int4* CB = XB + 2 * p.nxt;                       // [2*nxc] their union per chunk
   off += (size_t)(p.nxt + nxc) * 32;
   double* R = reinterpret_cast<double*>(smem + off);
-  off += kMaxBlockRot * 9 * 8;                     // (the block kernel's layout: same offsets)
+  off += kRotAreaBytes;                            // (the block kernel's layout: same offsets)
   int* red = reinterpret_cast<int*>(smem + off);    // [3 * 32] reduction scratch + counters
   off += 4 * 32 * 4;
   unsigned* units = reinterpret_cast<unsigned*>(smem + off);  // [unit_cap] (group << 16 | unit)
@@ -829,8 +829,8 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   int4* CB = XB + 2 * p.nxt;
   int4* DQ = CB + 2 * nxc;                          // per unit: the widening per axis
   off += (size_t)(p.nxt + nxc) * 32 + (size_t)p.nxt * 16;
-  double* Rb = reinterpret_cast<double*>(smem + off);  // [kMaxBlockRot][9]
-  off += kMaxBlockRot * 9 * 8;
+  double* Rb = reinterpret_cast<double*>(smem + off);  // [kMaxBlockRot + 1][9]: block, centre
+  off += kRotAreaBytes;
   int* red = reinterpret_cast<int*>(smem + off);
   off += 4 * 32 * 4;
   unsigned* units = reinterpret_cast<unsigned*>(smem + off);
@@ -848,8 +848,11 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   __shared__ int s_wide;                         // some unit's widening overflowed
   __shared__ int s_nseg;
   __shared__ int s_lovf;
-  __shared__ long long s_lo;                     // the current block: first rotation ...
-  __shared__ int s_nb;                           // ... and count (-1: done)
+  __shared__ long long s_rl[kMaxBlockRot];       // the current block's rotations ...
+  __shared__ int s_nb;                           // ... their count (-1: done) ...
+  __shared__ long long s_rc;                     // ... its centre rotation ...
+  __shared__ int s_tc;                           // ... and the centre's place in s_rl (-1: none)
+  __shared__ long long s_qa[6];                  // block queue: first a-part, a-parts, parts per axis, blocks
   __shared__ unsigned long long s_wst[32][2];    // per-warp (pairs, votes) statistics
   if (tid < 64) s_wst[tid >> 1][tid & 1] = 0;
   if (tid == 0) {
@@ -884,26 +887,57 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   const int gmax = max(1, min(min(p.nyt, p.unit_cap / 4), p.unit_cap - p.nxt - 1));
   const bool masks = nxc > 1 && nxc <= 32;
 
-  // blocks: runs of blk_L rotations of a grid row, from a global queue (the
-  // first one static); thread 0 keeps the claim state, the rest read the
-  // block from shared memory (no 64-bit loop state in every thread)
+  // blocks: boxes of blk_s[0] x blk_s[1] x blk_s[2] neighbouring grid
+  // rotations (balanced parts of the Euler-index axes), restricted to
+  // [r_begin, r_end), from a global queue (the first one static); thread 0
+  // keeps the claim state, the rest read the block from shared memory (no
+  // 64-bit loop state in every thread)
   long long bclaim = blockIdx.x;
+  if (tid == 0) {  // the block queue's geometry: parts per axis, the a-parts that meet the range
+    const int64_t n = 2 * p.rot.k + 1, n2 = n * n, pa = (n + p.blk_s[0] - 1) / p.blk_s[0];
+    const int64_t a_lo = p.r_begin / n2, a_hi = (p.r_begin + p.r_count - 1) / n2;
+    int64_t q0 = pa, q1 = -1;
+    for (int64_t q = 0; q < pa; ++q)
+      if ((q + 1) * n / pa > a_lo && q * n / pa <= a_hi) { q0 = min(q0, q); q1 = q; }
+    s_qa[0] = q0;
+    s_qa[1] = q1 - q0 + 1;
+    s_qa[2] = pa;
+    s_qa[3] = (n + p.blk_s[1] - 1) / p.blk_s[1];
+    s_qa[4] = (n + p.blk_s[2] - 1) / p.blk_s[2];
+    s_qa[5] = s_qa[1] * s_qa[3] * s_qa[4];  // blocks
+  }
   for (;;) {
     if (tid == 0) {
-      const int64_t BL = p.blk_L, side = 2 * p.rot.k + 1, r_end = p.r_begin + p.r_count;
-      const int64_t row0 = p.r_begin / side, bpr = (side + BL - 1) / BL;
-      const int64_t nblk = ((r_end - 1) / side - row0 + 1) * bpr;
+      // the next non-empty block: the box's rotations inside [r_begin, r_end),
+      // its centre and the centre's place among them (-1: outside the range);
+      // per-axis indices in 32 bits (sides < 2^16), flat rotations in 64
+      const int n = 2 * (int)p.rot.k + 1, pa = s_qa[2], pb = s_qa[3], pc = s_qa[4];
+      const long long r_end = p.r_begin + p.r_count;
       int nb = -1;
-      int64_t lo = 0;
-      while (bclaim < nblk) {
-        // a row's bpr blocks are balanced: sizes differ by at most one
-        const int64_t row = row0 + bclaim / bpr, k = bclaim % bpr;
-        lo = max(row * side + k * side / bpr, p.r_begin);
-        const int64_t hi = min(row * side + (k + 1) * side / bpr, r_end);
+      while (bclaim < s_qa[5]) {
+        const int qa = (int)s_qa[0] + (int)(bclaim / (pb * pc)), qb = (int)((bclaim / pc) % pb),
+                  qc = (int)(bclaim % pc);
         bclaim = (long long)gridDim.x + (long long)atomicAdd(&p.stats[3], 1ull);
-        if (hi > lo) { nb = (int)(hi - lo); break; }
+        const int a0 = qa * n / pa, a1 = (qa + 1) * n / pa, b0 = qb * n / pb, b1 = (qb + 1) * n / pb,
+                  c0 = qc * n / pc, c1 = (qc + 1) * n / pc;
+        const long long rcen = ((long long)((a0 + a1 - 1) / 2) * n + (b0 + b1 - 1) / 2) * n + (c0 + c1 - 1) / 2;
+        int cnt = 0, tc = -1;
+        for (int a = a0; a < a1; ++a)
+          for (int b = b0; b < b1; ++b) {
+            const long long r0 = ((long long)a * n + b) * n;
+            for (int c = c0; c < c1; ++c)
+              if (r0 + c >= p.r_begin && r0 + c < r_end) {
+                if (r0 + c == rcen) tc = cnt;
+                s_rl[cnt++] = r0 + c;
+              }
+          }
+        if (cnt > 0) {
+          nb = cnt;
+          s_rc = rcen;
+          s_tc = tc;
+          break;
+        }
       }
-      s_lo = lo;
       s_nb = nb;
       s_nseg = 0;
       s_lovf = 0;
@@ -913,10 +947,11 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
     const int nb = s_nb;
     if (nb < 0) break;
     {
-      const int rc = nb >> 1;
-      if (tid < 9 * nb) Rb[tid] = rotation_entry(p.rot, s_lo + tid / 9, tid % 9);
+      const int tc = s_tc;  // the centre's place in the block (-1: outside the range)
+      double* R = Rb + 9 * kMaxBlockRot;  // the centre rotation
+      if (tid < 9) R[tid] = rotation_entry(p.rot, s_rc, tid);
+      if (tid >= 32 && tid < 32 + 9 * nb) Rb[tid - 32] = rotation_entry(p.rot, s_rl[(tid - 32) / 9], (tid - 32) % 9);
       __syncthreads();
-      const double* R = Rb + 9 * rc;
       // ---- A at the centre rotation: fixed-point points, and per unit the
       //      bound on its points' motion over the block's rotations,
       //      |(R_t - Rc) x|_k <= sum_l |R_t,kl - Rc,kl| max_unit |x_l|
@@ -1083,14 +1118,15 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
       if (!room && lane == 0) s_lovf = 1;
       __syncthreads();
       if (s_lovf) {  // left to vote_kernel
-        if (tid < nb) p.redo[atomicAdd(p.redo_n, 1ull)] = s_lo + tid;
+        if (tid < nb) p.redo[atomicAdd(p.redo_n, 1ull)] = s_rl[tid];
       } else {
         const int nseg = s_nseg;
         if (lane == 0) s_wst[warp][0] += (unsigned long long)wcount * (unsigned long long)nb;
         for (int t0 = 0; t0 < nb; ++t0) {
-          const int t = t0 == 0 ? rc : (t0 <= rc ? t0 - 1 : t0);  // the centre first: P holds it
+          // the centre first when it is in the block: P holds it
+          const int t = tc < 0 ? t0 : (t0 == 0 ? tc : (t0 <= tc ? t0 - 1 : t0));
           const double* Rt = Rb + 9 * t;
-          if (t0 > 0) {
+          if (t != tc) {
             for (int i = tid; i < p.n; i += nthreads) {
               const double x0 = p.xs[3 * i], x1 = p.xs[3 * i + 1], x2 = p.xs[3 * i + 2];
               sts_v4(P_sh + 16u * (unsigned)i,
@@ -1206,7 +1242,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
               bties += __shfl_xor_sync(0xffffffffu, bties, o);
             }
             if (lane == 0) {
-              const int64_t ro = s_lo + t - p.r_begin;
+              const int64_t ro = s_rl[t] - p.r_begin;
               p.counts[ro] = M;
               p.lins[ro] = M > 0 ? blin : -1;
               p.ties[ro] = M > 0 ? bties : 0;
@@ -1233,7 +1269,7 @@ size_t vote_smem_bytes(const VoteParams& p, bool hsmem, bool psmem, int threads)
   size_t b = 0;
   if (hsmem) b += (size_t)p.hist_words * 4;
   if (psmem) b += (size_t)p.n_pad * 16;
-  b += (size_t)(p.nxt + (p.nxt + 31) / 32) * 32 + (size_t)p.nxt * 16 + kMaxBlockRot * 9 * 8 + 4 * 32 * 4 +
+  b += (size_t)(p.nxt + (p.nxt + 31) / 32) * 32 + (size_t)p.nxt * 16 + kRotAreaBytes + 4 * 32 * 4 +
        (size_t)p.unit_cap * 4;  // (unit boxes, chunk boxes, the block kernel's per-unit widening, ...)
   b += (size_t)(threads / 32) * kRare * 8;
   b += (size_t)(threads / 32) * 32 * 16;  // per-warp staged sources

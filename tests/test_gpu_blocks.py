@@ -25,9 +25,9 @@ def _plan_modes(x, y, b, ilo, dims, k, step, center=None, r_begin=0, r_count=Non
     g = _native.make_grid(k, c, s, center)
     n = (2 * k + 1) ** 3 if r_count is None else r_count
     with _native.Plan(x, y, b, ilo, dims) as plan:
-        plan.set_block_rotations(0)
+        plan.set_blocks(0)
         ref = plan.mode_grid(g, r_begin, n)
-        plan.set_block_rotations(L, cap)
+        plan.set_blocks(L, cap)
         got = plan.mode_grid(g, r_begin, n)
     return ref, got
 
@@ -47,16 +47,16 @@ def test_blocks_equal_per_rotation_kernel_full_grid(name, Ls):
     g = _native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot)
     R = cfg.rotation_count
     with _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims) as plan:
-        plan.set_block_rotations(0)
+        plan.set_blocks(0)
         ref = plan.mode_grid(g, 0, R)
         for L in Ls:
-            plan.set_block_rotations(L)
+            plan.set_blocks(L)
             assert _same(ref, plan.mode_grid(g, 0, R)), L
         # ranges that start and end inside grid rows, and single rotations
         for r0, n in ((7, 50), (R // 2 + 3, 1), (R - 40, 40), (2 * cfg.k_rot + 2, 1000)):
-            plan.set_block_rotations(0)
+            plan.set_blocks(0)
             a = plan.mode_grid(g, r0, n)
-            plan.set_block_rotations(5)
+            plan.set_blocks(5)
             assert _same(a, plan.mode_grid(g, r0, n)), (r0, n)
 
 
@@ -133,7 +133,7 @@ def test_dses_on_c4_uses_blocks_and_matches_per_rotation_kernel():
     with _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims) as plan:
         for L in (None, 0):
             if L is not None:
-                plan.set_block_rotations(L)
+                plan.set_blocks(L)
             r = plan.search(g, cfg.q, p.code, p.param, p.skip_refine)
             out.append({k: r[k] for k in ("winner_row", "winner_lin", "winner_count", "best_error", "mstar",
                                           "candidates_evaluated", "candidates_refined", "best_inliers",

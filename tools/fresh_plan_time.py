@@ -18,7 +18,7 @@ for s in range(4):
     g = _native.make_grid(cfg.k_rot, p.cos_tab, p.sin_tab, p.center_rot)
     with _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims) as plan:
         if L >= 0:
-            plan.set_block_rotations(L)
+            plan.set_blocks(L)
         if res:
             plan.reserve(cfg.rotation_count)
         ts = []
