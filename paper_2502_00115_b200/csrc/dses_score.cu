@@ -736,8 +736,12 @@ __global__ void exact_sum_kernel(const double* vals, int n, int64_t nsel_cap, do
     }
     double total = 0.0;
     int i0 = 0;
-    for (; i0 + 32 <= n; i0 += 32) {  // full chunks: shuffles issued ahead of the adds
-      const double mine = v[i0 + lane];
+    // full chunks: the next chunk's load and the shuffles are issued ahead of
+    // the dependent adds (the serial chain is then DADD latency, not memory)
+    double next = n >= 32 ? v[lane] : 0.0;
+    for (; i0 + 32 <= n; i0 += 32) {
+      const double mine = next;
+      if (i0 + 64 <= n) next = v[i0 + 32 + lane];
 #pragma unroll
       for (int k0 = 0; k0 < 32; k0 += 8) {
         double t[8];

@@ -330,6 +330,7 @@ __device__ __forceinline__ void vote_slot(const VoteParams& p, const FastK& fk, 
 // rotation blocks whose candidate list overflowed (vote_blocks_kernel)
 template <bool HSMEM, bool PSMEM, bool RISK, bool REDO = false>
 __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams p) {
+  if (REDO && *p.redo_n == 0) return;  // (the usual case: no block overflowed)
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int nthreads = blockDim.x, nwarps = nthreads >> 5, warp = tid >> 5;
