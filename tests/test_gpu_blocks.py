@@ -19,6 +19,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _plan_modes(x, y, b, ilo, dims, k, step, center=None, r_begin=0, r_count=None, L=5, cap=0):
+    """(per-rotation kernel, block kernel) modes; the block kernel is run with
+    the shape L (an int n = a 1 x 1 x n run) and with 1 x 3 x 3 and 3 x 3 x 3
+    boxes, which must all agree."""
     from oracle import oracle as O
     from paper_2502_00115_b200 import _native
     c, s = O.trig_tables(k, step)
@@ -27,8 +30,12 @@ def _plan_modes(x, y, b, ilo, dims, k, step, center=None, r_begin=0, r_count=Non
     with _native.Plan(x, y, b, ilo, dims) as plan:
         plan.set_blocks(0)
         ref = plan.mode_grid(g, r_begin, n)
-        plan.set_blocks(L, cap)
-        got = plan.mode_grid(g, r_begin, n)
+        got = None
+        for shape in (L, (1, 3, 3), (3, 3, 3)):
+            plan.set_blocks(shape, cap)
+            out = plan.mode_grid(g, r_begin, n)
+            assert got is None or _same(got, out), shape
+            got = out
     return ref, got
 
 
@@ -36,7 +43,8 @@ def _same(a, b):
     return all(np.array_equal(u, v) for u, v in zip(a, b))
 
 
-@pytest.mark.parametrize("name,Ls", [("c4", (1, 3, 5, 8)), ("c2", (1, 3, 5))])
+@pytest.mark.parametrize("name,Ls", [("c4", (1, 7, (1, 3, 3), (2, 3, 3), (3, 3, 3))),
+                                     ("c2", (1, 3, (1, 3, 3)))])
 def test_blocks_equal_per_rotation_kernel_full_grid(name, Ls):
     import bench
     from paper_2502_00115_b200 import _native
@@ -56,8 +64,9 @@ def test_blocks_equal_per_rotation_kernel_full_grid(name, Ls):
         for r0, n in ((7, 50), (R // 2 + 3, 1), (R - 40, 40), (2 * cfg.k_rot + 2, 1000)):
             plan.set_blocks(0)
             a = plan.mode_grid(g, r0, n)
-            plan.set_blocks(5)
-            assert _same(a, plan.mode_grid(g, r0, n)), (r0, n)
+            for shape in ((1, 1, 5), (1, 3, 3), (3, 3, 3)):
+                plan.set_blocks(shape)
+                assert _same(a, plan.mode_grid(g, r0, n)), (r0, n, shape)
 
 
 def test_blocks_small_rows_and_large_steps_match_oracle():
@@ -73,6 +82,21 @@ def test_blocks_small_rows_and_large_steps_match_oracle():
         assert _same(ref, got), k
         oc, ol, ot = O.mode_batch(x, y, b, ilo, dims, grid=(k, step, None))
         assert np.array_equal(got[0], oc) and np.array_equal(got[1], ol) and np.array_equal(got[2], ot)
+
+
+def test_blocks_with_huge_steps_fall_back_to_per_rotation_kernel():
+    # 60-degree steps: the motion bound exceeds the block kernel's 2^27-unit
+    # widening limit, so every block goes to the per-rotation kernel
+    from oracle import oracle as O
+    rng = np.random.default_rng(41)
+    x = rng.normal(size=(200, 3)) * 0.5
+    y = rng.normal(size=(300, 3)) * 0.5
+    b, ilo, dims = 0.05, np.full(3, -3), np.full(3, 7)
+    k, step = 1, math.radians(60)
+    ref, got = _plan_modes(x, y, b, ilo, dims, k, step, L=(1, 3, 3))
+    assert _same(ref, got)
+    oc, ol, ot = O.mode_batch(x, y, b, ilo, dims, grid=(k, step, None))
+    assert np.array_equal(got[0], oc) and np.array_equal(got[1], ol) and np.array_equal(got[2], ot)
 
 
 def test_blocks_dedup_components_and_exact_path_match_oracle():
