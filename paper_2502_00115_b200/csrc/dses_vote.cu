@@ -1148,6 +1148,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           }
           // (the next segment's entry is loaded one iteration ahead: the list
           // comes from L2)
+          const uint32_t dummy_sh = g_dummy_sh + 4u * (unsigned)lane;  // this lane's sink word
           unsigned e_next = __ldcg(p.list + (slab + 32u * (unsigned)min(warp, max(nseg - 1, 0)) + (unsigned)lane));
           for (int sg = warp; sg < nseg; sg += nwarps) {
             const unsigned e = e_next;
@@ -1176,7 +1177,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
                 const int k2 = __shfl_up_sync(0xffffffffu, key, d);
                 ok &= !((e - e2 - 1u < (unsigned)off) & (k2 == key));
               }
-              const uint32_t a = ok ? hist_sh + ((lin + lin) & ~3u) : g_dummy_sh + 4u * (unsigned)lane;
+              const uint32_t a = ok ? hist_sh + ((lin + lin) & ~3u) : dummy_sh;
               reds_add(a, __funnelshift_l(0u, 1u, lin << 4));
             } else {
               // a near / split pair in the segment: its partners' bins are not
