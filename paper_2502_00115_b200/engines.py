@@ -195,25 +195,30 @@ def dses(source, reference, cfg: SearchConfig, device: int = 0) -> RegistrationR
 _BUILD_POOL = None
 
 
+_BUILD_AHEAD = 2  # plans under construction ahead of the running search
+
+
 def _build_pool():
-    """One persistent plan-construction thread: its upload stream and pinned
-    staging buffer (per host thread in the C ABI) are created once, not on
-    every dses_batch call."""
+    """Persistent plan-construction threads (one per plan built ahead): their
+    upload streams and pinned staging buffers (per host thread in the C ABI)
+    are created once, not on every dses_batch call."""
     global _BUILD_POOL
     if _BUILD_POOL is None:
         import concurrent.futures as cf
-        _BUILD_POOL = cf.ThreadPoolExecutor(max_workers=1, thread_name_prefix="dses-plan")
+        _BUILD_POOL = cf.ThreadPoolExecutor(max_workers=_BUILD_AHEAD, thread_name_prefix="dses-plan")
     return _BUILD_POOL
 
 
 def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     """dses over a batch of (source, reference) pairs (the registration loop of
     harness.run_batch, harness.py:145-162), pipelined: the host preparation
-    and plan construction of pair k+1 run on a worker thread (the C ABI
-    releases the GIL; plans upload on their own stream) while the GPU searches
-    pair k, and search k+1 is queued before the result of k is read, so the
-    GPU runs the searches back to back.  Results are identical to calling
-    dses() on each pair; errors are raised for the first failing pair."""
+    and plan construction of pairs k+1 and k+2 run on worker threads (the C
+    ABI releases the GIL; plans upload on their own streams) while the GPU
+    searches pair k, and search k+1 is queued before the result of k is read,
+    so the GPU runs the searches back to back (small registrations, c1, are
+    host-bound with one plan ahead).  Results are identical to calling dses()
+    on each pair; errors are raised for the first failing pair."""
+    from collections import deque
     pairs = list(zip(sources, references))
     out = []
     if not pairs:
@@ -224,16 +229,24 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     streams = [_native.Stream(device), _native.Stream(device)]  # alternate: the
     # vote of k+1 fills the SMs that k's last rotations and score stage leave idle
     ex = _build_pool()
-    fut = ex.submit(_build, pairs[0][0], pairs[0][1], cfg, device)  # not yet consumed
+    futs = deque()  # plans under construction, in pair order (not yet consumed)
+    nxt = 0
+
+    def top_up():
+        nonlocal nxt
+        while len(futs) < _BUILD_AHEAD and nxt < len(pairs):
+            futs.append(ex.submit(_build, pairs[nxt][0], pairs[nxt][1], cfg, device))
+            nxt += 1
+
+    top_up()
     try:
         for k in range(len(pairs) + 1):
             item, err = None, None
             if k < len(pairs):
                 try:
-                    cur, fut = fut, None
+                    cur = futs.popleft()
                     item = cur.result()
-                    if k + 1 < len(pairs):
-                        fut = ex.submit(_build, pairs[k + 1][0], pairs[k + 1][1], cfg, device)
+                    top_up()
                     _, prep, grid, plan = item
                     plan.search_async(grid, cfg.q, prep.code, prep.param, prep.skip_refine,
                                       stream=streams[k % 2].handle)
@@ -258,9 +271,9 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
             except Exception:
                 pass
             pending[3].close()
-        if fut is not None:  # a prefetched plan nobody will use
+        for f in futs:  # prefetched plans nobody will use
             try:
-                fut.result()[3].close()
+                f.result()[3].close()
             except Exception:
                 pass
         for st in streams:
