@@ -679,7 +679,8 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
     __syncthreads();
     int M = 0;
     for (int w = 0; w < nwarps; ++w) M = max(M, red[w]);
-    __syncthreads();  // red[] is reused below
+    // (no barrier: pass 2 writes red[32..95], red[0..31] is rewritten only
+    // after the next rotation's barriers)
     // ---- pass 2: re-zero, and locate the smallest flat bin at M and the
     //      number of bins at M (_kernels.py:159-170); words without M are skipped
     int best = M, blin = INT_MAX, bties = 0;
