@@ -1416,7 +1416,7 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
   CK(cudaEventRecord(P->ev[5], st));
   CK(cudaMemsetAsync(v.stats + 3, 0, sizeof(unsigned long long), st));  // rotation queue
   if (use_blocks(P, rs)) {
-    // rotation blocks: one candidate list per run of blk_L rotations; blocks
+    // rotation blocks: one candidate list per box of neighbouring rotations; blocks
     // whose list overflows the slab are re-run by the per-rotation kernel
     for (int k = 0; k < 3; ++k) v.blk_s[k] = P->blk_s[k];
     v.list_cap = P->blk_cap;

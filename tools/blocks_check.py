@@ -1,5 +1,5 @@
 """Rotation-block vote vs the per-rotation vote kernel on the bench pairs:
-identical per-rotation (count, bin, ties) and the vote time per block length.
+identical per-rotation (count, bin, ties) and the vote time per block shape.
     python tools/blocks_check.py c2 [L,L,...] [pairs]"""
 import sys
 sys.path.insert(0, '.')
