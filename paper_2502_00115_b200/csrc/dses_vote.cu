@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   int* s_next = red + 97;
   int* s_ovf = red + 98;
   const unsigned lanemask_lt = lanemask_lt_sr();
-  __shared__ __align__(16) unsigned kc[12];
+  __shared__ __align__(16) unsigned kc[16];
   __shared__ int s_wide;                         // some unit's widening overflowed
   __shared__ int s_nseg;
   __shared__ int s_lovf;
@@ -864,6 +864,9 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
     kc[9] = 0u - (1u << p.F);
     kc[10] = (uint32_t)__cvta_generic_to_shared(P);
     kc[11] = (1u << p.jbits) - 1u;
+    kc[12] = (unsigned)blockIdx.x * (unsigned)p.list_cap;  // this CTA's list slab (entry offset)
+    kc[13] = g_dummy_sh;                                    // the dummy vote words
+    kc[14] = kc[15] = 0u;
     g_exR = Rb;
     g_exP = P;
     g_exH = hist;
@@ -882,7 +885,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   const int nw4 = p.hist_words >> 2;
   for (int w = tid; w < nw4; w += nthreads) hist4[w] = make_uint4(0, 0, 0, 0);
 
-  const unsigned slab = (unsigned)blockIdx.x * (unsigned)p.list_cap;  // this CTA's list (entry offset)
+  const unsigned slab = kc[12];  // this CTA's list (entry offset)
   const uint32_t nseg_sh = (uint32_t)__cvta_generic_to_shared(&s_nseg);
   const unsigned jmask = kc[11];
   const unsigned pad_entry = (unsigned)p.m_pad;  // i = 0, j = the empty sentinel slot
@@ -1149,7 +1152,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           }
           // (the next segment's entry is loaded one iteration ahead: the list
           // comes from L2)
-          const uint32_t dummy_sh = g_dummy_sh + 4u * (unsigned)lane;  // this lane's sink word
+          const uint32_t dummy_sh = kc[13] + 4u * (unsigned)lane;  // this lane's sink word
           unsigned e_next = __ldcg(p.list + (slab + 32u * (unsigned)min(warp, max(nseg - 1, 0)) + (unsigned)lane));
           for (int sg = warp; sg < nseg; sg += nwarps) {
             const unsigned e = e_next;
