@@ -212,11 +212,11 @@ def _build_pool():
 def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     """dses over a batch of (source, reference) pairs (the registration loop of
     harness.run_batch, harness.py:145-162), pipelined: the host preparation
-    and plan construction of pairs k+1 and k+2 run on worker threads (the C
-    ABI releases the GIL; plans upload on their own streams) while the GPU
+    and plan construction of pair k+1 (and k+2 for small registrations, which
+    are host-bound with one plan ahead: c1) run on worker threads (the C ABI
+    releases the GIL; plans upload on their own streams) while the GPU
     searches pair k, and search k+1 is queued before the result of k is read,
-    so the GPU runs the searches back to back (small registrations, c1, are
-    host-bound with one plan ahead).  Results are identical to calling dses()
+    so the GPU runs the searches back to back.  Results are identical to calling dses()
     on each pair; errors are raised for the first failing pair."""
     from collections import deque
     pairs = list(zip(sources, references))
@@ -231,10 +231,14 @@ def dses_batch(sources, references, cfg: SearchConfig, device: int = 0) -> list:
     ex = _build_pool()
     futs = deque()  # plans under construction, in pair order (not yet consumed)
     nxt = 0
+    # small registrations are host-bound: two plans ahead; larger ones keep one
+    # (a second builder only contends with the main thread for the GIL)
+    work = cfg.rotation_count * len(pairs[0][0]) * len(pairs[0][1])
+    ahead = _BUILD_AHEAD if work < 4e9 else 1
 
     def top_up():
         nonlocal nxt
-        while len(futs) < _BUILD_AHEAD and nxt < len(pairs):
+        while len(futs) < ahead and nxt < len(pairs):
             futs.append(ex.submit(_build, pairs[nxt][0], pairs[nxt][1], cfg, device))
             nxt += 1
 
