@@ -17,6 +17,9 @@
 #include <thread>
 #include <cstring>
 #include <future>
+#include <functional>
+#include <deque>
+#include <condition_variable>
 #include <limits>
 #include <numeric>
 #include <string>
@@ -416,9 +419,63 @@ static void kd_split(KdPoint* a, int64_t lo, int64_t hi, std::vector<std::pair<i
   kd_split(a, lo + left, hi, tiles, tile, 0);
 }
 
+// Persistent helper threads for the host-side plan build (thread creation
+// costs about as much as the work it would take over for clouds of a few
+// thousand points).
+class HelperPool {
+ public:
+  explicit HelperPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~HelperPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  std::future<void> submit(std::function<void()> fn) {
+    auto task = std::make_shared<std::packaged_task<void()>>(std::move(fn));
+    std::future<void> f = task->get_future();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      q_.push_back([task] { (*task)(); });
+    }
+    cv_.notify_one();
+    return f;
+  }
+ private:
+  void loop() {
+    for (;;) {
+      std::function<void()> job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+        if (stop_ && q_.empty()) return;
+        job = std::move(q_.front());
+        q_.pop_front();
+      }
+      job();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::deque<std::function<void()>> q_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool stop_ = false;
+};
+
+static HelperPool& helper_pool() {
+  static HelperPool pool(3);
+  return pool;
+}
+
 // Recursive median split of pts[perm[lo..hi)] until tiles hold <= `tile`
 // points; splits at a multiple of `tile` so that all but the last tile of
-// each branch are full.  perm is reordered into tile order.
+// each branch are full.  perm is reordered into tile order.  Clouds of
+// >= 2048 points: the first two levels on this thread, the four subtrees on
+// it and three persistent helpers (disjoint ranges, tiles in order).
 void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
               std::vector<std::pair<int, int>>& tiles, int tile, int spawn = 0) {
   std::vector<KdPoint> a((size_t)(hi - lo));
@@ -428,7 +485,41 @@ void kd_tiles(const double* pts, int64_t lo, int64_t hi, std::vector<int>& perm,
     for (int d = 0; d < 3; ++d) k.c[d] = pts[3 * (int64_t)k.idx + d];
   }
   std::vector<std::pair<int, int>> t;
-  kd_split(a.data(), 0, hi - lo, t, tile, spawn);
+  if (spawn > 0 && hi - lo >= 2048) {
+    // two median levels here: up to four disjoint subranges
+    std::vector<std::pair<int64_t, int64_t>> r1, r2;
+    auto split = [&](int64_t l, int64_t h, std::vector<std::pair<int64_t, int64_t>>& out) {
+      const int64_t cnt = h - l;
+      if (cnt <= tile) { out.emplace_back(l, h); return; }
+      double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int64_t q = l; q < h; ++q)
+        for (int k = 0; k < 3; ++k) {
+          mn[k] = std::min(mn[k], a[q].c[k]);
+          mx[k] = std::max(mx[k], a[q].c[k]);
+        }
+      int axis = 0;
+      for (int k = 1; k < 3; ++k)
+        if (mx[k] - mn[k] > mx[axis] - mn[axis]) axis = k;
+      const int64_t left = (((cnt + tile - 1) / tile) / 2) * tile;
+      std::nth_element(a.begin() + l, a.begin() + l + left, a.begin() + h,
+                       [axis](const KdPoint& u, const KdPoint& v) {
+                         return u.c[axis] < v.c[axis] || (u.c[axis] == v.c[axis] && u.idx < v.idx);
+                       });
+      out.emplace_back(l, l + left);
+      out.emplace_back(l + left, h);
+    };
+    split(0, hi - lo, r1);
+    for (const auto& r : r1) split(r.first, r.second, r2);
+    std::vector<std::vector<std::pair<int, int>>> parts(r2.size());
+    std::vector<std::future<void>> fut;
+    for (size_t k = 1; k < r2.size(); ++k)
+      fut.push_back(helper_pool().submit([&, k] { kd_split(a.data(), r2[k].first, r2[k].second, parts[k], tile, 0); }));
+    kd_split(a.data(), r2[0].first, r2[0].second, parts[0], tile, 0);
+    for (auto& f : fut) f.get();
+    for (const auto& pt : parts) t.insert(t.end(), pt.begin(), pt.end());
+  } else {
+    kd_split(a.data(), 0, hi - lo, t, tile, 0);
+  }
   for (int64_t q = lo; q < hi; ++q) perm[q] = a[(size_t)(q - lo)].idx;
   for (const auto& e : t) tiles.emplace_back(e.first + (int)lo, e.second);
 }
