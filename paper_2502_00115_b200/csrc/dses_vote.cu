@@ -750,30 +750,34 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 }
 
 // ===========================================================================
-// Rotation-block kernel.  A block is a run of up to kMaxBlockRot consecutive
-// rotations of one grid row (the innermost Euler axis).  Every rotation R of
-// the block moves a source point by at most
-//     |(R - Rc) x|_k <= sum_l |R_kl - Rc_kl| * max_i |x_il|
-// from its position under the block's centre rotation Rc, so the pairs that
-// can vote for ANY rotation of the block are among the pairs inside the
-// window widened by that bound (dq fixed-point units per axis, with margin
-// for the two roundings) at Rc.  The kernel
+// Rotation-block kernel.  A block is a box of up to
+// kMaxBlockRot neighbouring grid rotations (blk_s[0] x blk_s[1] x blk_s[2]
+// along the Euler-index axes) inside the search's rotation range.  Every
+// rotation R_t of the block moves a source point x by at most
+//     |(R_t - Rc) x|_k <= sum_l |R_t,kl - Rc,kl| * max_unit |x_l|
+// from its position under the block's centre rotation Rc (per source unit,
+// in fixed-point units, + 3 for the two roundings), so the pairs that can
+// vote for ANY rotation of the block are among the pairs inside the window
+// widened by that bound at Rc.  The kernel
 //   1. builds that candidate-pair list ONCE per block: the per-rotation
 //      kernel's culling (unit boxes, group boxes, per-source tests) with the
-//      widened window, then one ballot per (source, group) and the candidate
+//      widened windows, then one ballot per (source, group) and the candidate
 //      lanes appended as entries i << jbits | j;
 //   2. votes it for each rotation of the block: lane = one entry (no idle
 //      lanes on out-of-window reference points), the same fixed-point bin
-//      and guard band as the per-rotation kernel, and the per-source dedup by
-//      __match_any_sync on (i, bin) within the 32-entry segment.
+//      and guard band as the per-rotation kernel, and the per-source dedup
+//      within the 32-entry segment: an entry compares its bin with the
+//      entries of its earlier component mates (shuffles over the `off`
+//      preceding lanes; mates of one source are contiguous in a run).
 // Exact dedup needs every pair that can share (i, bin) -- dedup partners, i.e.
 // points of one component -- in the same segment: a (source, group) run's
 // entries never straddle a segment boundary (the rest of the segment is
-// padded with the empty sentinel entry).  A segment holding a guard-band ("near") or
-// split-component pair sends all its partnered pairs through the exact
-// binary64 path (vote_exact: the reference's rule over the full near list).
-// A block whose list exceeds the CTA's slab is left to vote_kernel (redo
-// list).  Counts, bins and ties are those of the per-rotation kernel.
+// padded with the empty sentinel entry).  A segment holding a guard-band
+// ("near") or split-component pair sends all its partnered pairs through the
+// exact binary64 path (vote_exact: the reference's rule over the full near
+// list).  A block whose list exceeds the CTA's slab, or whose widening
+// exceeds 2^27 units, is left to vote_kernel (redo list).  Counts, bins and
+// ties are those of the per-rotation kernel.
 
 // The warp's open list segment is staged in shared memory (the warp's
 // exact-path list area, unused while a block's list is built) and written to
