@@ -1180,10 +1180,15 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
               const int key = cand ? (int)lin : -1;
               const int dmax = __reduce_max_sync(0xffffffffu, cand ? off : 0);
               bool ok = cand;
-              for (int d = 1; d <= dmax; ++d) {
-                const unsigned e2 = __shfl_up_sync(0xffffffffu, e, d);
-                const int k2 = __shfl_up_sync(0xffffffffu, key, d);
-                ok &= !((e - e2 - 1u < (unsigned)off) & (k2 == key));
+              if (dmax > 0) {  // (warp-uniform) most segments need one step, a few more
+                ok &= !((e - __shfl_up_sync(0xffffffffu, e, 1) - 1u < (unsigned)off) &
+                        (__shfl_up_sync(0xffffffffu, key, 1) == key));
+#pragma unroll 1
+                for (int d = 2; d <= dmax; ++d) {
+                  const unsigned e2 = __shfl_up_sync(0xffffffffu, e, d);
+                  const int k2 = __shfl_up_sync(0xffffffffu, key, d);
+                  ok &= !((e - e2 - 1u < (unsigned)off) & (k2 == key));
+                }
               }
               const uint32_t a = ok ? hist_sh + ((lin + lin) & ~3u) : dummy_sh;
               reds_add(a, __funnelshift_l(0u, 1u, lin << 4));
@@ -1217,8 +1222,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           }
           if (lane == 0) { red[warp] = (int)mx; s_wst[warp][1] += nv; }
           __syncthreads();
-          int M = 0;
-          for (int w = 0; w < nwarps; ++w) M = max(M, red[w]);
+          const int M = (int)__reduce_max_sync(0xffffffffu, lane < nwarps ? (unsigned)red[lane] : 0u);
           __syncthreads();
           int blin = INT_MAX, bties = 0;
           const unsigned MM = (unsigned)M * 0x10001u;
