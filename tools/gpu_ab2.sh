@@ -5,4 +5,3 @@ for c in ${CFGS:-c1 c2 c4 c2local}; do
   timeout 300 python tools/variant_time.py $c
   [ -f paper_2502_00115_b200/_lib/libdses_v1.so ] && timeout 300 python tools/variant_time.py $c $PWD/paper_2502_00115_b200/_lib/libdses_v1.so
 done
-for pu in ${PUS:-}; do DSES_PIECE_UNITS=$pu timeout 300 python tools/variant_time.py ${PUCFG:-c2}; done
