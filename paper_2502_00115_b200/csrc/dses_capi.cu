@@ -757,9 +757,8 @@ static std::shared_ptr<const RefTopo> build_ref_topo(const double* y, int64_t m,
   std::vector<int2>& range = T->range;
   RefTopo* PT = T.get();
   // ---- scoring layout (y sorted by axis 0, fp32 copy, uniform grid) on a
-  //      helper thread: independent of the vote layout built below
-  // (small clouds: deferred, i.e. run inline at get(); a thread costs more)
-  auto scoring = std::async(m >= 4096 ? std::launch::async : std::launch::deferred, [&]() {
+  //      persistent helper thread: independent of the vote layout built below
+  auto scoring = helper_pool().submit([&]() {
   // ---- scoring layout: x original order, y sorted by axis 0 (stable)
   trace("scoring layout");
   std::vector<int> sy(m);
