@@ -289,6 +289,7 @@ struct dses_plan {
   int vote_grid_cap = 0;                               // testing hook: 0 = one wave
   int blk_s[3] = {0, 0, 0};                            // rotation-block sides (0: per-rotation kernel)
   int blk_cap = kBlockListCap;                         // list entries per CTA (testing hook)
+  double lane_use = 0;                                 // estimated lane use of the per-rotation kernel
   DevBuf blist, redo;                                  // block kernel: candidate lists, redo rotations
   // device data
   DevBuf xs, ys, yq, near_off, near_idx, xt, yt;  // vote (tile order)
@@ -725,6 +726,7 @@ struct RefTopo {
   std::vector<int> noff, nidx;                 // exact-path near lists (tile order, j' < j)
   std::vector<double> ys;                      // the cloud in tile order
   double ymax = 0, ext = 0;                    // max |y| over the axes; largest axis extent
+  std::vector<double> gbox;                    // per reference group: lo xyz, hi xyz (world)
   mutable std::mutex dmu;
   mutable std::shared_ptr<DeviceRef> dev[64];  // device copies of the arrays above
   mutable std::mutex fmu;
@@ -942,6 +944,16 @@ static std::shared_ptr<const RefTopo> build_ref_topo(const double* y, int64_t m,
       T->ymax = std::max(T->ymax, std::fabs(y[3 * j + k]));
     }
     if (m > 0) T->ext = std::max(T->ext, hi - lo);
+  }
+  T->gbox.assign(6 * groups.size(), 0.0);
+  for (size_t g = 0; g < groups.size(); ++g) {
+    double* b = &T->gbox[6 * g];
+    for (int k = 0; k < 3; ++k) { b[k] = INFINITY; b[3 + k] = -INFINITY; }
+    for (int q = groups[g].start; q < groups[g].start + groups[g].count; ++q)
+      for (int k = 0; k < 3; ++k) {
+        b[k] = std::min(b[k], T->ys[3 * q + k]);
+        b[3 + k] = std::max(b[3 + k], T->ys[3 * q + k]);
+      }
   }
   scoring.get();
   return T;
@@ -1342,14 +1354,37 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
       return v;
     }();
     // Rotation blocks pay off when a source point's window holds few of a
-    // reference group's points (the per-rotation kernel then idles most lanes
-    // of its (source, group) steps): windows small against the reference
-    // cloud (c4: 36 mm in a 1.4 m cloud -> 1.7x).  With windows comparable to
-    // the cloud (c1-c3, c5) most lanes vote and the per-rotation kernel is
-    // faster (c2: 10.1 vs 18 ms with blocks).
-    double win = 0;
-    for (int k = 0; k < 3; ++k) win = std::max(win, (double)P->dims[k] * P->bin);
-    const bool small = win < kBlockWindowFrac * topo->ext;
+    // reference group's points: the per-rotation kernel then idles most lanes
+    // of its (source, group) steps.  Estimated lane use (identity rotation,
+    // up to 32 sampled sources): reference points in the window over 32 x the
+    // groups whose box meets it.  Measured (tools/block_crossover.py): c4
+    // (0.07) 3.5x faster with blocks, c2 at k_trans 2-10 (0.006-0.15)
+    // 2.5-1.5x, c4 at k_trans 8 (0.17) even, c2 (0.40) 0.77x.
+    const double blo[3] = {((double)P->ilo[0] - 0.5) * P->bin, ((double)P->ilo[1] - 0.5) * P->bin,
+                           ((double)P->ilo[2] - 0.5) * P->bin};
+    const double bhi[3] = {blo[0] + (double)P->dims[0] * P->bin, blo[1] + (double)P->dims[1] * P->bin,
+                           blo[2] + (double)P->dims[2] * P->bin};
+    const std::vector<GroupSpan>& gs = topo->groups;
+    int64_t nw = 0, gw = 0;
+    const int64_t ns = std::min<int64_t>(n, 32);
+    for (int64_t k = 0; k < ns; ++k) {
+      const double* xi = x + 3 * (k * n / std::max<int64_t>(ns, 1));
+      double wl[3], wh[3];
+      for (int a = 0; a < 3; ++a) { wl[a] = xi[a] + blo[a]; wh[a] = xi[a] + bhi[a]; }
+      for (size_t g = 0; g < gs.size(); ++g) {
+        const double* b = &topo->gbox[6 * g];
+        if (!(b[3] >= wl[0] && b[0] < wh[0] && b[4] >= wl[1] && b[1] < wh[1] && b[5] >= wl[2] && b[2] < wh[2]))
+          continue;
+        ++gw;
+        for (int q = gs[g].start; q < gs[g].start + gs[g].count; ++q) {
+          const double* yq = &topo->ys[3 * q];
+          nw += (yq[0] >= wl[0]) & (yq[0] < wh[0]) & (yq[1] >= wl[1]) & (yq[1] < wh[1]) & (yq[2] >= wl[2]) &
+                (yq[2] < wh[2]);
+        }
+      }
+    }
+    P->lane_use = (double)nw / (32.0 * (double)std::max<int64_t>(gw, 1));
+    const bool small = P->lane_use < kBlockLaneUseMax;
     for (int k = 0; k < 3; ++k) P->blk_s[k] = small ? kDefaultBlockShape[k] : 0;
     if (env_shape[0] >= 0 && set_block_shape(P, env_shape.data()) != DSES_OK) {
       for (int k = 0; k < 3; ++k) P->blk_s[k] = 0;

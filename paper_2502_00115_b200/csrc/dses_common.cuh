@@ -47,7 +47,7 @@ constexpr int kMaxBlockRot = 32;  // rotations per block (the block kernel's R a
 // shared-memory bytes of the rotation-matrix area (the block's rotations and
 // its centre), a multiple of 16 so that the int4 areas after it stay aligned
 constexpr int kRotAreaBytes = ((kMaxBlockRot + 1) * 9 * 8 + 15) / 16 * 16;
-constexpr double kBlockWindowFrac = 0.15;  // blocks when the window is below this part of the cloud
+constexpr double kBlockLaneUseMax = 0.2;   // blocks when the per-rotation kernel would use fewer lanes
 constexpr int kDefaultBlockShape[3] = {1, 3, 3};  // rotations per block along the Euler-index axes
 constexpr int kBlockListCap = 1 << 17;  // candidate-list entries per CTA (512 KiB)
 constexpr int kRiskBits = 10;     // fraction buckets per axis of the guard-band risk bitmaps
