@@ -111,8 +111,9 @@ int dses_plan_set_vote_grid(dses_plan* plan, int64_t ctas);
 /* Rotation blocks: boxes of shape[0] x shape[1] x shape[2]
  * neighbouring grid rotations (along the three Euler-index axes, at most 32
  * rotations) share one candidate-pair list; 0,0,0 = the per-rotation vote
- * kernel.  Default: 1,3,3 when the translation window is small against the
- * reference cloud, else 0,0,0 (environment DSES_BLOCK_SHAPE="a,b,c"
+ * kernel.  Default: 1,3,3 when few reference points of a group fall in a
+ * source point's window (estimated lane use of the per-rotation kernel below
+ * 0.2), else 0,0,0 (environment DSES_BLOCK_SHAPE="a,b,c"
  * overrides).  list_cap: list entries per CTA (0 = default 2^17; blocks whose
  * list overflows are re-run by the per-rotation kernel).  Results do not
  * depend on either. */
