@@ -6,6 +6,8 @@
 // the small host<->device scalar traffic between stages.  The Python layer
 // (paper_2502_00115_b200/engines.py) mirrors gridreg's API and exceptions on top.
 #include <algorithm>
+#include <new>
+#include <stdexcept>
 #include <array>
 #include <atomic>
 #include <chrono>
@@ -1645,7 +1647,14 @@ extern "C" int dses_plan_create(int device, const double* x, int64_t n, const do
   P->rec_host = rec_take();
   if (!P->rec_host) { dses_plan_destroy(P); return fail(DSES_E_NOMEM, "pinned record"); }
   TrafficScope ts_(P);
-  const int rc = build_plan(P, x, y);
+  int rc;
+  try {  // no C++ exception may cross the C ABI (host allocations of the layout)
+    rc = build_plan(P, x, y);
+  } catch (const std::bad_alloc&) {
+    rc = fail(DSES_E_NOMEM, "host memory exhausted building the plan");
+  } catch (const std::exception& e) {
+    rc = fail(DSES_E_CUDA, "plan construction failed: %s", e.what());
+  }
   if (rc != DSES_OK) { dses_plan_destroy(P); return rc; }
   *out = P;
   return DSES_OK;
