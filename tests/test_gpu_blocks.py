@@ -167,3 +167,32 @@ def test_dses_on_c4_uses_blocks_and_matches_per_rotation_kernel():
     # the block kernel's statistic is list entries per rotation, well below
     # the per-rotation kernel's evaluated pairs
     assert pairs[0] < pairs[1] / 2
+
+
+@pytest.mark.parametrize("kind,param", [("trunc_l1", 0.02), ("l1", None), ("inliers", 0.01),
+                                        ("l2", None)])
+def test_dses_small_window_every_metric_matches_oracle(kind, param):
+    """The full registration on the default path for a small window (the
+    rotation-block kernel) against the oracle dses, for each scoring path."""
+    import paper_2502_00115_b200 as api
+    from oracle import oracle as O
+    from paper_2502_00115_b200 import _native
+    from paper_2502_00115_b200.engines import prepare
+    from paper_2502_00115_b200.synth import CONFIGS, make_pair
+    x, y, _ = make_pair(CONFIGS["c2"]["spec"], 23)
+    cfg = api.SearchConfig(k_rot=3, rot_step=math.radians(3), k_trans=3, trans_bin=0.01,
+                           metric=api.ErrorMetric.from_name(kind, param) if param is not None
+                           else api.ErrorMetric(kind))
+    p = prepare(x, y, cfg)
+    with _native.Plan(p.x, p.y, cfg.trans_bin, p.ilo, p.dims) as plan:
+        assert plan.blocks()[0] > 0, "a small window takes the rotation-block kernel"
+    res = api.dses(x, y, cfg)
+    m = cfg.metric
+    ref = O.dses(x, y, k_rot=cfg.k_rot, rot_step=cfg.rot_step, k_trans=cfg.k_trans,
+                 trans_bin=cfg.trans_bin, q=cfg.q, metric=(m.kind, m.param))
+    assert tuple(res.best.grid_coords) == tuple(ref["grid_coords"])
+    assert np.array_equal(res.best.translation, ref["translation"])
+    assert math.isclose(res.best_error, ref["best_error"], rel_tol=1e-9, abs_tol=1e-12)
+    assert res.candidates_evaluated == ref["candidates_evaluated"]
+    assert res.candidates_refined == ref["candidates_refined"]
+    assert res.best_inliers == ref["best_inliers"]
