@@ -49,7 +49,10 @@ constexpr int kMaxBlockRot = 32;  // rotations per block (the block kernel's R a
 constexpr int kRotAreaBytes = ((kMaxBlockRot + 1) * 9 * 8 + 15) / 16 * 16;
 constexpr double kBlockLaneUseMax = 0.2;   // blocks when the per-rotation kernel would use fewer lanes
 constexpr int kDefaultBlockShape[3] = {1, 3, 3};  // rotations per block along the Euler-index axes
-constexpr int kBlockListCap = 1 << 17;  // candidate-list entries per CTA (512 KiB)
+#ifndef DSES_BLOCK_LIST_CAP
+#define DSES_BLOCK_LIST_CAP (1 << 17)
+#endif
+constexpr int kBlockListCap = DSES_BLOCK_LIST_CAP;  // candidate-list entries per CTA (2 MiB of 16-byte entries)
 constexpr int kRiskBits = 10;     // fraction buckets per axis of the guard-band risk bitmaps
 constexpr int kRiskWords = 3 * (1 << kRiskBits) / 32;  // words per group (3 axes)
 constexpr int kVoteThreads = 1024;

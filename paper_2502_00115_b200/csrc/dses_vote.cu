@@ -786,32 +786,30 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 // that does not fit the open segment's room closes it (the rest padded with
 // the empty sentinel entry).  Returns false once the CTA's slab is full.
 __device__ __forceinline__ bool flush_segment(const VoteParams& p, uint32_t buf_sh, int lane,
-                                              uint32_t nseg_sh, unsigned slab, unsigned pad_entry,
+                                              uint32_t nseg_sh, unsigned slab, const int4& pad_entry,
                                               int& fill) {
   if (fill == 0) return true;
-  if (lane >= fill) asm volatile("st.shared.u32 [%0], %1;" ::"r"(buf_sh + 4u * (unsigned)lane), "r"(pad_entry) : "memory");
+  if (lane >= fill) sts_v4(buf_sh + 16u * (unsigned)lane, pad_entry);
   __syncwarp();
-  unsigned e, s = 0;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(buf_sh + 4u * (unsigned)lane) : "memory");
+  const int4 e = lds_v4(buf_sh + 16u * (unsigned)lane);
+  unsigned s = 0;
   if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(s) : "r"(nseg_sh) : "memory");
   s = __shfl_sync(0xffffffffu, s, 0);
   fill = 0;
   if (32u * (s + 1u) > (unsigned)p.list_cap) return false;
-  __stcg(p.list + (slab + 32u * s + (unsigned)lane), e);
+  __stcg(reinterpret_cast<int4*>(p.list) + (slab + 32u * s + (unsigned)lane), e);
   return true;
 }
 
-__device__ __forceinline__ bool emit_entries(const VoteParams& p, unsigned m, unsigned entry, int lane,
+__device__ __forceinline__ bool emit_entries(const VoteParams& p, unsigned m, const int4& entry, int lane,
                                              unsigned lanemask_lt, uint32_t buf_sh, uint32_t nseg_sh,
-                                             unsigned slab, unsigned pad_entry, int& fill,
+                                             unsigned slab, const int4& pad_entry, int& fill,
                                              unsigned& wcount) {
   const int cnt = __popc(m);
   wcount += (unsigned)cnt;
   bool ok = true;
   if (cnt > 32 - fill) ok = flush_segment(p, buf_sh, lane, nseg_sh, slab, pad_entry, fill);  // warp-uniform
-  if ((m >> lane) & 1u)
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(buf_sh + 4u * (unsigned)(fill + __popc(m & lanemask_lt))),
-                 "r"(entry) : "memory");
+  if ((m >> lane) & 1u) sts_v4(buf_sh + 16u * (unsigned)(fill + __popc(m & lanemask_lt)), entry);
   fill += cnt;
   return ok;
 }
@@ -892,7 +890,10 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   const unsigned slab = kc[12];  // this CTA's list (entry offset)
   const uint32_t nseg_sh = (uint32_t)__cvta_generic_to_shared(&s_nseg);
   const unsigned jmask = kc[11];
-  const unsigned pad_entry = (unsigned)p.m_pad;  // i = 0, j = the empty sentinel slot
+  // list entries carry the reference point: (Yq.x, Yq.y, Yq.z, i << (jbits + 4) | j << 4 | o),
+  // o = the point's offset in its dedup component (15: split component, exact path)
+  const int ishift = p.jbits + 4;
+  const int4 pad_entry = make_int4(kNoRef, 0, 0, (int)((unsigned)p.m_pad << 4));  // never a candidate
   const int gmax = max(1, min(min(p.nyt, p.unit_cap / 4), p.unit_cap - p.nxt - 1));
   const bool masks = nxc > 1 && nxc <= 32;
 
@@ -1083,6 +1084,8 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           int4 Y = __ldg(&p.yq[j]);
           if (!valid) Y = make_int4(kNoRef, 0, 0, 0);
           const int4 dq = DQ[unit & 0xffffu];  // the unit's widening
+          const unsigned offs = (Y.w & kSplitFlag) ? 15u : (unsigned)min((Y.w >> kCompOffShift) & 15, 15);
+          const unsigned jw = ((unsigned)j << 4) | offs;
           const int y0 = (int)((unsigned)Y.x + (unsigned)dq.x), y1 = (int)((unsigned)Y.y + (unsigned)dq.y),
                     y2 = (int)((unsigned)Y.z + (unsigned)dq.z);
           const unsigned Wp0 = p.W0 + 2u * (unsigned)dq.x, Wp1 = p.W1 + 2u * (unsigned)dq.y,
@@ -1112,11 +1115,11 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
                             ((unsigned)y2 - (unsigned)P1.z < Wp2) & (t + 1 < nsrc);
             const unsigned m0 = __ballot_sync(0xffffffffu, c0), m1 = __ballot_sync(0xffffffffu, c1);
             if (m0)
-              room &= emit_entries(p, m0, ((unsigned)P0.w << p.jbits) | (unsigned)j, lane, lanemask_lt,
-                                   L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
+              room &= emit_entries(p, m0, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P0.w << ishift) | jw)), lane,
+                                   lanemask_lt, L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
             if (m1)
-              room &= emit_entries(p, m1, ((unsigned)P1.w << p.jbits) | (unsigned)j, lane, lanemask_lt,
-                                   L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
+              room &= emit_entries(p, m1, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P1.w << ishift) | jw)), lane,
+                                   lanemask_lt, L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
           }
         }
         __syncthreads();
@@ -1157,17 +1160,18 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           // (the next segment's entry is loaded one iteration ahead: the list
           // comes from L2)
           const uint32_t dummy_sh = kc[13] + 4u * (unsigned)lane;  // this lane's sink word
-          unsigned e_next = __ldcg(p.list + (slab + 32u * (unsigned)min(warp, max(nseg - 1, 0)) + (unsigned)lane));
+          const int4* list4 = reinterpret_cast<const int4*>(p.list);
+          int4 en_next = __ldcg(list4 + (slab + 32u * (unsigned)min(warp, max(nseg - 1, 0)) + (unsigned)lane));
           for (int sg = warp; sg < nseg; sg += nwarps) {
-            const unsigned e = e_next;
-            e_next = __ldcg(p.list + (slab + 32u * (unsigned)min(sg + nwarps, nseg - 1) + (unsigned)lane));
-            const int i = (int)(e >> p.jbits), j = (int)(e & jmask);
+            const int4 Y = en_next;  // the entry: the reference point and (i, j, o)
+            en_next = __ldcg(list4 + (slab + 32u * (unsigned)min(sg + nwarps, nseg - 1) + (unsigned)lane));
+            const unsigned ew = (unsigned)Y.w, e = ew >> 4;
+            const int i = (int)(ew >> ishift);
             const int4 Pi = lds_v4(P_sh + 16u * (unsigned)i);
-            const int4 Y = __ldg(&p.yq[j]);
             const unsigned u0 = (unsigned)(Y.x - Pi.x), u1 = (unsigned)(Y.y - Pi.y), u2 = (unsigned)(Y.z - Pi.z);
             const bool cand = (u0 < fk.W0) & (u1 < fk.W1) & (u2 < fk.W2);
             const unsigned q0 = u0 >> fk.F, q1 = u1 >> fk.F, q2 = u2 >> fk.F;
-            const unsigned gthr = (Y.w & kSplitFlag) ? 0xffffffffu : fk.gthr;
+            const unsigned gthr = (ew & 15u) == 15u ? 0xffffffffu : fk.gthr;
             const bool near = cand & (__vimin3_u32(u0 + q0 * fk.negP, u1 + q1 * fk.negP, u2 + q2 * fk.negP) < gthr);
             const unsigned lin = (q0 * fk.d1 + q1) * fk.d2 + q2;
             if (!__any_sync(0xffffffffu, near)) {
@@ -1176,16 +1180,16 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
               // one source: contiguous, the earlier ones at lane distance d <=
               // off (the point's offset in its component), entry e - d' with
               // 1 <= d' <= off
-              const int off = (Y.w >> kCompOffShift) & 15;
+              const int off = (int)(ew & 15u);
               const int key = cand ? (int)lin : -1;
               const int dmax = __reduce_max_sync(0xffffffffu, cand ? off : 0);
               bool ok = cand;
               if (dmax > 0) {  // (warp-uniform) most segments need one step, a few more
-                ok &= !((e - __shfl_up_sync(0xffffffffu, e, 1) - 1u < (unsigned)off) &
+                ok &= !((e - (__shfl_up_sync(0xffffffffu, ew, 1) >> 4) - 1u < (unsigned)off) &
                         (__shfl_up_sync(0xffffffffu, key, 1) == key));
 #pragma unroll 1
                 for (int d = 2; d <= dmax; ++d) {
-                  const unsigned e2 = __shfl_up_sync(0xffffffffu, e, d);
+                  const unsigned e2 = __shfl_up_sync(0xffffffffu, ew, d) >> 4;
                   const int k2 = __shfl_up_sync(0xffffffffu, key, d);
                   ok &= !((e - e2 - 1u < (unsigned)off) & (k2 == key));
                 }
@@ -1195,7 +1199,8 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
             } else {
               // a near / split pair in the segment: its partners' bins are not
               // known exactly -- every partnered candidate takes the exact path
-              const bool def = near | (cand & ((Y.w & kPartFlag) != 0));
+              const int j = (int)(e & jmask);
+              const bool def = near | (cand && (__ldg(&p.yq[j].w) & kPartFlag) != 0);
               vote_if<true>(hist, hist_sh, lin, cand & !def, (unsigned)p.nbins);
               const unsigned dm = __ballot_sync(0xffffffffu, def);
               if (dm) defer_pairs<true, true>(p, hist_sh, L, dm, def, i, j, lane, lanemask_lt);

@@ -1,5 +1,9 @@
 import sys, time
 sys.path.insert(0, '.')
+from paper_2502_00115_b200 import _native
+if len(sys.argv) > 3:
+    _native.LIB_PATH = sys.argv[3]
+_native.load(_native.LIB_PATH)
 import torch, bench
 from paper_2502_00115_b200 import engines, dses_batch
 name = sys.argv[1]; ahead = int(sys.argv[2])
