@@ -1348,6 +1348,7 @@ int build_plan(dses_plan* P, const double* x, const double* y) {
     int jb = 1;
     while (jb < 31 && ((int64_t)1 << jb) <= P->m_pad) ++jb;  // j <= m_pad (sentinel)
     v.jbits = (((uint64_t)std::max<int64_t>(n - 1, 0) << (jb + 4)) >> 32) == 0 ? jb : 0;  // (+ 4 offset bits)
+    v.ishift = v.jbits + 4;
     // DSES_BLOCK_SHAPE="a,b,c" overrides the default block shape ("0,0,0": off)
     static const std::array<int, 3> env_shape = [] {
       std::array<int, 3> v{-1, -1, -1};
@@ -1547,7 +1548,7 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
     // whose list overflows the slab are re-run by the per-rotation kernel
     for (int k = 0; k < 3; ++k) v.blk_s[k] = P->blk_s[k];
     v.list_cap = P->blk_cap;
-    CK(P->blist.ensure((size_t)grid * v.list_cap * 16, st));  // 16-byte entries
+    CK(P->blist.ensure(((size_t)grid * v.list_cap + kBlockListSlack) * 16, st));  // 16-byte entries
     CK(P->redo.ensure(8 * (size_t)(r_count + 1), st));
     v.list = P->blist.as<unsigned>();
     v.redo_n = P->redo.as<unsigned long long>();
@@ -2055,7 +2056,7 @@ static int reserve_search(dses_plan* P, int64_t nr, cudaStream_t st = 0) {
     if (!P->psmem) CK(P->p_g.ensure((size_t)grid * v.n_pad * 16, st));
   }
   if (blocks_enabled(P)) {
-    CK(P->blist.ensure((size_t)P->vote_grid * P->blk_cap * 16, st));  // rotation-block lists
+    CK(P->blist.ensure(((size_t)P->vote_grid * P->blk_cap + kBlockListSlack) * 16, st));  // rotation-block lists
     CK(P->redo.ensure(8 * (size_t)(nr + 1), st));
   }
   const int64_t cap = std::min<int64_t>(nr, kFusedRescoreCap);

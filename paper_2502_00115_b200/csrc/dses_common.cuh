@@ -53,6 +53,8 @@ constexpr int kDefaultBlockShape[3] = {1, 3, 3};  // rotations per block along t
 #define DSES_BLOCK_LIST_CAP (1 << 17)
 #endif
 constexpr int kBlockListCap = DSES_BLOCK_LIST_CAP;  // candidate-list entries per CTA (2 MiB of 16-byte entries)
+// the list vote prefetches one segment per warp past the last: slack after the slabs
+constexpr int kBlockListSlack = 32 * 32;
 constexpr int kRiskBits = 10;     // fraction buckets per axis of the guard-band risk bitmaps
 constexpr int kRiskWords = 3 * (1 << kRiskBits) / 32;  // words per group (3 axes)
 constexpr int kVoteThreads = 1024;
@@ -137,6 +139,7 @@ struct VoteParams {
   // widened by its points' maximal motion over the block
   int blk_s[3];               // sides along the three Euler-index axes (0: per-rotation kernel)
   int jbits;                  // list entry = i << jbits | j; j = m_pad is the empty sentinel slot
+  int ishift;                 // jbits + 4: the source index's place in a 16-byte entry's .w
   int list_cap;               // entries per CTA slab (multiple of 32)
   unsigned* list;             // per-CTA slabs
   long long* redo;            // rotations of blocks whose list overflowed ...

@@ -784,11 +784,11 @@ __global__ void __launch_bounds__(kVoteThreads, 1) vote_kernel(const VoteParams 
 // the CTA's slab, 32 entries at once, when full.  One (source, group) run
 // never straddles two segments (so neither does a dedup component): a run
 // that does not fit the open segment's room closes it (the rest padded with
-// the empty sentinel entry).  Returns false once the CTA's slab is full.
-__device__ __forceinline__ bool flush_segment(const VoteParams& p, uint32_t buf_sh, int lane,
-                                              uint32_t nseg_sh, unsigned slab, const int4& pad_entry,
-                                              int& fill) {
-  if (fill == 0) return true;
+// the empty sentinel entry).  A full slab sets the block's overflow flag.
+__device__ __forceinline__ void flush_segment(const VoteParams& p, uint32_t buf_sh, int lane,
+                                              uint32_t nseg_sh, uint32_t lovf_sh, unsigned slab,
+                                              const int4& pad_entry, int& fill) {
+  if (fill == 0) return;
   if (lane >= fill) sts_v4(buf_sh + 16u * (unsigned)lane, pad_entry);
   __syncwarp();
   const int4 e = lds_v4(buf_sh + 16u * (unsigned)lane);
@@ -796,22 +796,23 @@ __device__ __forceinline__ bool flush_segment(const VoteParams& p, uint32_t buf_
   if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(s) : "r"(nseg_sh) : "memory");
   s = __shfl_sync(0xffffffffu, s, 0);
   fill = 0;
-  if (32u * (s + 1u) > (unsigned)p.list_cap) return false;
+  if (32u * (s + 1u) > (unsigned)p.list_cap) {
+    if (lane == 0) asm volatile("st.shared.u32 [%0], 1;" ::"r"(lovf_sh) : "memory");
+    return;
+  }
   __stcg(reinterpret_cast<int4*>(p.list) + (slab + 32u * s + (unsigned)lane), e);
-  return true;
 }
 
-__device__ __forceinline__ bool emit_entries(const VoteParams& p, unsigned m, const int4& entry, int lane,
-                                             unsigned lanemask_lt, uint32_t buf_sh, uint32_t nseg_sh,
-                                             unsigned slab, const int4& pad_entry, int& fill,
-                                             unsigned& wcount) {
+// m = the warp's ballot of `mine`
+__device__ __forceinline__ void emit_entries(const VoteParams& p, unsigned m, bool mine, const int4& entry,
+                                             int lane, unsigned lanemask_lt, uint32_t buf_sh,
+                                             uint32_t nseg_sh, uint32_t lovf_sh, unsigned slab,
+                                             const int4& pad_entry, int& fill, unsigned& wcount) {
   const int cnt = __popc(m);
   wcount += (unsigned)cnt;
-  bool ok = true;
-  if (cnt > 32 - fill) ok = flush_segment(p, buf_sh, lane, nseg_sh, slab, pad_entry, fill);  // warp-uniform
-  if ((m >> lane) & 1u) sts_v4(buf_sh + 16u * (unsigned)(fill + __popc(m & lanemask_lt)), entry);
+  if (cnt > 32 - fill) flush_segment(p, buf_sh, lane, nseg_sh, lovf_sh, slab, pad_entry, fill);  // warp-uniform
+  if (mine) sts_v4(buf_sh + 16u * (unsigned)(fill + __popc(m & lanemask_lt)), entry);
   fill += cnt;
-  return ok;
 }
 
 #ifndef DSES_BLOCK_THREADS
@@ -820,7 +821,8 @@ __device__ __forceinline__ bool emit_entries(const VoteParams& p, unsigned m, co
 __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(const VoteParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = (int)lane_sr();
-  const int nthreads = blockDim.x, nwarps = nthreads >> 5, warp = tid >> 5;
+  constexpr int nthreads = DSES_BLOCK_THREADS, nwarps = nthreads >> 5;  // (launch_vote_blocks' launch)
+  const int warp = tid >> 5;
 
   // the per-rotation kernel's layout (hsmem, psmem)
   size_t off = 0;
@@ -889,10 +891,11 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
 
   const unsigned slab = kc[12];  // this CTA's list (entry offset)
   const uint32_t nseg_sh = (uint32_t)__cvta_generic_to_shared(&s_nseg);
+  const uint32_t lovf_sh = (uint32_t)__cvta_generic_to_shared(&s_lovf);
   const unsigned jmask = kc[11];
   // list entries carry the reference point: (Yq.x, Yq.y, Yq.z, i << (jbits + 4) | j << 4 | o),
   // o = the point's offset in its dedup component (15: split component, exact path)
-  const int ishift = p.jbits + 4;
+  const int ishift = p.ishift;
   const int4 pad_entry = make_int4(kNoRef, 0, 0, (int)((unsigned)p.m_pad << 4));  // never a candidate
   const int gmax = max(1, min(min(p.nyt, p.unit_cap / 4), p.unit_cap - p.nxt - 1));
   const bool masks = nxc > 1 && nxc <= 32;
@@ -1032,7 +1035,7 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
       //      against the widened unit boxes)
       int fill = 0;
       const bool wide = s_wide != 0;  // block-uniform
-      bool room = !wide;
+      if (wide && tid == 0) s_lovf = 1;  // (read after the build's barriers)
       unsigned wcount = 0;
       for (int b0 = 0, gnext = gmax; b0 < (wide ? 0 : p.nyt);) {
         const int b1 = min(p.nyt, b0 + gnext);
@@ -1115,19 +1118,18 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
                             ((unsigned)y2 - (unsigned)P1.z < Wp2) & (t + 1 < nsrc);
             const unsigned m0 = __ballot_sync(0xffffffffu, c0), m1 = __ballot_sync(0xffffffffu, c1);
             if (m0)
-              room &= emit_entries(p, m0, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P0.w << ishift) | jw)), lane,
-                                   lanemask_lt, L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
+              emit_entries(p, m0, c0, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P0.w << ishift) | jw)), lane,
+                           lanemask_lt, L.rare_sh, nseg_sh, lovf_sh, slab, pad_entry, fill, wcount);
             if (m1)
-              room &= emit_entries(p, m1, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P1.w << ishift) | jw)), lane,
-                                   lanemask_lt, L.rare_sh, nseg_sh, slab, pad_entry, fill, wcount);
+              emit_entries(p, m1, c1, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P1.w << ishift) | jw)), lane,
+                           lanemask_lt, L.rare_sh, nseg_sh, lovf_sh, slab, pad_entry, fill, wcount);
           }
         }
         __syncthreads();
         gnext = ((int)ovf == b0) ? 1 : gmax;
         b0 = (int)ovf;
       }
-      room &= flush_segment(p, L.rare_sh, lane, nseg_sh, slab, pad_entry, fill);
-      if (!room && lane == 0) s_lovf = 1;
+      flush_segment(p, L.rare_sh, lane, nseg_sh, lovf_sh, slab, pad_entry, fill);
       __syncthreads();
       if (s_lovf) {  // left to vote_kernel
         if (tid < nb) p.redo[atomicAdd(p.redo_n, 1ull)] = s_rl[tid];
@@ -1157,14 +1159,16 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
             fk.W0 = k0.x; fk.W1 = k0.y; fk.W2 = k0.z; fk.fmask = k0.w;
             fk.gthr = k1.x; fk.d1 = k1.y; fk.d2 = k1.z; fk.F = (int)k1.w; fk.negP = kc[9];
           }
-          // (the next segment's entry is loaded one iteration ahead: the list
-          // comes from L2)
           const uint32_t dummy_sh = kc[13] + 4u * (unsigned)lane;  // this lane's sink word
-          const int4* list4 = reinterpret_cast<const int4*>(p.list);
-          int4 en_next = __ldcg(list4 + (slab + 32u * (unsigned)min(warp, max(nseg - 1, 0)) + (unsigned)lane));
+          // (the next segment's entry is loaded one iteration ahead: the list
+          // comes from L2; one segment per warp past the list's end is read and
+          // unused -- the allocation has kBlockListSlack entries after the last slab)
+          const int4* qn = reinterpret_cast<const int4*>(p.list) + (slab + 32u * (unsigned)warp + (unsigned)lane);
+          int4 en_next = __ldcg(qn);
           for (int sg = warp; sg < nseg; sg += nwarps) {
             const int4 Y = en_next;  // the entry: the reference point and (i, j, o)
-            en_next = __ldcg(list4 + (slab + 32u * (unsigned)min(sg + nwarps, nseg - 1) + (unsigned)lane));
+            qn += 32 * nwarps;
+            en_next = __ldcg(qn);
             const unsigned ew = (unsigned)Y.w, e = ew >> 4;
             const int i = (int)(ew >> ishift);
             const int4 Pi = lds_v4(P_sh + 16u * (unsigned)i);
