@@ -185,13 +185,14 @@ struct DevBuf {
   bool borrowed = false;  // points into another buffer (an upload arena): never freed here
   // A growing buffer is freed and re-allocated on the stream that uses it, so
   // the free is ordered after the work already queued there on the old one.
-  cudaError_t ensure(size_t bytes, cudaStream_t st) {
+  // (grow = false: exactly `bytes`, for buffers sized once, e.g. the block lists)
+  cudaError_t ensure(size_t bytes, cudaStream_t st, bool grow = true) {
     if (bytes <= cap && p) return cudaSuccess;
     if (p && !borrowed) cudaFreeAsync(p, st);
     p = nullptr;
     cap = 0;
     borrowed = false;
-    size_t want = std::max<size_t>(bytes + bytes / 2, 256);
+    size_t want = std::max<size_t>(grow ? bytes + bytes / 2 : bytes, 256);
     cudaError_t e = cudaMallocAsync(&p, want, st);
     if (e == cudaSuccess) cap = want;
     return e;
@@ -1548,7 +1549,7 @@ int run_vote(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_count
     // whose list overflows the slab are re-run by the per-rotation kernel
     for (int k = 0; k < 3; ++k) v.blk_s[k] = P->blk_s[k];
     v.list_cap = P->blk_cap;
-    CK(P->blist.ensure(((size_t)grid * v.list_cap + kBlockListSlack) * 16, st));  // 16-byte entries
+    CK(P->blist.ensure(((size_t)grid * v.list_cap + kBlockListSlack) * 16, st, false));  // 16-byte entries
     CK(P->redo.ensure(8 * (size_t)(r_count + 1), st));
     v.list = P->blist.as<unsigned>();
     v.redo_n = P->redo.as<unsigned long long>();
@@ -2056,7 +2057,7 @@ static int reserve_search(dses_plan* P, int64_t nr, cudaStream_t st = 0) {
     if (!P->psmem) CK(P->p_g.ensure((size_t)grid * v.n_pad * 16, st));
   }
   if (blocks_enabled(P)) {
-    CK(P->blist.ensure(((size_t)P->vote_grid * P->blk_cap + kBlockListSlack) * 16, st));  // rotation-block lists
+    CK(P->blist.ensure(((size_t)P->vote_grid * P->blk_cap + kBlockListSlack) * 16, st, false));  // rotation-block lists
     CK(P->redo.ensure(8 * (size_t)(nr + 1), st));
   }
   const int64_t cap = std::min<int64_t>(nr, kFusedRescoreCap);
