@@ -893,8 +893,9 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
   const uint32_t nseg_sh = (uint32_t)__cvta_generic_to_shared(&s_nseg);
   const uint32_t lovf_sh = (uint32_t)__cvta_generic_to_shared(&s_lovf);
   const unsigned jmask = kc[11];
-  // list entries carry the reference point: (Yq.x, Yq.y, Yq.z, i << (jbits + 4) | j << 4 | o),
-  // o = the point's offset in its dedup component (15: split component, exact path)
+  // list entries carry the reference point: (Yq.x, Yq.y, Yq.z, i << (jbits + 4) | j << 4 | c),
+  // c = the number of earlier entries of the run in the point's dedup component
+  // (15: split component / offset >= 15, exact path)
   const int ishift = p.ishift;
   const int4 pad_entry = make_int4(kNoRef, 0, 0, (int)((unsigned)p.m_pad << 4));  // never a candidate
   const int gmax = max(1, min(min(p.nyt, p.unit_cap / 4), p.unit_cap - p.nxt - 1));
@@ -1087,8 +1088,12 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           int4 Y = __ldg(&p.yq[j]);
           if (!valid) Y = make_int4(kNoRef, 0, 0, 0);
           const int4 dq = DQ[unit & 0xffffu];  // the unit's widening
+          // the entry's low 4 bits: the number of earlier entries of the same
+          // run (source) in the point's dedup component -- the lanes it must
+          // compare bins with -- or 15 (split component / offset >= 15: exact)
           const unsigned offs = (Y.w & kSplitFlag) ? 15u : (unsigned)min((Y.w >> kCompOffShift) & 15, 15);
-          const unsigned jw = ((unsigned)j << 4) | offs;
+          const unsigned jw = ((unsigned)j << 4) | (offs == 15u ? 15u : 0u);
+          const unsigned cmask = offs == 15u ? 0u : lanemask_lt & (0xffffffffu << max(lane - (int)offs, 0));
           const int y0 = (int)((unsigned)Y.x + (unsigned)dq.x), y1 = (int)((unsigned)Y.y + (unsigned)dq.y),
                     y2 = (int)((unsigned)Y.z + (unsigned)dq.z);
           const unsigned Wp0 = p.W0 + 2u * (unsigned)dq.x, Wp1 = p.W1 + 2u * (unsigned)dq.y,
@@ -1118,10 +1123,12 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
                             ((unsigned)y2 - (unsigned)P1.z < Wp2) & (t + 1 < nsrc);
             const unsigned m0 = __ballot_sync(0xffffffffu, c0), m1 = __ballot_sync(0xffffffffu, c1);
             if (m0)
-              emit_entries(p, m0, c0, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P0.w << ishift) | jw)), lane,
+              emit_entries(p, m0, c0, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P0.w << ishift) | jw |
+                                                                     (unsigned)__popc(m0 & cmask))), lane,
                            lanemask_lt, L.rare_sh, nseg_sh, lovf_sh, slab, pad_entry, fill, wcount);
             if (m1)
-              emit_entries(p, m1, c1, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P1.w << ishift) | jw)), lane,
+              emit_entries(p, m1, c1, make_int4(Y.x, Y.y, Y.z, (int)(((unsigned)P1.w << ishift) | jw |
+                                                                     (unsigned)__popc(m1 & cmask))), lane,
                            lanemask_lt, L.rare_sh, nseg_sh, lovf_sh, slab, pad_entry, fill, wcount);
           }
         }
@@ -1181,22 +1188,16 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
             if (!__any_sync(0xffffffffu, near)) {
               // every candidate decided: a (source, bin) votes once, by its lowest
               // lane.  Lanes that can share it are entries of one component for
-              // one source: contiguous, the earlier ones at lane distance d <=
-              // off (the point's offset in its component), entry e - d' with
-              // 1 <= d' <= off
-              const int off = (int)(ew & 15u);
+              // one source, contiguous in the segment: the entry's `c` (its low
+              // 4 bits, set by the build) earlier lanes are exactly its mates
+              const int c = (int)(ew & 15u);
               const int key = cand ? (int)lin : -1;
-              const int dmax = __reduce_max_sync(0xffffffffu, cand ? off : 0);
+              const int dmax = __reduce_max_sync(0xffffffffu, cand ? c : 0);
               bool ok = cand;
               if (dmax > 0) {  // (warp-uniform) most segments need one step, a few more
-                ok &= !((e - (__shfl_up_sync(0xffffffffu, ew, 1) >> 4) - 1u < (unsigned)off) &
-                        (__shfl_up_sync(0xffffffffu, key, 1) == key));
+                ok &= !(__shfl_up_sync(0xffffffffu, key, 1) == key && c >= 1);
 #pragma unroll 1
-                for (int d = 2; d <= dmax; ++d) {
-                  const unsigned e2 = __shfl_up_sync(0xffffffffu, ew, d) >> 4;
-                  const int k2 = __shfl_up_sync(0xffffffffu, key, d);
-                  ok &= !((e - e2 - 1u < (unsigned)off) & (k2 == key));
-                }
+                for (int d = 2; d <= dmax; ++d) ok &= !(__shfl_up_sync(0xffffffffu, key, d) == key && c >= d);
               }
               const uint32_t a = ok ? hist_sh + ((lin + lin) & ~3u) : dummy_sh;
               reds_add(a, __funnelshift_l(0u, 1u, lin << 4));
