@@ -1501,9 +1501,9 @@ int run_sparse(dses_plan* P, const RotSource& rs, int64_t r_begin, int64_t r_cou
   return DSES_OK;
 }
 
-// Rotation-block kernel eligibility: grid rotations (blocks are runs of one
-// grid row), shared-memory histogram and points, fixed-point binning, and
-// list entries i << jbits | j in 32 bits.
+// Rotation-block kernel eligibility: grid rotations (blocks are boxes of the
+// grid), shared-memory histogram and points, fixed-point binning, and the
+// entry word i << (jbits + 4) | j << 4 | c in 32 bits (n * m_pad < 2^28).
 static bool blocks_enabled(const dses_plan* P) {
   return P->blk_s[0] > 0 && P->hsmem && P->psmem && P->F > 0 && P->vp.jbits > 0 && !P->sparse;
 }

@@ -138,7 +138,7 @@ struct VoteParams {
   // built at the block's centre rotation with each source unit's window
   // widened by its points' maximal motion over the block
   int blk_s[3];               // sides along the three Euler-index axes (0: per-rotation kernel)
-  int jbits;                  // list entry = i << jbits | j; j = m_pad is the empty sentinel slot
+  int jbits;                  // entry word = i << (jbits + 4) | j << 4 | c; j = m_pad: the empty sentinel
   int ishift;                 // jbits + 4: the source index's place in a 16-byte entry's .w
   int list_cap;               // entries per CTA slab (multiple of 32)
   unsigned* list;             // per-CTA slabs
