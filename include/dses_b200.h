@@ -114,9 +114,10 @@ int dses_plan_set_vote_grid(dses_plan* plan, int64_t ctas);
  * kernel.  Default: 1,3,3 when few reference points of a group fall in a
  * source point's window (estimated lane use of the per-rotation kernel below
  * 0.2), else 0,0,0 (environment DSES_BLOCK_SHAPE="a,b,c"
- * overrides).  list_cap: list entries per CTA (0 = default 2^17; blocks whose
- * list overflows are re-run by the per-rotation kernel).  Results do not
- * depend on either. */
+ * overrides); plans with n * m_pad >= 2^28 always take the per-rotation
+ * kernel.  list_cap: 16-byte list entries per CTA (0 = default 2^17, 2 MiB;
+ * blocks whose list overflows are re-run by the per-rotation kernel).
+ * Results do not depend on either. */
 int dses_plan_set_blocks(dses_plan* plan, const int64_t shape[3], int64_t list_cap);
 /* The block shape this plan's grid searches use (0,0,0: per-rotation kernel). */
 int dses_plan_blocks(const dses_plan* plan, int64_t shape[3]);
