@@ -1232,8 +1232,9 @@ __global__ void __launch_bounds__(DSES_BLOCK_THREADS, 1) vote_blocks_kernel(cons
           }
           if (lane == 0) { red[warp] = (int)mx; s_wst[warp][1] += nv; }
           __syncthreads();
+          // (no barrier after reading the maxima: pass 2 writes red[32..95], and
+          // red[0..31] is rewritten only after the next rotation's vote barrier)
           const int M = (int)__reduce_max_sync(0xffffffffu, lane < nwarps ? (unsigned)red[lane] : 0u);
-          __syncthreads();
           int blin = INT_MAX, bties = 0;
           const unsigned MM = (unsigned)M * 0x10001u;
           for (int w = tid; w < nw4; w += nthreads) {
