@@ -795,6 +795,7 @@ __device__ __forceinline__ void flush_segment(const VoteParams& p, uint32_t buf_
   unsigned s = 0;
   if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(s) : "r"(nseg_sh) : "memory");
   s = __shfl_sync(0xffffffffu, s, 0);
+  __syncwarp();  // every lane's read of the staging area before the next emit's writes
   fill = 0;
   if (32u * (s + 1u) > (unsigned)p.list_cap) {
     if (lane == 0) asm volatile("st.shared.u32 [%0], 1;" ::"r"(lovf_sh) : "memory");
