@@ -1,3 +1,5 @@
+"""dses_batch wall time against the number of plans built ahead (engines._BUILD_AHEAD):
+    python tools/batch_ahead_time.py c4 AHEAD [lib.so]"""
 import sys, time
 sys.path.insert(0, '.')
 from paper_2502_00115_b200 import _native

@@ -1,3 +1,4 @@
+"""c3 (753,571 rotations) search time, per-rotation vs rotation-block vote kernel."""
 import sys, time
 sys.path.insert(0,'.')
 import bench, torch

@@ -1,3 +1,4 @@
+"""One search of a bench pair, twice (stage times, stats): python tools/one_search.py c2"""
 import sys
 sys.path.insert(0, '.')
 import bench
